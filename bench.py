@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""bench.py -- assembled elements/s of the P1-tet momentum-RHS assembly on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json config 2): a 128^3 Kuhn box (12,582,912 tets,
+2,146,689 nodes), random:1 velocity (uniform [-1,1), default_rng(1)),
+PhysParams defaults, RCM node renumbering + Morton element order.  Under
+torchrun (N>1) every rank assembles its own 128^3 slab of a 128x128x(128N)
+box and the interface planes are summed over NCCL (weak scaling).
+
+One step = one full RHS assembly (zero/merge + element kernel) with inputs
+resident in HBM; L2 is flushed (256 MiB write) before every step, outside
+the CUDA-event-timed interval.  ``e2e`` repeats the step through the public
+host API (pinned host u -> H2D -> assembly -> D2H rhs) and times it by wall
+clock.  ``--impl reference`` times the reference algorithm's CPU port
+(oracle/, the threaded private driver of variants.py:573-596) on all host
+cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FLOP_PER_ELEM = 448  # reference RSP ledger, variants.py:207-217 (cli.py:182 convention)
+NOMINAL_FP64_TFLOPS = 37.2  # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cells", type=int, default=128, help="cells per side (per rank slab)")
+    ap.add_argument("--init", default="random:1")
+    ap.add_argument("--scatter", default="private-atomic")
+    ap.add_argument("--renumber", default="rcm")
+    ap.add_argument("--element-order", default="sfc")
+    ap.add_argument("--chunk-elems", type=int, default=512)
+    ap.add_argument("--chunk-nodes", type=int, default=1024)
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--permute", action="store_true", help="config 3: random node permutation")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, ValueError):
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
+        sm, smax, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if s > 500] or sm
+        return {
+            "sm_mhz": statistics.median(load) if load else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "power_w_max": max(pw) if pw else None,
+            "samples": len(sm),
+            "reasons": sorted(reasons),
+        }
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference algorithm's CPU port on all host cores
+# ---------------------------------------------------------------------------
+def run_reference(a) -> None:
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    c = a.cells
+    m = O.box_mesh(c, c, c)
+    u = O.velocity(m.coords, a.init)
+    T = O.default_threads()
+    E = m.n_elems
+    # bounded sample: whole mesh per step unless that would exceed ~150 s total
+    t0 = time.perf_counter()
+    O.assemble_rsp(m.coords, m.connectivity, u, n_threads=T)
+    first = time.perf_counter() - t0
+    total_steps = max(a.steps, 1) + max(a.warmup, 0)
+    sample_elems = E
+    if first * total_steps > 150.0:
+        sample_elems = max(int(E * 150.0 / (first * total_steps)), 6)
+    ids = np.arange(sample_elems, dtype=np.int64)
+    conn = np.ascontiguousarray(m.connectivity[:sample_elems])
+
+    def step():
+        return O.assemble_rsp(m.coords, conn, u, n_threads=T)
+
+    for _ in range(max(a.warmup, 0)):
+        step()
+    times = []
+    for _ in range(max(a.steps, 1)):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = sample_elems * len(times) / tot
+    del ids
+    sample = (f"{'full' if sample_elems == E else 'first %d of' % sample_elems} "
+              f"{c}^3 Kuhn box ({E} tets), {a.init}, C port of _rsp_kernels.assemble_elements "
+              f"with the variants.py private driver, {T} threads, per step")
+    line = {
+        "impl": "reference", "metric": "assembled elements/s", "value": value,
+        "unit": "elem/s", "n_gpus": ws, "steps": len(times), "warmup": a.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{c}^3 Kuhn box, {a.init}", "n_elems": E, "n_nodes": m.n_nodes},
+        "cpu_baseline": {"value": value, "unit": "elem/s", "cores": T, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "elem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def measured_hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6532.9, "MEASURED_PEAKS.json value at round start (file absent on this box)"
+
+
+def ncu_traffic(kernel_key: str, workload: str):
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        ent = d.get(workload, {}).get(kernel_key)
+        return None if ent is None else float(ent["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+def run_ours(a) -> None:
+    import torch
+
+    import paper_2403_08777_b200 as tb
+    from paper_2403_08777_b200 import _native as N
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = local
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P = tb.PhysParams()
+    cfg = tb.RunConfig(scatter=a.scatter, renumber=a.renumber, element_order=a.element_order,
+                       chunk_elems=a.chunk_elems, chunk_nodes=a.chunk_nodes, device=dev)
+    c = a.cells
+    t0 = time.perf_counter()
+    if ws > 1:
+        from paper_2403_08777_b200.distributed import SlabDomain
+        dom = SlabDomain((c, c, c * ws), rank, ws, cfg)
+        mesh, u = dom.mesh, dom.velocity(a.init)
+        asm = dom.assembler
+    else:
+        dom = None
+        mesh = tb.generate_box_mesh(c, c, c)
+        if a.permute:
+            mesh = tb.permute_nodes(mesh, np.random.default_rng(0).permutation(mesh.n_nodes))
+        u = tb.make_velocity(mesh, a.init)
+        asm = tb.Assembler(mesh, cfg)
+    prep_s = time.perf_counter() - t0
+    info = asm.info()
+    E, Nn = mesh.n_elems, mesh.n_nodes
+
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def one_step():
+        if dom is None:
+            return asm.run(P, stream=stream)
+        return dom.step(P, stream=stream)
+
+    # parity + CPU baseline (rank 0, N=1): the oracle as checker / baseline only
+    parity = None
+    cpu_baseline = None
+    if ws == 1 and not a.no_cpu_baseline:
+        from oracle import oracle as O
+        O.build()
+        T = O.default_threads()
+        rhs_gpu, _ = asm.assemble(u, P)
+        O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)  # warm-up
+        ts = []
+        ref = None
+        for _ in range(3):
+            t1 = time.perf_counter()
+            ref = O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)
+            ts.append(time.perf_counter() - t1)
+        med = statistics.median(ts)
+        cpu_baseline = {"value": E / med, "unit": "elem/s", "cores": T, "kind": "port",
+                        "sample": f"full {c}^3 mesh ({E} tets), {a.init}; C port of the reference "
+                                  f"numba kernel + private driver, 1 warm-up + median of 3"}
+        chk = O.compare(rhs_gpu, ref, mesh.coords, mesh.connectivity, u)
+        parity = {"reference_rel_diff": chk.rel_diff, "rel_l2": chk.rel_l2,
+                  "entry_rel": chk.entry_rel, "passed": bool(chk.passed)}
+
+    asm.set_velocity_host(u, stream=stream)
+    flush_buf = None if a.no_flush else torch.empty(64 * 1024 * 1024, dtype=torch.int32,
+                                                    device=f"cuda:{dev}")
+
+    def flush():
+        if flush_buf is not None:
+            flush_buf.fill_(1)
+
+    asm.profile(True)
+    for _ in range(max(a.warmup, 0)):
+        flush()
+        one_step()
+    torch.cuda.synchronize()
+    asm.profile_read()
+    fp64_tf, fp64_mhz = N.fp64_peak(dev, 100.0)
+
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.15)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    launches = 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for i in range(a.steps):
+        flush()
+        starts[i].record()
+        launches += one_step()
+        ends[i].record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    wall1 = time.perf_counter()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kern_ms = asm.profile_read()
+    total_ms = float(sum(step_ms))
+    if dist:
+        t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    units = E * ws * a.steps
+    value = units / (total_ms * 1e-3)
+
+    # end-to-end through the public host API (pinned host buffers)
+    e2e = None
+    if not a.no_e2e and dom is None:
+        pu = N.PinnedArray((Nn, 3))
+        pr = N.PinnedArray((Nn, 3))
+        pu.array[:] = u
+        ksteps = max(min(a.steps, 50), 3)
+        for _ in range(2):
+            asm.assemble_into(pu.array, P, pr.array, a.scatter)
+        torch.cuda.synchronize()
+        tot = 0.0
+        for _ in range(ksteps):
+            flush()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            asm.assemble_into(pu.array, P, pr.array, a.scatter)
+            tot += time.perf_counter() - t1
+        e2e = {"value": E * ksteps / tot, "unit": "elem/s", "h2d_bytes_per_step": 24 * Nn,
+               "d2h_bytes_per_step": 24 * Nn, "steps": ksteps,
+               "api": "Assembler.assemble_into (tal_assemble), wall clock"}
+        pu.free()
+        pr.free()
+    clocks = sampler.stop()
+    asm.profile(False)
+
+    kmean = float(np.mean(kern_ms)) if len(kern_ms) else float("nan")
+    workload = f"{c}^3 Kuhn box{' x%d slabs' % ws if ws > 1 else ''}, {a.init}"
+    tf = FLOP_PER_ELEM * E / (kmean * 1e-3) / 1e12
+    alg_bytes = 16 * E + 72 * Nn  # int32 conn + coords/u read + rhs write
+    hbm_peak, hbm_src = measured_hbm_peak()
+    kname = {"private": "k_assemble_private<true,true>",
+             "private-atomic": "k_assemble_private<true,false>",
+             "atomic": "k_assemble_atomic<true>", "colored": "k_assemble_colored<true> (all colours)"}[a.scatter]
+    traffic = ncu_traffic(kname, workload)
+    line = {
+        "metric": "assembled elements/s", "value": value, "unit": "elem/s", "n_gpus": ws,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated Kuhn box mesh, seeded velocity)",
+        "config": {"workload": workload, "n_elems": E, "n_nodes": Nn, "scatter": a.scatter,
+                   "renumber": a.renumber, "element_order": a.element_order,
+                   "chunk_elems": a.chunk_elems, "chunk_nodes": a.chunk_nodes,
+                   "permuted": bool(a.permute),
+                   "l2": "flushed (256 MiB write) before every step, outside the timed events"
+                         if flush_buf is not None else "not flushed",
+                   "parallelism": f"dp{ws} z-slabs" if ws > 1 else "single GPU"},
+        "roofline": {"bound": "fp64", "kernel": kname, "achieved": tf, "peak": fp64_tf,
+                     "unit": "TFLOP/s", "frac": tf / fp64_tf,
+                     "peak_source": "live DFMA probe (tal_fp64_peak) in this run; "
+                                    f"nominal {NOMINAL_FP64_TFLOPS}",
+                     "flop_per_elem": FLOP_PER_ELEM, "kernel_ms": kmean,
+                     "traffic": traffic,
+                     "hbm": {"achieved": alg_bytes / (kmean * 1e-3) / 1e9, "peak": hbm_peak,
+                             "unit": "GB/s", "frac": alg_bytes / (kmean * 1e-3) / 1e9 / hbm_peak,
+                             "alg_bytes_per_launch": alg_bytes, "peak_source": hbm_src}},
+        "e2e": e2e,
+        "cpu_baseline": cpu_baseline,
+        "parity": parity,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "prep": {"seconds": prep_s, "native_prep_seconds": info["prep_seconds"],
+                 "n_chunks": info["n_chunks"], "n_chunk_nodes": info["n_chunk_nodes"],
+                 "n_shared_nodes": info["n_shared_nodes"], "device_bytes": info["device_bytes"]},
+        "fp64_probe_mhz": fp64_mhz,
+        "wall_s_timed_region": wall1 - wall0,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    asm.close() if dom is None else dom.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,197 @@
+/*
+ * tal_b200.h -- C-ABI of the B200-native P1-tetrahedron momentum-RHS assembly.
+ *
+ * Drop-in boundary for the reference package tet-assembly-lab 0.1.0
+ * (/root/reference/pkg/src/tet_assembly_lab).  The reference has no native
+ * code: its hot path is the numba function
+ *     _rsp_kernels.assemble_elements(coords, conn, u, rho, mu, cvre, pmat,
+ *                                    ids, rhs)            (_rsp_kernels.py:20-21)
+ * called by the Python operator
+ *     variants.assemble_rsp(mesh, u, params, cfg) -> AssemblyResult
+ *                                                        (variants.py:553-616)
+ * This header is what that seam binds to instead (ctypes).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch types.  Host arrays are C-order:
+ *    coords (n_nodes,3) f64, conn (n_elems,4) int64, u/rhs (n_nodes,3) f64 --
+ *    exactly the reference Mesh / velocity layout (mesh.py:36-47,
+ *    kernel.py:194-200).
+ *  - Every function returns a status: TAL_OK (0) or a TAL_E* code.  The
+ *    message of the last failure on the calling thread is tal_last_error().
+ *    TAL_EINVAL maps to Python ValueError (the reference raises ValueError
+ *    for bad shapes / non-finite input / bad config), everything else to
+ *    RuntimeError.  No C++ exception crosses the ABI.
+ *  - A handle owns one CUDA device's copy of one mesh (device-resident,
+ *    renumbered, SoA FP64) plus the per-field buffers.  Calls on one handle
+ *    must be serialised by the caller; distinct handles are independent.
+ *  - There is NO CPU fallback: without a usable sm_100 device every compute
+ *    entry point fails with TAL_ECUDA.
+ */
+#ifndef TAL_B200_H
+#define TAL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TAL_ABI_VERSION 1
+
+/* status codes */
+#define TAL_OK 0
+#define TAL_EINVAL 1 /* bad argument / input          -> ValueError   */
+#define TAL_ECUDA 2  /* CUDA failure / no device      -> RuntimeError */
+#define TAL_ENOMEM 3 /* host or device allocation     -> MemoryError  */
+#define TAL_ESTATE 4 /* call order (e.g. no mesh yet) -> RuntimeError */
+
+/* scatter strategies (the reference RunConfig.scatter, variants.py:74-101,
+ * offers 'private' and 'colored'; the GPU adds two atomic forms) */
+#define TAL_SCATTER_PRIVATE 0        /* CTA-private smem sums, ordered merge: bitwise reproducible */
+#define TAL_SCATTER_COLORED 1        /* colour-by-colour plain read-modify-write: bitwise reproducible */
+#define TAL_SCATTER_ATOMIC 2         /* 12 FP64 REDs per element */
+#define TAL_SCATTER_PRIVATE_ATOMIC 3 /* CTA-private smem sums, FP64 RED per shared node */
+
+/* node renumbering applied at upload (inverted on every host read-back) */
+#define TAL_RENUMBER_NONE 0
+#define TAL_RENUMBER_RCM 1 /* reverse Cuthill-McKee on the node graph */
+#define TAL_RENUMBER_SFC 2 /* Morton (Z-order) of node coordinates */
+
+/* element order used to cut CTA chunks */
+#define TAL_EORDER_KEEP 0 /* as given */
+#define TAL_EORDER_NODE 1 /* by smallest (renumbered) node id */
+#define TAL_EORDER_SFC 2  /* Morton order of element centroids */
+
+typedef struct tal_handle tal_handle;
+
+typedef struct {
+    double rho;       /* PhysParams.rho       (kernel.py:36)   */
+    double mu;        /* PhysParams.mu        (kernel.py:37)   */
+    double c_vreman;  /* PhysParams.c_vreman  (kernel.py:38)   */
+    double pmat[16];  /* P^T P of the 4-point rule, row-major (variants.py:559) */
+} tal_params;
+
+typedef struct {
+    int renumber;        /* TAL_RENUMBER_*                              */
+    int element_order;   /* TAL_EORDER_*                                */
+    int chunk_elems;     /* max elements per CTA chunk (<= 1024)        */
+    int chunk_nodes;     /* max unique nodes per CTA chunk (<= 2048)    */
+    int validate;        /* 1: reject out-of-range ids / non-positive volume */
+    int build_colors;    /* 1: colour (greedy, element order) if colors==NULL */
+} tal_mesh_opts;
+
+typedef struct {
+    int64_t n_nodes, n_elems;
+    int64_t n_colors;        /* 0 if no colouring available              */
+    int64_t n_chunks;        /* CTA chunks of the private scatter        */
+    int64_t n_chunk_nodes;   /* sum over chunks of unique nodes          */
+    int64_t n_shared_nodes;  /* nodes touched by >1 chunk                */
+    int64_t device_bytes;    /* device memory held by the handle         */
+    double prep_seconds;     /* host preprocessing time of the upload    */
+} tal_mesh_info;
+
+typedef struct {
+    /* CUDA-event times in milliseconds of the last tal_assemble call */
+    double h2d_ms, pack_ms, kernel_ms, unpack_ms, d2h_ms, total_ms;
+    int64_t kernel_launches; /* kernels (of this library) launched by that call */
+} tal_timings;
+
+typedef struct {
+    /* device pointers in the handle's internal (renumbered) node order */
+    double *ux, *uy, *uz; /* velocity components, n_nodes each   */
+    double *rx, *ry, *rz; /* assembled RHS components            */
+    const int32_t *perm;  /* internal -> caller node id (NULL = identity) */
+    const int32_t *iperm; /* caller -> internal node id (NULL = identity) */
+} tal_buffers;
+
+/* ---- library / device ---------------------------------------------------- */
+const char *tal_last_error(void);
+int tal_abi_version(void);
+int tal_device_count(int *count);
+/* one tal_handle per (device, mesh) */
+int tal_create(int device, tal_handle **out);
+int tal_destroy(tal_handle *h);
+/* pinned host memory for copy-overlapped end-to-end use */
+int tal_host_alloc(int64_t bytes, void **out);
+int tal_host_free(void *p);
+
+/* ---- mesh ------------------------------------------------------------------ */
+/* Replaces the per-call coords/conn arguments of assemble_elements
+ * (_rsp_kernels.py:20-21) with a one-time upload.  colors may be NULL
+ * (mesh.py:43-47: Mesh.colors is optional). */
+int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn,
+                    int64_t n_nodes, int64_t n_elems, const int64_t *colors,
+                    const tal_mesh_opts *opts);
+int tal_mesh_info_get(tal_handle *h, tal_mesh_info *out);
+int tal_default_mesh_opts(tal_mesh_opts *out);
+
+/* ---- assembly ------------------------------------------------------------- */
+/* End-to-end drop-in for assemble_rsp's kernel loop (variants.py:572-615):
+ * host u (n_nodes,3) in caller numbering -> host rhs (n_nodes,3), overwritten.
+ * Synchronous.  t may be NULL. */
+int tal_assemble(tal_handle *h, const double *u, const tal_params *p,
+                 double *rhs, int scatter, tal_timings *t);
+
+/* Device-resident path (no host copies).  'stream' is a cudaStream_t (or 0).
+ * tal_set_velocity_*: caller-numbered AoS (n_nodes,3) -> internal SoA.
+ * tal_run: assemble internal u -> internal rhs (overwrites).  Asynchronous.
+ * tal_get_rhs_*: internal SoA -> caller-numbered AoS (n_nodes,3). */
+int tal_buffers_get(tal_handle *h, tal_buffers *out);
+int tal_set_velocity_host(tal_handle *h, const double *u, void *stream);
+int tal_set_velocity_device(tal_handle *h, const double *d_u, void *stream);
+int tal_run(tal_handle *h, const tal_params *p, int scatter, void *stream,
+            int64_t *kernel_launches);
+int tal_get_rhs_host(tal_handle *h, double *rhs, void *stream);
+int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream);
+int tal_synchronize(tal_handle *h, void *stream);
+
+/* Element-subset seam, signature-for-signature the numba kernel
+ * _rsp_kernels.assemble_elements (_rsp_kernels.py:20-21): assembles elements
+ * ids[0..k) and ADDS (+=) into the host rhs, as the numba loop does.  Runs
+ * on 'device' with a transient upload (no renumbering). */
+int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
+                          int64_t n_nodes, int64_t n_elems, const double *u,
+                          double rho, double mu, double cvre,
+                          const double *pmat, const int64_t *ids, int64_t k,
+                          double *rhs);
+
+/* ---- multi-GPU interface (domain decomposition) ----------------------------- */
+/* Gather rhs of internal node ids list[0..n) into a packed buffer d_out
+ * (n*3 doubles, component-interleaved) / add a packed buffer into rhs. */
+int tal_halo_pack(tal_handle *h, const int32_t *d_list, int64_t n, double *d_out, void *stream);
+int tal_halo_accumulate(tal_handle *h, const int32_t *d_list, int64_t n, const double *d_in, void *stream);
+/* caller node id -> internal node id (host arrays) */
+int tal_map_nodes(tal_handle *h, const int64_t *caller_ids, int64_t n, int32_t *internal_ids);
+
+/* ---- host-side mesh utilities (native; used by the Python Mesh type) ------- */
+/* Kuhn 6-tet split of a box (mesh.py:145-184). coords (N,3), conn (E,4). */
+int tal_box_mesh(int64_t nx, int64_t ny, int64_t nz, double ex, double ey,
+                 double ez, double *coords, int64_t *conn);
+/* signed volumes det/6 (mesh.py:110-123); min_out may be NULL */
+int tal_signed_volumes(const double *coords, const int64_t *conn, int64_t n_elems,
+                       double *vols);
+/* greedy lowest-free colouring in element order (mesh.py:235-257) */
+int tal_color_elements(const int64_t *conn, int64_t n_nodes, int64_t n_elems,
+                       int64_t *colors, int64_t *n_colors);
+/* 1 if no two elements sharing a node share a colour (mesh.py:260-267) */
+int tal_check_coloring(const int64_t *conn, const int64_t *colors, int64_t n_nodes,
+                       int64_t n_elems, int *valid);
+/* node permutation perm[new] = old by the given TAL_RENUMBER_* */
+int tal_renumber_nodes(const double *coords, const int64_t *conn, int64_t n_nodes,
+                       int64_t n_elems, int method, int64_t *perm);
+
+/* ---- measurement ------------------------------------------------------------ */
+/* When enabled, tal_run records a CUDA event pair around the dominant
+ * assembly kernel of every call (on the launching stream, inside the real
+ * step).  tal_profile_read waits for and returns the per-call durations (ms)
+ * recorded since the last read, oldest first (at most 'cap', ring of 4096). */
+int tal_profile(tal_handle *h, int enable);
+int tal_profile_read(tal_handle *h, double *ms_out, int64_t cap, int64_t *n_out);
+/* Sustained FP64 FMA throughput of 'device' (TFLOP/s, 2 flop per DFMA),
+ * timed with CUDA events over 'ms_target' milliseconds of work. */
+int tal_fp64_peak(int device, double ms_target, double *tflops, double *sm_clock_mhz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAL_B200_H */

@@ -1,0 +1,411 @@
+"""The drop-in assembly operator: ``assemble_rsp`` on a B200.
+
+Reference interface mirrored (tet-assembly-lab 0.1.0, variants.py):
+
+* ``RunConfig`` (variants.py:74-101) -- same fields and validation; the
+  GPU adds scatter modes and device-layout knobs (superset).
+* ``CounterLedger`` / ``VariantInfo`` / ``AssemblyResult`` (variants.py:104-135).
+* ``assemble_rsp(mesh, u, params, cfg) -> AssemblyResult`` (variants.py:553-616),
+  registered in ``ASSEMBLERS`` and dispatched by ``assemble`` (:619-627).
+* ``assemble_elements(coords, conn, u, rho, mu, cvre, pmat, ids, rhs)`` --
+  the numba seam (_rsp_kernels.py:20-21), accumulating into ``rhs``.
+
+Everything numerical runs in ``libtal_b200.so`` on the GPU; there is no CPU
+fallback (a missing library raises ImportError, a missing GPU RuntimeError).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+from collections import OrderedDict
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _native as N
+from .fields import PhysParams, interpolation_table, validate_velocity
+
+
+class VariantId(enum.Enum):
+    RSP = "rsp"
+
+
+SCATTER_MODES = tuple(N.SCATTER)
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    """Execution shape.
+
+    Reference fields (variants.py:74-101): ``vector_dim``, ``n_threads``,
+    ``reps``, ``scatter``, ``cache_capacity_bytes`` -- validated identically
+    (vector_dim / n_threads / cache_capacity_bytes have no effect on the GPU
+    path).  ``scatter`` is a superset:
+
+    * ``private``        CTA-private shared-memory sums, ordered merge (bitwise
+                         reproducible; the reference default),
+    * ``colored``        colour-by-colour plain read-modify-write (bitwise
+                         reproducible; uses ``mesh.colors`` or a greedy colouring),
+    * ``atomic``         12 FP64 REDs per element,
+    * ``private-atomic`` CTA-private sums, one FP64 RED per shared node.
+
+    GPU knobs: ``device``, ``renumber`` (rcm | sfc | none), ``element_order``
+    (sfc | node | keep), ``chunk_elems`` / ``chunk_nodes`` (CTA chunk limits).
+    """
+
+    vector_dim: int = 16
+    n_threads: int = 1
+    reps: int = 5
+    scatter: str = "private"
+    cache_capacity_bytes: int = 1 << 20
+    device: int = 0
+    renumber: str = "rcm"
+    element_order: str = "sfc"
+    chunk_elems: int = 512
+    chunk_nodes: int = 1024
+
+    def __post_init__(self):
+        if self.vector_dim < 1:
+            raise ValueError(f"vector_dim must be >= 1, got {self.vector_dim}")
+        if self.n_threads < 1:
+            raise ValueError(f"n_threads must be >= 1, got {self.n_threads}")
+        if self.reps < 1:
+            raise ValueError(f"reps must be >= 1, got {self.reps}")
+        if self.scatter not in SCATTER_MODES:
+            raise ValueError(f"scatter must be one of {SCATTER_MODES}, got {self.scatter!r}")
+        if self.cache_capacity_bytes < 0:
+            raise ValueError("cache_capacity_bytes must be >= 0")
+        if self.device < 0:
+            raise ValueError("device must be >= 0")
+        if self.renumber not in N.RENUMBER:
+            raise ValueError(f"renumber must be one of {tuple(N.RENUMBER)}, got {self.renumber!r}")
+        if self.element_order not in N.EORDER:
+            raise ValueError(f"element_order must be one of {tuple(N.EORDER)}")
+        if not 1 <= self.chunk_elems <= 1024:
+            raise ValueError("chunk_elems must be in [1, 1024]")
+        if not 4 <= self.chunk_nodes <= 2048:
+            raise ValueError("chunk_nodes must be in [4, 2048]")
+
+
+@dataclass(frozen=True)
+class CounterLedger:
+    """Static per-element counts (1 FMA = 2 Flop); bytes_dram_est is modeled."""
+
+    flops_per_elem: int
+    loadstore_per_elem: int
+    intermediate_doubles_per_elem: int
+    intermediate_arrays: int
+    bytes_dram_est: float
+
+
+@dataclass(frozen=True)
+class VariantInfo:
+    variant: VariantId
+    name: str
+    summary: str
+    flops_per_elem: int
+    loadstore_per_elem: int
+    intermediate_doubles_per_elem: int
+    intermediate_arrays: int
+    flop_formula: str
+
+
+# The operator and its algorithmic cost are the reference RSP ledger's
+# (variants.py:207-217); the kernel executes fewer FP64 instructions.
+VARIANT_INFO: dict[VariantId, VariantInfo] = {
+    VariantId.RSP: VariantInfo(
+        variant=VariantId.RSP,
+        name="privatized (B200)",
+        summary="one sm_100a element kernel, all intermediates in registers, "
+        "CTA-private shared-memory scatter",
+        flops_per_elem=448,
+        loadstore_per_elem=48,
+        intermediate_doubles_per_elem=79,
+        intermediate_arrays=0,
+        flop_formula="62 (geometry) + 63 (velocity gradient) + 64 (eddy viscosity) "
+        "+ 7 (factors) + 4 nodes x 63 (moments, rhs entries, scatter)",
+    ),
+}
+
+
+def make_ledger(variant: VariantId, cfg: RunConfig) -> CounterLedger:
+    info = VARIANT_INFO[variant]
+    return CounterLedger(
+        flops_per_elem=info.flops_per_elem,
+        loadstore_per_elem=info.loadstore_per_elem,
+        intermediate_doubles_per_elem=info.intermediate_doubles_per_elem,
+        intermediate_arrays=info.intermediate_arrays,
+        bytes_dram_est=float(4 * 3 * 8 * 2 + 4 * 3 * 8 * 2),
+    )
+
+
+@dataclass(frozen=True)
+class Timings:
+    h2d_ms: float
+    pack_ms: float
+    kernel_ms: float
+    unpack_ms: float
+    d2h_ms: float
+    total_ms: float
+    kernel_launches: int
+
+
+@dataclass(frozen=True)
+class AssemblyResult:
+    rhs: np.ndarray
+    ledger: CounterLedger
+    wall_time: float
+    elements_per_second: float
+    variant: VariantId
+    timings: Optional[Timings] = None
+
+
+def _params(params: PhysParams, pmat: Optional[np.ndarray] = None) -> N.TalParams:
+    p = N.TalParams()
+    p.rho = float(params.rho)
+    p.mu = float(params.mu)
+    p.c_vreman = float(params.c_vreman)
+    pm = interpolation_table() if pmat is None else np.asarray(pmat, dtype=np.float64)
+    if pm.shape != (4, 4):
+        raise ValueError("pmat must be 4x4")
+    for i, v in enumerate(pm.ravel()):
+        p.pmat[i] = float(v)
+    return p
+
+
+class _CudaView:
+    """Minimal __cuda_array_interface__ wrapper so torch can view device buffers."""
+
+    def __init__(self, ptr: int, shape, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {
+            "shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+            "version": 3, "strides": None,
+        }
+
+
+class Assembler:
+    """One mesh resident on one GPU (a ``tal_handle``).
+
+    Upload once, assemble many times.  ``assemble(u, params)`` is the host
+    round trip; ``run(params, stream)`` the device-resident step on the
+    internal (renumbered, SoA) buffers exposed by ``device_buffers()``.
+    """
+
+    def __init__(self, mesh, cfg: Optional[RunConfig] = None, build_colors: Optional[bool] = None):
+        cfg = cfg or RunConfig()
+        self.cfg = cfg
+        L = N.lib()
+        h = ctypes.c_void_p()
+        N.check(L.tal_create(cfg.device, ctypes.byref(h)))
+        self._h = h
+        self.n_nodes = int(mesh.coords.shape[0])
+        self.n_elems = int(mesh.connectivity.shape[0])
+        coords = np.ascontiguousarray(mesh.coords, dtype=np.float64)
+        conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int64)
+        colors = getattr(mesh, "colors", None)
+        colors = None if colors is None else np.ascontiguousarray(colors, dtype=np.int64)
+        opts = N.TalMeshOpts()
+        opts.renumber = N.RENUMBER[cfg.renumber]
+        opts.element_order = N.EORDER[cfg.element_order]
+        opts.chunk_elems = cfg.chunk_elems
+        opts.chunk_nodes = cfg.chunk_nodes
+        opts.validate = 1
+        if build_colors is None:
+            build_colors = cfg.scatter == "colored"
+        opts.build_colors = 1 if build_colors else 0
+        try:
+            N.check(L.tal_upload_mesh(h, N.ptr(coords), N.ptr(conn), self.n_nodes, self.n_elems,
+                                      N.ptr(colors), ctypes.byref(opts)))
+        except Exception:
+            L.tal_destroy(h)
+            self._h = None
+            raise
+
+    # -- info ---------------------------------------------------------------
+    def info(self) -> dict:
+        inf = N.TalMeshInfo()
+        N.check(N.lib().tal_mesh_info_get(self._h, ctypes.byref(inf)))
+        return {k: getattr(inf, k) for k, _ in N.TalMeshInfo._fields_}
+
+    # -- host round trip -----------------------------------------------------
+    def assemble_into(self, u: np.ndarray, params: PhysParams, rhs: np.ndarray,
+                      scatter: Optional[str] = None, pmat=None) -> Timings:
+        scatter = scatter or self.cfg.scatter
+        if scatter not in N.SCATTER:
+            raise ValueError(f"unknown scatter mode {scatter!r}")
+        if u.shape != (self.n_nodes, 3) or rhs.shape != (self.n_nodes, 3):
+            raise ValueError("u and rhs must have shape (n_nodes, 3)")
+        if not (u.flags.c_contiguous and rhs.flags.c_contiguous and u.dtype == np.float64
+                and rhs.dtype == np.float64):
+            raise ValueError("u and rhs must be C-contiguous float64")
+        t = N.TalTimings()
+        N.check(N.lib().tal_assemble(self._h, N.ptr(u), ctypes.byref(_params(params, pmat)),
+                                     N.ptr(rhs), N.SCATTER[scatter], ctypes.byref(t)))
+        return Timings(t.h2d_ms, t.pack_ms, t.kernel_ms, t.unpack_ms, t.d2h_ms, t.total_ms,
+                       int(t.kernel_launches))
+
+    def assemble(self, u: np.ndarray, params: PhysParams, scatter: Optional[str] = None):
+        rhs = np.empty((self.n_nodes, 3))
+        t = self.assemble_into(np.ascontiguousarray(u, dtype=np.float64), params, rhs, scatter)
+        return rhs, t
+
+    # -- device-resident path ----------------------------------------------
+    def device_buffers(self) -> dict:
+        """Raw device pointers (internal node order): ux,uy,uz,rx,ry,rz,perm,iperm."""
+        b = N.TalBuffers()
+        N.check(N.lib().tal_buffers_get(self._h, ctypes.byref(b)))
+        return {k: getattr(b, k) for k, _ in N.TalBuffers._fields_}
+
+    def torch_views(self):
+        """torch tensors viewing the internal SoA buffers (no copy)."""
+        import torch
+        b = self.device_buffers()
+        n = self.n_nodes
+        return {k: torch.as_tensor(_CudaView(b[k], (n,)), device=f"cuda:{self.cfg.device}")
+                for k in ("ux", "uy", "uz", "rx", "ry", "rz")}
+
+    def set_velocity_host(self, u: np.ndarray, stream: int = 0) -> None:
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        if u.shape != (self.n_nodes, 3):
+            raise ValueError("u must have shape (n_nodes, 3)")
+        N.check(N.lib().tal_set_velocity_host(self._h, N.ptr(u), ctypes.c_void_p(stream or None)))
+
+    def set_velocity_device(self, d_u_ptr: int, stream: int = 0) -> None:
+        N.check(N.lib().tal_set_velocity_device(self._h, ctypes.c_void_p(d_u_ptr),
+                                                ctypes.c_void_p(stream or None)))
+
+    def run(self, params: PhysParams, scatter: Optional[str] = None, stream: int = 0,
+            pmat=None) -> int:
+        """Enqueue one assembly on internal buffers; returns kernels launched."""
+        scatter = scatter or self.cfg.scatter
+        if scatter not in N.SCATTER:
+            raise ValueError(f"unknown scatter mode {scatter!r}")
+        nl = ctypes.c_int64(0)
+        N.check(N.lib().tal_run(self._h, ctypes.byref(_params(params, pmat)), N.SCATTER[scatter],
+                                ctypes.c_void_p(stream or None), ctypes.byref(nl)))
+        return int(nl.value)
+
+    def get_rhs_host(self, out: Optional[np.ndarray] = None, stream: int = 0) -> np.ndarray:
+        out = np.empty((self.n_nodes, 3)) if out is None else out
+        N.check(N.lib().tal_get_rhs_host(self._h, N.ptr(out), ctypes.c_void_p(stream or None)))
+        return out
+
+    def get_rhs_device(self, d_out_ptr: int, stream: int = 0) -> None:
+        N.check(N.lib().tal_get_rhs_device(self._h, ctypes.c_void_p(d_out_ptr),
+                                           ctypes.c_void_p(stream or None)))
+
+    def synchronize(self, stream: int = 0) -> None:
+        N.check(N.lib().tal_synchronize(self._h, ctypes.c_void_p(stream or None)))
+
+    def map_nodes(self, caller_ids: np.ndarray) -> np.ndarray:
+        ids = np.ascontiguousarray(caller_ids, dtype=np.int64)
+        out = np.empty(ids.shape[0], dtype=np.int32)
+        N.check(N.lib().tal_map_nodes(self._h, N.ptr(ids), ids.shape[0], N.ptr(out)))
+        return out
+
+    def halo_pack(self, d_list: int, n: int, d_out: int, stream: int = 0) -> None:
+        N.check(N.lib().tal_halo_pack(self._h, ctypes.c_void_p(d_list), n, ctypes.c_void_p(d_out),
+                                      ctypes.c_void_p(stream or None)))
+
+    def halo_accumulate(self, d_list: int, n: int, d_in: int, stream: int = 0) -> None:
+        N.check(N.lib().tal_halo_accumulate(self._h, ctypes.c_void_p(d_list), n,
+                                            ctypes.c_void_p(d_in), ctypes.c_void_p(stream or None)))
+
+    def profile(self, enable: bool = True) -> None:
+        """Record CUDA events around the dominant kernel of every run()."""
+        N.check(N.lib().tal_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self, cap: int = 4096) -> np.ndarray:
+        """Dominant-kernel durations (ms) of the runs since the last read."""
+        out = np.empty(cap)
+        n = ctypes.c_int64(0)
+        N.check(N.lib().tal_profile_read(self._h, N.ptr(out), cap, ctypes.byref(n)))
+        return out[: n.value].copy()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            N.lib().tal_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# small LRU of resident meshes so repeated assemble_rsp calls on one mesh do
+# not re-upload (the reference likewise does its per-mesh work before t0)
+_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_CACHE_SIZE = 4
+
+
+def _cached_assembler(mesh, cfg: RunConfig) -> Assembler:
+    colors = getattr(mesh, "colors", None)
+    key = (id(mesh.coords), id(mesh.connectivity), id(colors), mesh.coords.shape,
+           mesh.connectivity.shape, cfg.device, cfg.renumber, cfg.element_order,
+           cfg.chunk_elems, cfg.chunk_nodes, cfg.scatter == "colored")
+    hit = _CACHE.get(key)
+    if hit is not None:
+        _CACHE.move_to_end(key)
+        return hit[0]
+    asm = Assembler(mesh, cfg)
+    # hold the arrays so their ids cannot be recycled while cached
+    _CACHE[key] = (asm, mesh.coords, mesh.connectivity, colors)
+    while len(_CACHE) > _CACHE_SIZE:
+        _, (old, *_) = _CACHE.popitem(last=False)
+        old.close()
+    return asm
+
+
+def clear_cache() -> None:
+    while _CACHE:
+        _, (asm, *_) = _CACHE.popitem()
+        asm.close()
+
+
+def assemble_rsp(mesh, u: np.ndarray, params: PhysParams,
+                 cfg: Optional[RunConfig] = None) -> AssemblyResult:
+    """Drop-in for ``tet_assembly_lab.assemble_rsp`` (variants.py:553-616).
+
+    ``wall_time`` is the CUDA-event time of the call's device timeline
+    (velocity H2D + layout pack + assembly kernels + unpack + RHS D2H); the
+    one-time mesh upload is excluded like the reference's colouring.
+    """
+    cfg = cfg or RunConfig()
+    u = validate_velocity(mesh, u)
+    asm = _cached_assembler(mesh, cfg)
+    rhs = np.empty((asm.n_nodes, 3))
+    t = asm.assemble_into(u, params, rhs, cfg.scatter)
+    wall = t.total_ms * 1e-3
+    rate = asm.n_elems / wall if wall > 0.0 else 0.0
+    return AssemblyResult(rhs=rhs, ledger=make_ledger(VariantId.RSP, cfg), wall_time=wall,
+                          elements_per_second=rate, variant=VariantId.RSP, timings=t)
+
+
+ASSEMBLERS: dict[VariantId, Callable] = {VariantId.RSP: assemble_rsp}
+
+
+def assemble(variant: VariantId, mesh, u, params, cfg=None) -> AssemblyResult:
+    return ASSEMBLERS[variant](mesh, u, params, cfg)
+
+
+def assemble_elements(coords, conn, u, rho, mu, cvre, pmat, ids, rhs, device: int = 0) -> None:
+    """The numba seam ``_rsp_kernels.assemble_elements`` on the GPU: assemble
+    elements ``ids`` and ADD into ``rhs`` (in place, like the numba loop)."""
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    conn = np.ascontiguousarray(conn, dtype=np.int64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    pm = np.ascontiguousarray(pmat, dtype=np.float64)
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    if not (isinstance(rhs, np.ndarray) and rhs.flags.c_contiguous and rhs.dtype == np.float64):
+        raise ValueError("rhs must be a C-contiguous float64 array (accumulated in place)")
+    if coords.shape[1:] != (3,) or conn.shape[1:] != (4,) or u.shape != coords.shape \
+            or rhs.shape != coords.shape or pm.shape != (4, 4):
+        raise ValueError("bad array shapes")
+    N.check(N.lib().tal_assemble_elements(device, N.ptr(coords), N.ptr(conn), coords.shape[0],
+                                          conn.shape[0], N.ptr(u), float(rho), float(mu),
+                                          float(cvre), N.ptr(pm), N.ptr(ids), ids.shape[0],
+                                          N.ptr(rhs)))

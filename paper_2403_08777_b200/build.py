@@ -1,0 +1,90 @@
+"""Build the in-tree native library ``libtal_b200.so`` for sm_100a.
+
+    python -m paper_2403_08777_b200.build [--verbose]
+
+nvcc cross-compiles without a GPU; the resulting .so is git-ignored but
+travels to the GPU box with the repo snapshot.  ``-Xptxas -v`` output
+(registers / spills per kernel) is written to ``build/ptxas.log``.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OUT = PKG / "libtal_b200.so"
+BUILD = ROOT / "build"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nvcc() -> str:
+    cand = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(cand).exists():
+        raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libtal_b200.so")
+    return cand
+
+
+def _sources():
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp")) + sorted(CSRC.glob("*.cuh")) + \
+        sorted(CSRC.glob("*.hpp")) + [ROOT / "include" / "tal_b200.h"]
+
+
+def up_to_date() -> bool:
+    if not OUT.exists():
+        return False
+    t = OUT.stat().st_mtime
+    return all(s.stat().st_mtime <= t for s in _sources())
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    if not force and up_to_date():
+        return OUT
+    BUILD.mkdir(exist_ok=True)
+    nvcc = _nvcc()
+    objs = []
+    log = []
+    for src in sorted(CSRC.glob("*.cpp")):
+        obj = BUILD / (src.stem + ".o")
+        cmd = ["g++", "-O3", "-fPIC", "-std=c++17", "-Wall", "-c", str(src), "-o", str(obj)]
+        subprocess.run(cmd, check=True)
+        objs.append(obj)
+    for src in sorted(CSRC.glob("*.cu")):
+        obj = BUILD / (src.stem + ".o")
+        cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+               "-Xptxas", "-v", "--expt-relaxed-constexpr", "-c", str(src), "-o", str(obj)]
+        r = subprocess.run(cmd, check=False, capture_output=True, text=True)
+        log.append(r.stdout + r.stderr)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {src.name}")
+        objs.append(obj)
+    tmp = OUT.with_suffix(".so.tmp")
+    cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs),
+           "-lpthread"]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, OUT)
+    (BUILD / "ptxas.log").write_text("".join(log))
+    if verbose:
+        print("".join(log))
+    return OUT
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--force", action="store_true")
+    a = ap.parse_args()
+    p = build(verbose=a.verbose, force=a.force)
+    print(p)
+
+
+if __name__ == "__main__":
+    main()

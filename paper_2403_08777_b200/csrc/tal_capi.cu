@@ -1,0 +1,1026 @@
+// tal_capi.cu -- the C-ABI (include/tal_b200.h) over the sm_100a kernels.
+//
+// Replaces the reference seam _rsp_kernels.assemble_elements
+// (_rsp_kernels.py:20-21) and the kernel loop of variants.assemble_rsp
+// (variants.py:572-615).  See DESIGN.md for the data layout.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tal_b200.h"
+#include "tal_kernels.cuh"
+#include "tal_prep.hpp"
+
+using namespace tal;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+#define TAL_CK(call)                                                                        \
+    do {                                                                                    \
+        cudaError_t _e = (call);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            return fail(TAL_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+    } while (0)
+
+#define TAL_CK_LAUNCH()                                                                     \
+    do {                                                                                    \
+        cudaError_t _e = cudaGetLastError();                                                \
+        if (_e != cudaSuccess)                                                              \
+            return fail(TAL_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+template <class T>
+int dev_upload(T **dst, const T *src, size_t count)
+{
+    *dst = nullptr;
+    if (count == 0)
+        return TAL_OK;
+    TAL_CK(cudaMalloc((void **)dst, count * sizeof(T)));
+    TAL_CK(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return TAL_OK;
+}
+
+unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+}  // namespace
+
+struct tal_handle {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};
+    int64_t N = 0, E = 0;
+    bool has_mesh = false;
+    // node data (internal order)
+    double *nodebuf = nullptr;  // x,y,z,ux,uy,uz,rx,ry,rz: 9*N doubles
+    double *staging = nullptr;  // 3*N doubles (AoS in/out)
+    int32_t *perm = nullptr, *iperm = nullptr;
+    std::vector<int32_t> h_iperm;  // caller -> internal (host)
+    int4 *conn = nullptr;          // element order of the chunking
+    // colouring
+    int4 *conn_col = nullptr;
+    std::vector<int64_t> col_off;
+    // private scatter
+    Chunking ch;
+    int4 *d_chunks = nullptr;
+    int32_t *d_chunk_nodes = nullptr;
+    uint16_t *d_csr_off = nullptr, *d_csr_slots = nullptr;
+    ushort4 *d_lconn = nullptr;
+    int32_t *d_bnd_nodes = nullptr, *d_bnd_off = nullptr, *d_bnd_pos = nullptr;
+    double *d_partial = nullptr;  // 3 * n_chunk_nodes
+    size_t smem_private = 0;
+    tal_mesh_info info = {};
+    tal_timings last = {};
+    // dominant-kernel event ring (tal_profile)
+    static constexpr int PROF_RING = 4096;
+    bool prof_on = false;
+    std::vector<cudaEvent_t> prof_ev;  // 2 per slot
+    int64_t prof_head = 0, prof_count = 0;
+
+    double *X() const { return nodebuf; }
+    double *Y() const { return nodebuf + N; }
+    double *Z() const { return nodebuf + 2 * N; }
+    double *UX() const { return nodebuf + 3 * N; }
+    double *UY() const { return nodebuf + 4 * N; }
+    double *UZ() const { return nodebuf + 5 * N; }
+    double *RX() const { return nodebuf + 6 * N; }
+    double *RY() const { return nodebuf + 7 * N; }
+    double *RZ() const { return nodebuf + 8 * N; }
+
+    void free_mesh()
+    {
+        void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_chunks, d_chunk_nodes,
+                        d_csr_off, d_csr_slots, d_lconn, d_bnd_nodes, d_bnd_off, d_bnd_pos,
+                        d_partial};
+        for (void *p : ptrs)
+            if (p)
+                cudaFree(p);
+        nodebuf = staging = d_partial = nullptr;
+        perm = iperm = d_chunk_nodes = d_bnd_nodes = d_bnd_off = d_bnd_pos = nullptr;
+        conn = conn_col = d_chunks = nullptr;
+        d_csr_off = d_csr_slots = nullptr;
+        d_lconn = nullptr;
+        col_off.clear();
+        h_iperm.clear();
+        ch = Chunking();
+        has_mesh = false;
+        info = tal_mesh_info{};
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0)
+            cudaSetDevice(prev);
+    }
+};
+
+bool make_consts(const tal_params *p, ElemConsts &kc, bool &sym)
+{
+    kc.rho = p->rho;
+    kc.mu = p->mu;
+    kc.cvre = p->c_vreman;
+    for (int i = 0; i < 16; ++i)
+        kc.pm[i] = p->pmat[i];
+    double pd = 0.0, po = 0.0;
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b)
+            (a == b ? pd : po) += p->pmat[4 * a + b];
+    pd /= 4.0;
+    po /= 12.0;
+    sym = true;
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+            const double ref = (a == b) ? pd : po;
+            if (std::fabs(p->pmat[4 * a + b] - ref) > 1e-14 * std::max(std::fabs(ref), 1e-300))
+                sym = false;
+        }
+    kc.a_po = -p->rho * po / 24.0;
+    kc.a_q = -p->rho * (pd - po) / 24.0;
+    return std::isfinite(p->rho) && std::isfinite(p->mu) && std::isfinite(p->c_vreman);
+}
+
+int check_params(const tal_params *p)
+{
+    if (!p)
+        return fail(TAL_EINVAL, "params is NULL");
+    // PhysParams.__post_init__ (kernel.py:41-49)
+    if (!(p->rho > 0.0))
+        return fail(TAL_EINVAL, "rho must be positive, got " + std::to_string(p->rho));
+    if (p->mu < 0.0)
+        return fail(TAL_EINVAL, "mu must be non-negative, got " + std::to_string(p->mu));
+    if (p->c_vreman < 0.0)
+        return fail(TAL_EINVAL, "c_vreman must be non-negative, got " + std::to_string(p->c_vreman));
+    for (int i = 0; i < 16; ++i)
+        if (!std::isfinite(p->pmat[i]))
+            return fail(TAL_EINVAL, "pmat contains non-finite entries");
+    return TAL_OK;
+}
+
+struct ProfMark {
+    tal_handle *h;
+    cudaStream_t s;
+    int64_t slot = -1;
+    void begin()
+    {
+        if (!h->prof_on)
+            return;
+        slot = (h->prof_head + h->prof_count) % tal_handle::PROF_RING;
+        if (h->prof_count == tal_handle::PROF_RING)  // overwrite the oldest
+            h->prof_head = (h->prof_head + 1) % tal_handle::PROF_RING;
+        else
+            ++h->prof_count;
+        cudaEventRecord(h->prof_ev[2 * slot], s);
+    }
+    void end()
+    {
+        if (slot >= 0)
+            cudaEventRecord(h->prof_ev[2 * slot + 1], s);
+    }
+};
+
+int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, int64_t *launches)
+{
+    ProfMark pm{h, s};
+    ElemConsts kc;
+    bool sym;
+    if (!make_consts(p, kc, sym))
+        return fail(TAL_EINVAL, "non-finite physical parameters");
+    NodeSoA nodes{h->X(), h->Y(), h->Z(), h->UX(), h->UY(), h->UZ()};
+    RhsSoA rhs{h->RX(), h->RY(), h->RZ()};
+    int64_t nl = 0;
+    const int64_t N = h->N, E = h->E;
+    switch (scatter) {
+    case TAL_SCATTER_ATOMIC: {
+        if (N)
+            TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
+        if (E) {
+            pm.begin();
+            if (sym)
+                k_assemble_atomic<true><<<grid_for(E, 256), 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc);
+            else
+                k_assemble_atomic<false><<<grid_for(E, 256), 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc);
+            pm.end();
+            TAL_CK_LAUNCH();
+            ++nl;
+        }
+        break;
+    }
+    case TAL_SCATTER_COLORED: {
+        if (!h->conn_col && E)
+            return fail(TAL_ESTATE, "mesh was uploaded without a colouring (build_colors=0, colors=NULL)");
+        if (N)
+            TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
+        pm.begin();  // colour launches together form the dominant work
+        for (size_t c = 0; c + 1 < h->col_off.size(); ++c) {
+            const int64_t b = h->col_off[c], e = h->col_off[c + 1];
+            if (e <= b)
+                continue;
+            if (sym)
+                k_assemble_colored<true><<<grid_for(e - b, 256), 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc);
+            else
+                k_assemble_colored<false><<<grid_for(e - b, 256), 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc);
+            TAL_CK_LAUNCH();
+            ++nl;
+        }
+        pm.end();
+        break;
+    }
+    case TAL_SCATTER_PRIVATE:
+    case TAL_SCATTER_PRIVATE_ATOMIC: {
+        const bool ordered = scatter == TAL_SCATTER_PRIVATE;
+        ChunkArgs ca{h->d_chunks, h->d_chunk_nodes, h->d_csr_off, h->d_csr_slots, h->d_lconn,
+                     h->ch.chunk_elems, h->ch.max_nodes, nullptr, nullptr, nullptr};
+        const int64_t ncn = (int64_t)h->ch.chunk_nodes.size();
+        if (ordered && h->d_partial) {
+            ca.px = h->d_partial;
+            ca.py = h->d_partial + ncn;
+            ca.pz = h->d_partial + 2 * ncn;
+        }
+        if (!ordered && N)
+            TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
+        const int64_t nch = h->info.n_chunks;
+        if (nch) {
+            const size_t sm = h->smem_private;
+            pm.begin();
+            if (sym && ordered)
+                k_assemble_private<true, true><<<(unsigned)nch, PRIV_THREADS, sm, s>>>(ca, nodes, rhs, kc);
+            else if (sym)
+                k_assemble_private<true, false><<<(unsigned)nch, PRIV_THREADS, sm, s>>>(ca, nodes, rhs, kc);
+            else if (ordered)
+                k_assemble_private<false, true><<<(unsigned)nch, PRIV_THREADS, sm, s>>>(ca, nodes, rhs, kc);
+            else
+                k_assemble_private<false, false><<<(unsigned)nch, PRIV_THREADS, sm, s>>>(ca, nodes, rhs, kc);
+            pm.end();
+            TAL_CK_LAUNCH();
+            ++nl;
+        }
+        const int64_t nb = (int64_t)h->ch.bnd_nodes.size();
+        if (ordered && nb) {
+            k_merge_partials<<<grid_for(nb, 256), 256, 0, s>>>(h->d_bnd_nodes, h->d_bnd_off, h->d_bnd_pos,
+                                                              nb, ca.px, ca.py, ca.pz, rhs);
+            TAL_CK_LAUNCH();
+            ++nl;
+        }
+        break;
+    }
+    default:
+        return fail(TAL_EINVAL, "unknown scatter mode " + std::to_string(scatter));
+    }
+    if (launches)
+        *launches = nl;
+    return TAL_OK;
+}
+
+int set_kernel_attrs(size_t smem)
+{
+    const void *fns[] = {(const void *)k_assemble_private<true, true>,
+                         (const void *)k_assemble_private<true, false>,
+                         (const void *)k_assemble_private<false, true>,
+                         (const void *)k_assemble_private<false, false>};
+    for (const void *f : fns)
+        TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return TAL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *tal_last_error(void) { return g_err.c_str(); }
+int tal_abi_version(void) { return TAL_ABI_VERSION; }
+
+int tal_device_count(int *count)
+{
+    if (!count)
+        return fail(TAL_EINVAL, "count is NULL");
+    *count = 0;
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return fail(TAL_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    return TAL_OK;
+}
+
+int tal_create(int device, tal_handle **out)
+{
+    if (!out)
+        return fail(TAL_EINVAL, "out is NULL");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(TAL_ECUDA, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                                   "); the assembly has no CPU fallback");
+    if (device < 0 || device >= n)
+        return fail(TAL_EINVAL, "device index out of range");
+    cudaDeviceProp prop;
+    TAL_CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return fail(TAL_ECUDA, std::string("device ") + prop.name + " is not sm_100-class");
+    DeviceGuard g(device);
+    tal_handle *h = new tal_handle();
+    h->device = device;
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete h;
+        return fail(TAL_ECUDA, "cudaStreamCreate failed");
+    }
+    for (auto &ev : h->ev)
+        cudaEventCreate(&ev);
+    *out = h;
+    return TAL_OK;
+}
+
+int tal_destroy(tal_handle *h)
+{
+    if (!h)
+        return TAL_OK;
+    DeviceGuard g(h->device);
+    cudaStreamSynchronize(h->stream);
+    h->free_mesh();
+    for (auto &ev : h->ev)
+        cudaEventDestroy(ev);
+    for (auto &ev : h->prof_ev)
+        cudaEventDestroy(ev);
+    cudaStreamDestroy(h->stream);
+    delete h;
+    return TAL_OK;
+}
+
+int tal_host_alloc(int64_t bytes, void **out)
+{
+    if (!out || bytes < 0)
+        return fail(TAL_EINVAL, "bad arguments");
+    TAL_CK(cudaMallocHost(out, (size_t)std::max<int64_t>(bytes, 1)));
+    return TAL_OK;
+}
+
+int tal_host_free(void *p)
+{
+    if (p)
+        TAL_CK(cudaFreeHost(p));
+    return TAL_OK;
+}
+
+int tal_default_mesh_opts(tal_mesh_opts *o)
+{
+    if (!o)
+        return fail(TAL_EINVAL, "NULL");
+    o->renumber = TAL_RENUMBER_RCM;
+    o->element_order = TAL_EORDER_SFC;
+    o->chunk_elems = 512;
+    o->chunk_nodes = 1024;
+    o->validate = 1;
+    o->build_colors = 0;
+    return TAL_OK;
+}
+
+int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, int64_t n_nodes,
+                    int64_t n_elems, const int64_t *colors, const tal_mesh_opts *opts_in)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (n_nodes < 0 || n_elems < 0)
+        return fail(TAL_EINVAL, "negative sizes");
+    if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
+        return fail(TAL_EINVAL, "meshes are limited to 2^31-1 nodes/elements per device");
+    if ((n_nodes && !coords) || (n_elems && !conn))
+        return fail(TAL_EINVAL, "NULL mesh arrays");
+    tal_mesh_opts opts;
+    tal_default_mesh_opts(&opts);
+    if (opts_in)
+        opts = *opts_in;
+    const auto t0 = std::chrono::steady_clock::now();
+    // validation (Mesh.__post_init__, mesh.py:50-75)
+    for (int64_t i = 0; i < 4 * n_elems; ++i)
+        if (conn[i] < 0 || conn[i] >= n_nodes)
+            return fail(TAL_EINVAL, "connectivity index out of range [0, n_nodes)");
+    if (opts.validate && n_elems) {
+        std::vector<double> vols((size_t)n_elems);
+        signed_volumes(coords, conn, n_elems, vols.data());
+        for (int64_t e = 0; e < n_elems; ++e)
+            if (!(vols[e] > 0.0)) {
+                char buf[128];
+                snprintf(buf, sizeof buf, "element %lld has non-positive signed volume %g",
+                         (long long)e, vols[e]);
+                return fail(TAL_EINVAL, buf);
+            }
+    }
+    if (colors && !check_coloring(conn, colors, n_nodes, n_elems))
+        return fail(TAL_EINVAL, "coloring invalid: elements sharing a node share a color");
+
+    DeviceGuard g(h->device);
+    cudaStreamSynchronize(h->stream);
+    h->free_mesh();
+    h->N = n_nodes;
+    h->E = n_elems;
+
+    // node renumbering: perm[new] = old
+    std::vector<int32_t> perm;
+    if (opts.renumber == TAL_RENUMBER_RCM)
+        renumber_rcm(conn, n_nodes, n_elems, perm);
+    else if (opts.renumber == TAL_RENUMBER_SFC)
+        renumber_sfc(coords, n_nodes, perm);
+    else if (opts.renumber != TAL_RENUMBER_NONE)
+        return fail(TAL_EINVAL, "unknown renumber method");
+    const bool renum = !perm.empty();
+    std::vector<int32_t> iperm;
+    if (renum) {
+        iperm.resize((size_t)n_nodes);
+        for (int64_t i = 0; i < n_nodes; ++i)
+            iperm[perm[i]] = (int32_t)i;
+    }
+    std::vector<double> xin((size_t)(3 * n_nodes));  // internal AoS coords
+    for (int64_t i = 0; i < n_nodes; ++i) {
+        const int64_t s = renum ? perm[i] : i;
+        for (int c = 0; c < 3; ++c)
+            xin[3 * i + c] = coords[3 * s + c];
+    }
+    std::vector<int32_t> cin((size_t)(4 * n_elems));
+    for (int64_t i = 0; i < 4 * n_elems; ++i)
+        cin[i] = renum ? iperm[conn[i]] : (int32_t)conn[i];
+    // element order
+    std::vector<int32_t> eperm;
+    element_order(opts.element_order, cin.data(), xin.data(), n_nodes, n_elems, eperm);
+    std::vector<int32_t> cord((size_t)(4 * n_elems));
+    for (int64_t e = 0; e < n_elems; ++e)
+        for (int a = 0; a < 4; ++a)
+            cord[4 * e + a] = cin[4 * (int64_t)eperm[e] + a];
+    // chunks
+    std::string err;
+    if (!build_chunks(cord.data(), n_nodes, n_elems, opts.chunk_elems, opts.chunk_nodes, h->ch, err))
+        return fail(TAL_EINVAL, err);
+    // colouring (caller's or greedy on the internal order), colour-sorted copy
+    std::vector<int64_t> col;
+    int64_t ncol = 0;
+    if (colors) {
+        col.resize((size_t)n_elems);
+        for (int64_t e = 0; e < n_elems; ++e)
+            col[e] = colors[eperm[e]];
+        for (int64_t c : col)
+            ncol = std::max(ncol, c + 1);
+    } else if (opts.build_colors) {
+        std::vector<int64_t> c64((size_t)(4 * n_elems));
+        for (int64_t i = 0; i < 4 * n_elems; ++i)
+            c64[i] = cord[i];
+        col.resize((size_t)n_elems);
+        ncol = color_elements(c64.data(), n_nodes, n_elems, col.data());
+        if (ncol < 0)
+            return fail(TAL_EINVAL, "greedy colouring needs more than 256 colours");
+    }
+    std::vector<int32_t> ccol;
+    if (!col.empty()) {
+        h->col_off.assign((size_t)ncol + 1, 0);
+        for (int64_t c : col)
+            h->col_off[c + 1]++;
+        for (int64_t c = 0; c < ncol; ++c)
+            h->col_off[c + 1] += h->col_off[c];
+        std::vector<int64_t> fill(h->col_off.begin(), h->col_off.end() - 1);
+        ccol.resize((size_t)(4 * n_elems));
+        for (int64_t e = 0; e < n_elems; ++e) {
+            const int64_t d = fill[col[e]]++;
+            for (int a = 0; a < 4; ++a)
+                ccol[4 * d + a] = cord[4 * e + a];
+        }
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+
+    // ---- device upload ----
+    int rc;
+    size_t bytes = 0;
+    TAL_CK(cudaMalloc((void **)&h->nodebuf, sizeof(double) * 9 * std::max<int64_t>(n_nodes, 1)));
+    TAL_CK(cudaMalloc((void **)&h->staging, sizeof(double) * 3 * std::max<int64_t>(n_nodes, 1)));
+    bytes += sizeof(double) * 12 * n_nodes;
+    TAL_CK(cudaMemset(h->nodebuf, 0, sizeof(double) * 9 * std::max<int64_t>(n_nodes, 1)));
+    {
+        std::vector<double> soa((size_t)(3 * n_nodes));
+        for (int64_t i = 0; i < n_nodes; ++i)
+            for (int c = 0; c < 3; ++c)
+                soa[c * n_nodes + i] = xin[3 * i + c];
+        if (n_nodes)
+            TAL_CK(cudaMemcpy(h->nodebuf, soa.data(), sizeof(double) * 3 * n_nodes, cudaMemcpyHostToDevice));
+    }
+    if (renum) {
+        if ((rc = dev_upload(&h->perm, perm.data(), perm.size())))
+            return rc;
+        if ((rc = dev_upload(&h->iperm, iperm.data(), iperm.size())))
+            return rc;
+        bytes += 8 * n_nodes;
+        h->h_iperm.swap(iperm);
+    }
+    if ((rc = dev_upload(&h->conn, (const int4 *)cord.data(), (size_t)n_elems)))
+        return rc;
+    bytes += 16 * n_elems;
+    if (!ccol.empty()) {
+        if ((rc = dev_upload(&h->conn_col, (const int4 *)ccol.data(), (size_t)n_elems)))
+            return rc;
+        bytes += 16 * n_elems;
+    }
+    const Chunking &C = h->ch;
+    if ((rc = dev_upload(&h->d_chunks, (const int4 *)C.chunks.data(), C.chunks.size() / 4)))
+        return rc;
+    if ((rc = dev_upload(&h->d_chunk_nodes, C.chunk_nodes.data(), C.chunk_nodes.size())))
+        return rc;
+    if ((rc = dev_upload(&h->d_csr_off, C.csr_off.data(), C.csr_off.size())))
+        return rc;
+    if ((rc = dev_upload(&h->d_csr_slots, C.csr_slots.data(), C.csr_slots.size())))
+        return rc;
+    if ((rc = dev_upload(&h->d_lconn, (const ushort4 *)C.lconn.data(), C.lconn.size() / 4)))
+        return rc;
+    if ((rc = dev_upload(&h->d_bnd_nodes, C.bnd_nodes.data(), C.bnd_nodes.size())))
+        return rc;
+    if ((rc = dev_upload(&h->d_bnd_off, C.bnd_off.data(), C.bnd_off.size())))
+        return rc;
+    if ((rc = dev_upload(&h->d_bnd_pos, C.bnd_pos.data(), C.bnd_pos.size())))
+        return rc;
+    if (!C.chunk_nodes.empty())
+        TAL_CK(cudaMalloc((void **)&h->d_partial, sizeof(double) * 3 * C.chunk_nodes.size()));
+    bytes += C.chunks.size() * 4 + C.chunk_nodes.size() * (4 + 2 + 24) + C.csr_slots.size() * 2 +
+             C.lconn.size() * 2 + (C.bnd_nodes.size() + C.bnd_off.size() + C.bnd_pos.size()) * 4;
+    h->smem_private = sizeof(double) * (6 * (size_t)C.max_nodes + 12 * (size_t)C.chunk_elems);
+    if ((rc = set_kernel_attrs(h->smem_private)))
+        return rc;
+    TAL_CK(cudaDeviceSynchronize());
+
+    h->has_mesh = true;
+    h->info.n_nodes = n_nodes;
+    h->info.n_elems = n_elems;
+    h->info.n_colors = col.empty() ? 0 : ncol;
+    h->info.n_chunks = (int64_t)C.chunks.size() / 4;
+    h->info.n_chunk_nodes = (int64_t)C.chunk_nodes.size();
+    h->info.n_shared_nodes = C.n_shared;
+    h->info.device_bytes = (int64_t)bytes;
+    h->info.prep_seconds = std::chrono::duration<double>(t1 - t0).count();
+    return TAL_OK;
+}
+
+int tal_mesh_info_get(tal_handle *h, tal_mesh_info *out)
+{
+    if (!h || !out)
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    *out = h->info;
+    return TAL_OK;
+}
+
+int tal_buffers_get(tal_handle *h, tal_buffers *out)
+{
+    if (!h || !out)
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    out->ux = h->UX();
+    out->uy = h->UY();
+    out->uz = h->UZ();
+    out->rx = h->RX();
+    out->ry = h->RY();
+    out->rz = h->RZ();
+    out->perm = h->perm;
+    out->iperm = h->iperm;
+    return TAL_OK;
+}
+
+int tal_set_velocity_device(tal_handle *h, const double *d_u, void *stream)
+{
+    if (!h || (!d_u && h->N))
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    DeviceGuard g(h->device);
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    if (h->N) {
+        k_pack_aos<<<grid_for(h->N, 256), 256, 0, s>>>(d_u, h->perm, h->N, h->UX(), h->UY(), h->UZ());
+        TAL_CK_LAUNCH();
+    }
+    return TAL_OK;
+}
+
+int tal_set_velocity_host(tal_handle *h, const double *u, void *stream)
+{
+    if (!h || (!u && h->N))
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    DeviceGuard g(h->device);
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    if (h->N)
+        TAL_CK(cudaMemcpyAsync(h->staging, u, sizeof(double) * 3 * h->N, cudaMemcpyHostToDevice, s));
+    return tal_set_velocity_device(h, h->staging, s);
+}
+
+int tal_run(tal_handle *h, const tal_params *p, int scatter, void *stream, int64_t *kernel_launches)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    int rc = check_params(p);
+    if (rc)
+        return rc;
+    DeviceGuard g(h->device);
+    return launch_run(h, p, scatter, stream ? (cudaStream_t)stream : h->stream, kernel_launches);
+}
+
+int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream)
+{
+    if (!h || (!d_rhs && h->N))
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    DeviceGuard g(h->device);
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    if (h->N) {
+        k_unpack_aos<<<grid_for(h->N, 256), 256, 0, s>>>(h->RX(), h->RY(), h->RZ(), h->iperm, h->N, d_rhs);
+        TAL_CK_LAUNCH();
+    }
+    return TAL_OK;
+}
+
+int tal_get_rhs_host(tal_handle *h, double *rhs, void *stream)
+{
+    if (!h || (!rhs && h->N))
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    DeviceGuard g(h->device);
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    int rc = tal_get_rhs_device(h, h->staging, s);
+    if (rc)
+        return rc;
+    if (h->N)
+        TAL_CK(cudaMemcpyAsync(rhs, h->staging, sizeof(double) * 3 * h->N, cudaMemcpyDeviceToHost, s));
+    return TAL_OK;
+}
+
+int tal_synchronize(tal_handle *h, void *stream)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    DeviceGuard g(h->device);
+    TAL_CK(cudaStreamSynchronize(stream ? (cudaStream_t)stream : h->stream));
+    return TAL_OK;
+}
+
+int tal_assemble(tal_handle *h, const double *u, const tal_params *p, double *rhs, int scatter,
+                 tal_timings *t)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    if (h->N && (!u || !rhs))
+        return fail(TAL_EINVAL, "NULL field arrays");
+    int rc = check_params(p);
+    if (rc)
+        return rc;
+    DeviceGuard g(h->device);
+    cudaStream_t s = h->stream;
+    const size_t nb = sizeof(double) * 3 * (size_t)h->N;
+    int64_t nl = 0;
+    TAL_CK(cudaEventRecord(h->ev[0], s));
+    if (nb)
+        TAL_CK(cudaMemcpyAsync(h->staging, u, nb, cudaMemcpyHostToDevice, s));
+    TAL_CK(cudaEventRecord(h->ev[1], s));
+    if ((rc = tal_set_velocity_device(h, h->staging, s)))
+        return rc;
+    nl += h->N ? 1 : 0;
+    TAL_CK(cudaEventRecord(h->ev[2], s));
+    int64_t nrun = 0;
+    if ((rc = launch_run(h, p, scatter, s, &nrun)))
+        return rc;
+    nl += nrun;
+    TAL_CK(cudaEventRecord(h->ev[3], s));
+    if ((rc = tal_get_rhs_device(h, h->staging, s)))
+        return rc;
+    nl += h->N ? 1 : 0;
+    TAL_CK(cudaEventRecord(h->ev[4], s));
+    if (nb)
+        TAL_CK(cudaMemcpyAsync(rhs, h->staging, nb, cudaMemcpyDeviceToHost, s));
+    TAL_CK(cudaEventRecord(h->ev[5], s));
+    TAL_CK(cudaEventSynchronize(h->ev[5]));
+    float ms[5];
+    for (int i = 0; i < 5; ++i)
+        TAL_CK(cudaEventElapsedTime(&ms[i], h->ev[i], h->ev[i + 1]));
+    tal_timings tt;
+    tt.h2d_ms = ms[0];
+    tt.pack_ms = ms[1];
+    tt.kernel_ms = ms[2];
+    tt.unpack_ms = ms[3];
+    tt.d2h_ms = ms[4];
+    float tot = 0.f;
+    TAL_CK(cudaEventElapsedTime(&tot, h->ev[0], h->ev[5]));
+    tt.total_ms = tot;
+    tt.kernel_launches = nl;
+    h->last = tt;
+    if (t)
+        *t = tt;
+    return TAL_OK;
+}
+
+int tal_assemble_elements(int device, const double *coords, const int64_t *conn, int64_t n_nodes,
+                          int64_t n_elems, const double *u, double rho, double mu, double cvre,
+                          const double *pmat, const int64_t *ids, int64_t k, double *rhs)
+{
+    if (n_nodes < 0 || n_elems < 0 || k < 0)
+        return fail(TAL_EINVAL, "negative sizes");
+    if (k == 0 || n_nodes == 0)
+        return TAL_OK;
+    if (!coords || !conn || !u || !pmat || !ids || !rhs)
+        return fail(TAL_EINVAL, "NULL arrays");
+    if (n_nodes >= (int64_t)1 << 31)
+        return fail(TAL_EINVAL, "too many nodes");
+    std::vector<int32_t> sub((size_t)(4 * k));
+    for (int64_t t = 0; t < k; ++t) {
+        if (ids[t] < 0 || ids[t] >= n_elems)
+            return fail(TAL_EINVAL, "element id out of range");
+        for (int a = 0; a < 4; ++a) {
+            const int64_t v = conn[4 * ids[t] + a];
+            if (v < 0 || v >= n_nodes)
+                return fail(TAL_EINVAL, "connectivity index out of range [0, n_nodes)");
+            sub[4 * t + a] = (int32_t)v;
+        }
+    }
+    tal_params p;
+    p.rho = rho;
+    p.mu = mu;
+    p.c_vreman = cvre;
+    std::memcpy(p.pmat, pmat, sizeof p.pmat);
+    int rc = check_params(&p);
+    if (rc)
+        return rc;
+    ElemConsts kc;
+    bool sym;
+    make_consts(&p, kc, sym);
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        return fail(TAL_ECUDA, "no CUDA device available; the assembly has no CPU fallback");
+    if (device < 0 || device >= n)
+        return fail(TAL_EINVAL, "device index out of range");
+    DeviceGuard g(device);
+    std::vector<double> soa((size_t)(6 * n_nodes));
+    for (int64_t i = 0; i < n_nodes; ++i)
+        for (int c = 0; c < 3; ++c) {
+            soa[c * n_nodes + i] = coords[3 * i + c];
+            soa[(3 + c) * n_nodes + i] = u[3 * i + c];
+        }
+    double *buf = nullptr;
+    int4 *dconn = nullptr;
+    TAL_CK(cudaMalloc((void **)&buf, sizeof(double) * 9 * n_nodes));
+    rc = TAL_OK;
+    do {
+        cudaError_t e;
+        if ((e = cudaMalloc((void **)&dconn, sizeof(int4) * k)) != cudaSuccess ||
+            (e = cudaMemcpy(buf, soa.data(), sizeof(double) * 6 * n_nodes, cudaMemcpyHostToDevice)) !=
+                cudaSuccess ||
+            (e = cudaMemset(buf + 6 * n_nodes, 0, sizeof(double) * 3 * n_nodes)) != cudaSuccess ||
+            (e = cudaMemcpy(dconn, sub.data(), sizeof(int4) * k, cudaMemcpyHostToDevice)) != cudaSuccess) {
+            rc = fail(TAL_ECUDA, std::string("assemble_elements upload: ") + cudaGetErrorString(e));
+            break;
+        }
+        NodeSoA nodes{buf, buf + n_nodes, buf + 2 * n_nodes, buf + 3 * n_nodes, buf + 4 * n_nodes,
+                      buf + 5 * n_nodes};
+        RhsSoA r{buf + 6 * n_nodes, buf + 7 * n_nodes, buf + 8 * n_nodes};
+        if (sym)
+            k_assemble_atomic<true><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc);
+        else
+            k_assemble_atomic<false><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc);
+        if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
+            rc = fail(TAL_ECUDA, std::string("assemble_elements kernel: ") + cudaGetErrorString(e));
+            break;
+        }
+        if ((e = cudaMemcpy(soa.data(), buf + 6 * n_nodes, sizeof(double) * 3 * n_nodes,
+                            cudaMemcpyDeviceToHost)) != cudaSuccess) {
+            rc = fail(TAL_ECUDA, std::string("assemble_elements download: ") + cudaGetErrorString(e));
+            break;
+        }
+        for (int64_t i = 0; i < n_nodes; ++i)
+            for (int c = 0; c < 3; ++c)
+                rhs[3 * i + c] += soa[c * n_nodes + i];
+    } while (0);
+    cudaFree(buf);
+    if (dconn)
+        cudaFree(dconn);
+    return rc;
+}
+
+int tal_halo_pack(tal_handle *h, const int32_t *d_list, int64_t n, double *d_out, void *stream)
+{
+    if (!h || n < 0 || (n && (!d_list || !d_out)))
+        return fail(TAL_EINVAL, "bad arguments");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    if (!n)
+        return TAL_OK;
+    DeviceGuard g(h->device);
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    k_halo_pack<<<grid_for(n, 256), 256, 0, s>>>(d_list, n, h->RX(), h->RY(), h->RZ(), d_out);
+    TAL_CK_LAUNCH();
+    return TAL_OK;
+}
+
+int tal_halo_accumulate(tal_handle *h, const int32_t *d_list, int64_t n, const double *d_in, void *stream)
+{
+    if (!h || n < 0 || (n && (!d_list || !d_in)))
+        return fail(TAL_EINVAL, "bad arguments");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    if (!n)
+        return TAL_OK;
+    DeviceGuard g(h->device);
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    k_halo_accumulate<<<grid_for(n, 256), 256, 0, s>>>(d_list, n, d_in, h->RX(), h->RY(), h->RZ());
+    TAL_CK_LAUNCH();
+    return TAL_OK;
+}
+
+int tal_map_nodes(tal_handle *h, const int64_t *caller_ids, int64_t n, int32_t *internal_ids)
+{
+    if (!h || n < 0 || (n && (!caller_ids || !internal_ids)))
+        return fail(TAL_EINVAL, "bad arguments");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t v = caller_ids[i];
+        if (v < 0 || v >= h->N)
+            return fail(TAL_EINVAL, "node id out of range");
+        internal_ids[i] = h->h_iperm.empty() ? (int32_t)v : h->h_iperm[v];
+    }
+    return TAL_OK;
+}
+
+int tal_box_mesh(int64_t nx, int64_t ny, int64_t nz, double ex, double ey, double ez, double *coords,
+                 int64_t *conn)
+{
+    if (nx < 1 || ny < 1 || nz < 1)
+        return fail(TAL_EINVAL, "box dimensions must be positive");
+    if (!(ex > 0.0 && ey > 0.0 && ez > 0.0))
+        return fail(TAL_EINVAL, "extents must be 3 positive lengths");
+    if (!coords || !conn)
+        return fail(TAL_EINVAL, "NULL output arrays");
+    box_mesh(nx, ny, nz, ex, ey, ez, coords, conn);
+    return TAL_OK;
+}
+
+int tal_signed_volumes(const double *coords, const int64_t *conn, int64_t n_elems, double *vols)
+{
+    if (n_elems < 0 || (n_elems && (!coords || !conn || !vols)))
+        return fail(TAL_EINVAL, "bad arguments");
+    signed_volumes(coords, conn, n_elems, vols);
+    return TAL_OK;
+}
+
+int tal_color_elements(const int64_t *conn, int64_t n_nodes, int64_t n_elems, int64_t *colors,
+                       int64_t *n_colors)
+{
+    if (n_elems < 0 || n_nodes < 0 || (n_elems && (!conn || !colors)) || !n_colors)
+        return fail(TAL_EINVAL, "bad arguments");
+    const int64_t nc = color_elements(conn, n_nodes, n_elems, colors);
+    if (nc < 0)
+        return fail(TAL_EINVAL, "greedy colouring needs more than 256 colours");
+    *n_colors = nc;
+    return TAL_OK;
+}
+
+int tal_check_coloring(const int64_t *conn, const int64_t *colors, int64_t n_nodes, int64_t n_elems,
+                       int *valid)
+{
+    if (!valid || n_elems < 0 || (n_elems && (!conn || !colors)))
+        return fail(TAL_EINVAL, "bad arguments");
+    *valid = check_coloring(conn, colors, n_nodes, n_elems) ? 1 : 0;
+    return TAL_OK;
+}
+
+int tal_renumber_nodes(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
+                       int method, int64_t *perm_out)
+{
+    if (n_nodes < 0 || n_elems < 0 || !perm_out)
+        return fail(TAL_EINVAL, "bad arguments");
+    std::vector<int32_t> perm;
+    if (method == TAL_RENUMBER_RCM)
+        renumber_rcm(conn, n_nodes, n_elems, perm);
+    else if (method == TAL_RENUMBER_SFC)
+        renumber_sfc(coords, n_nodes, perm);
+    else if (method == TAL_RENUMBER_NONE) {
+        for (int64_t i = 0; i < n_nodes; ++i)
+            perm_out[i] = i;
+        return TAL_OK;
+    } else
+        return fail(TAL_EINVAL, "unknown renumber method");
+    for (int64_t i = 0; i < n_nodes; ++i)
+        perm_out[i] = perm[i];
+    return TAL_OK;
+}
+
+int tal_profile(tal_handle *h, int enable)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    DeviceGuard g(h->device);
+    if (enable && h->prof_ev.empty()) {
+        h->prof_ev.resize(2 * tal_handle::PROF_RING);
+        for (auto &ev : h->prof_ev)
+            TAL_CK(cudaEventCreate(&ev));
+    }
+    h->prof_on = enable != 0;
+    h->prof_head = h->prof_count = 0;
+    return TAL_OK;
+}
+
+int tal_profile_read(tal_handle *h, double *ms_out, int64_t cap, int64_t *n_out)
+{
+    if (!h || !n_out || cap < 0 || (cap && !ms_out))
+        return fail(TAL_EINVAL, "bad arguments");
+    DeviceGuard g(h->device);
+    int64_t n = 0;
+    while (h->prof_count > 0 && n < cap) {
+        const int64_t slot = h->prof_head;
+        TAL_CK(cudaEventSynchronize(h->prof_ev[2 * slot + 1]));
+        float ms = 0.f;
+        TAL_CK(cudaEventElapsedTime(&ms, h->prof_ev[2 * slot], h->prof_ev[2 * slot + 1]));
+        ms_out[n++] = ms;
+        h->prof_head = (h->prof_head + 1) % tal_handle::PROF_RING;
+        --h->prof_count;
+    }
+    *n_out = n;
+    return TAL_OK;
+}
+
+int tal_fp64_peak(int device, double ms_target, double *tflops, double *sm_clock_mhz)
+{
+    if (!tflops)
+        return fail(TAL_EINVAL, "NULL output");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n)
+        return fail(TAL_ECUDA, "no such CUDA device");
+    DeviceGuard g(device);
+    cudaDeviceProp prop;
+    TAL_CK(cudaGetDeviceProperties(&prop, device));
+    const int blocks = prop.multiProcessorCount * 8, threads = 256;
+    double *out = nullptr;
+    TAL_CK(cudaMalloc((void **)&out, sizeof(double) * blocks));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    int iters = 64;
+    float ms = 0.f;
+    k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);  // warm-up
+    for (int rep = 0; rep < 12; ++rep) {
+        cudaEventRecord(a);
+        k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms >= ms_target)
+            break;
+        iters = (int)std::min<double>(iters * std::max(2.0, 1.2 * ms_target / std::max(ms, 1e-3f)), 1 << 26);
+    }
+    // best of 3 at the final size
+    float best = ms;
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(a);
+        k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        best = std::min(best, ms);
+    }
+    cudaError_t e = cudaGetLastError();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    if (e != cudaSuccess)
+        return fail(TAL_ECUDA, std::string("fp64 probe: ") + cudaGetErrorString(e));
+    const double flops = 2.0 * 16.0 * 8.0 * (double)iters * blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    if (sm_clock_mhz) {
+        // 64 DFMA lanes/SM/clk on sm_100 -> implied clock
+        *sm_clock_mhz = (*tflops * 1e12) / (2.0 * 64.0 * prop.multiProcessorCount) / 1e6;
+    }
+    return TAL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,161 @@
+// tal_element.cuh -- per-element momentum RHS of a linear tetrahedron, in
+// registers, specialised for 4 nodes and the folded 4-point Gauss rule.
+//
+// Operator (reference: _rsp_kernels.py:33-164, kernel.py:146-170):
+//   r_a[i] = -rho * int N_a (u.grad) u_i  -  (mu + rho nu_t) int gradN_a . grad u_i
+// with nu_t the Vreman closure (kernel.py:99-143) on the constant element
+// gradient and filter width cbrt(6 vol) = cbrt(|det|).
+//
+// B200 restructuring (same mathematics, fewer FP64 instructions; the parity
+// bound is 1e-12 of the max-norm, not bitwise):
+//  * Shape gradients are never divided out.  With cofactor rows c_b
+//    (b=1..3; c_0 = -sum) and D = det, G = Gh / D where
+//        Gh[k][i] = sum_{b=1..3} c_b[k] (u_b[i] - u_0[i]).
+//  * Vreman in the unscaled quantities: with aa = |G|^2, ssq = sum of the
+//    nine squared 2x2 minors of G (the Cauchy-Binet form the reference uses),
+//        nu_t = c * sqrt(delta^4 ssq / aa) = c * rcbrt(|D|) * sqrt(ssqh / aah)
+//    because delta^2 / |D| = |D|^(-1/3); the quiescent guard aa <= 1e-30
+//    (kernel.py:24) is tested as aah * (1/|D|)^2 <= 1e-30.
+//  * pmat = P^T P of the symmetric rule has one diagonal value pd and one
+//    off-diagonal value po, so the velocity moments are
+//        m_a = po * S + (pd - po) * u_a,  S = sum_b u_b.
+//  * Both terms share Gh:  r_a[i] = sum_k w_a[k] Gh[k][i] with
+//        w_a = A (po S + (pd-po) u_a) + B c_a,
+//        A = nrv / D = -rho sgn(D) / 24,   B = nvv / D^2 = -vis / (6 |D|).
+// About 215 FP64 instructions per element (FMA = 1) against the reference
+// ledger's 448 flop (variants.py:207-217).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace tal {
+
+struct ElemConsts {
+    double rho, mu, cvre;
+    double a_po;  // -rho * po / 24
+    double a_q;   // -rho * (pd - po) / 24
+    double pm[16];  // full pmat (general kernel only)
+};
+
+__device__ __forceinline__ void cross3(const double a[3], const double b[3], double c[3])
+{
+    c[0] = fma(a[1], b[2], -a[2] * b[1]);
+    c[1] = fma(a[2], b[0], -a[0] * b[2]);
+    c[2] = fma(a[0], b[1], -a[1] * b[0]);
+}
+
+// Shared geometry + gradient + Vreman part.  Returns Gh, cofactors c[0..3],
+// and the scalars A (signed) and B.
+__device__ __forceinline__ void element_core(const double X[4][3], const double U[4][3],
+                                             const ElemConsts &k, double cf[4][3],
+                                             double Gh[3][3], double &sg, double &B)
+{
+    double e[3][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            e[b][c] = X[b + 1][c] - X[0][c];
+    cross3(e[1], e[2], cf[1]);  // e2 x e3
+    cross3(e[2], e[0], cf[2]);  // e3 x e1
+    cross3(e[0], e[1], cf[3]);  // e1 x e2
+    const double det = fma(e[0][0], cf[1][0], fma(e[0][1], cf[1][1], e[0][2] * cf[1][2]));
+    const double ad = fabs(det);
+    const double inv = __drcp_rn(ad);
+    sg = (det < 0.0) ? -1.0 : 1.0;
+
+    double du[3][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            du[b][i] = U[b + 1][i] - U[0][i];
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            Gh[kk][i] = fma(cf[1][kk], du[0][i], fma(cf[2][kk], du[1][i], cf[3][kk] * du[2][i]));
+
+    // |Gh|^2 and the nine squared 2x2 minors (rows m<n, columns i<j)
+    double aah = Gh[0][0] * Gh[0][0];
+#pragma unroll
+    for (int q = 1; q < 9; ++q)
+        aah = fma(Gh[q / 3][q % 3], Gh[q / 3][q % 3], aah);
+    double ssqh = 0.0;
+#pragma unroll
+    for (int cp = 0; cp < 3; ++cp) {
+        const int ci = (cp == 2) ? 1 : 0, cj = (cp == 0) ? 1 : 2;
+#pragma unroll
+        for (int rp = 0; rp < 3; ++rp) {
+            const int m = (rp == 2) ? 1 : 0, n = (rp == 0) ? 1 : 2;
+            const double d = fma(Gh[m][ci], Gh[n][cj], -(Gh[m][cj] * Gh[n][ci]));
+            ssqh = fma(d, d, ssqh);
+        }
+    }
+    double nut = 0.0;
+    if (aah * inv * inv > 1e-30) {  // kernel.py:24 guard, in G units
+        nut = k.cvre * rcbrt(ad) * sqrt(ssqh * __drcp_rn(aah));
+    }
+    const double vis = fma(k.rho, nut, k.mu);
+    B = vis * (inv * (-1.0 / 6.0));
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        cf[0][c] = -(cf[1][c] + cf[2][c] + cf[3][c]);
+}
+
+// Symmetric-rule element (pmat = po * ones + (pd - po) * I).
+__device__ __forceinline__ void element_rhs_sym(const double X[4][3], const double U[4][3],
+                                                const ElemConsts &k, double R[4][3])
+{
+    double cf[4][3], Gh[3][3], sg, B;
+    element_core(X, U, k, cf, Gh, sg, B);
+    const double As = sg * k.a_po, Aq = sg * k.a_q;
+    double AsS[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        AsS[c] = As * ((U[0][c] + U[1][c]) + (U[2][c] + U[3][c]));
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        double w[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            w[c] = fma(Aq, U[a][c], fma(B, cf[a][c], AsS[c]));
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            R[a][i] = fma(w[0], Gh[0][i], fma(w[1], Gh[1][i], w[2] * Gh[2][i]));
+    }
+}
+
+// General pmat (any 4x4 interpolation table): m_a = sum_b pmat[a][b] u_b.
+__device__ __forceinline__ void element_rhs_gen(const double X[4][3], const double U[4][3],
+                                                const ElemConsts &k, double R[4][3])
+{
+    double cf[4][3], Gh[3][3], sg, B;
+    element_core(X, U, k, cf, Gh, sg, B);
+    const double A = sg * (-k.rho / 24.0);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        double w[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double m = fma(k.pm[4 * a + 0], U[0][c],
+                                 fma(k.pm[4 * a + 1], U[1][c],
+                                     fma(k.pm[4 * a + 2], U[2][c], k.pm[4 * a + 3] * U[3][c])));
+            w[c] = fma(A, m, B * cf[a][c]);
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            R[a][i] = fma(w[0], Gh[0][i], fma(w[1], Gh[1][i], w[2] * Gh[2][i]));
+    }
+}
+
+template <bool SYM>
+__device__ __forceinline__ void element_rhs(const double X[4][3], const double U[4][3],
+                                            const ElemConsts &k, double R[4][3])
+{
+    if constexpr (SYM)
+        element_rhs_sym(X, U, k, R);
+    else
+        element_rhs_gen(X, U, k, R);
+}
+
+}  // namespace tal

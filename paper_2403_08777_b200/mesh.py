@@ -1,0 +1,146 @@
+"""Tetrahedral mesh value type and native generators.
+
+Mirrors the reference's mesh layer (``mesh.py`` of tet-assembly-lab 0.1.0):
+``Mesh`` (mesh.py:36-89) with the same fields, validation and immutability,
+``generate_box_mesh`` (mesh.py:145-184), ``signed_volumes`` (mesh.py:110-123),
+``color_elements`` (mesh.py:235-257).  The per-element loops run in the
+native library (C++), not in Python.  ``assemble_rsp`` accepts this Mesh or
+the reference's own ``tet_assembly_lab.Mesh`` (anything with ``coords``,
+``connectivity`` and optional ``colors``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, replace
+from typing import Optional
+
+import numpy as np
+
+from ._native import check, lib, ptr
+
+VOLUME_EPSILON = 1e-300  # mesh.py:20
+
+
+@dataclass(frozen=True)
+class Mesh:
+    """coords (n_nodes,3) f64; connectivity (n_elems,4) int64, positively
+    oriented; optional colors (n_elems,) int64 with no two node-sharing
+    elements in one colour."""
+
+    coords: np.ndarray
+    connectivity: np.ndarray
+    colors: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        coords = np.ascontiguousarray(self.coords, dtype=np.float64)
+        conn = np.ascontiguousarray(self.connectivity, dtype=np.int64)
+        if coords.ndim != 2 or coords.shape[1] != 3:
+            raise ValueError(f"coords must have shape (n_nodes, 3), got {coords.shape}")
+        if conn.ndim != 2 or conn.shape[1] != 4:
+            raise ValueError(f"connectivity must have shape (n_elems, 4), got {conn.shape}")
+        if conn.size and (conn.min() < 0 or conn.max() >= coords.shape[0]):
+            raise ValueError("connectivity index out of range [0, n_nodes)")
+        vols = signed_volumes(coords, conn)
+        if vols.size and vols.min() <= 0.0:
+            bad = int(np.argmin(vols))
+            raise ValueError(f"element {bad} has non-positive signed volume {vols[bad]:g}")
+        colors = self.colors
+        if colors is not None:
+            colors = np.ascontiguousarray(colors, dtype=np.int64)
+            if colors.shape != (conn.shape[0],):
+                raise ValueError("colors must be one index per element")
+            if not check_coloring(conn, colors, coords.shape[0]):
+                raise ValueError("coloring invalid: elements sharing a node share a color")
+            colors.setflags(write=False)
+        for name, arr in (("coords", coords), ("connectivity", conn), ("colors", colors)):
+            if arr is not None:
+                arr.setflags(write=False)
+            object.__setattr__(self, name, arr)
+
+    @property
+    def n_nodes(self) -> int:
+        return self.coords.shape[0]
+
+    @property
+    def n_elems(self) -> int:
+        return self.connectivity.shape[0]
+
+    @property
+    def n_colors(self) -> Optional[int]:
+        if self.colors is None:
+            return None
+        return int(self.colors.max()) + 1 if self.colors.size else 0
+
+    __hash__ = object.__hash__
+    __eq__ = object.__eq__
+
+
+def signed_volumes(coords: np.ndarray, connectivity: np.ndarray) -> np.ndarray:
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    conn = np.ascontiguousarray(connectivity, dtype=np.int64)
+    out = np.empty(conn.shape[0])
+    if conn.shape[0]:
+        check(lib().tal_signed_volumes(ptr(coords), ptr(conn), conn.shape[0], ptr(out)))
+    return out
+
+
+def check_coloring(conn: np.ndarray, colors: np.ndarray, n_nodes: int) -> bool:
+    v = ctypes.c_int(0)
+    check(lib().tal_check_coloring(ptr(conn), ptr(colors), n_nodes, conn.shape[0], ctypes.byref(v)))
+    return bool(v.value)
+
+
+def _box_arrays(nx: int, ny: int, nz: int, extents=(1.0, 1.0, 1.0)):
+    for name, v in (("nx", nx), ("ny", ny), ("nz", nz)):
+        if int(v) != v or v < 1:
+            raise ValueError(f"{name} must be a positive integer, got {v!r}")
+    nx, ny, nz = int(nx), int(ny), int(nz)
+    ext = np.asarray(extents, dtype=np.float64)
+    if ext.shape != (3,) or not np.all(ext > 0.0):
+        raise ValueError(f"extents must be 3 positive lengths, got {extents!r}")
+    coords = np.empty(((nx + 1) * (ny + 1) * (nz + 1), 3))
+    conn = np.empty((6 * nx * ny * nz, 4), dtype=np.int64)
+    check(lib().tal_box_mesh(nx, ny, nz, float(ext[0]), float(ext[1]), float(ext[2]),
+                             ptr(coords), ptr(conn)))
+    return coords, conn
+
+
+def generate_box_mesh(nx: int, ny: int, nz: int, extents=(1.0, 1.0, 1.0)) -> Mesh:
+    """Structured box of nx*ny*nz hex cells, each split into 6 tetrahedra
+    (Kuhn split), nodes x-fastest, cell c -> elements 6c..6c+5."""
+    coords, conn = _box_arrays(nx, ny, nz, extents)
+    return Mesh(coords=coords, connectivity=conn)
+
+
+def color_elements(mesh) -> Mesh:
+    """Greedy lowest-free colouring in element order (mesh.py:235-257)."""
+    conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int64)
+    colors = np.empty(conn.shape[0], dtype=np.int64)
+    nc = ctypes.c_int64(0)
+    check(lib().tal_color_elements(ptr(conn), mesh.coords.shape[0], conn.shape[0], ptr(colors),
+                                   ctypes.byref(nc)))
+    if isinstance(mesh, Mesh):
+        return replace(mesh, colors=colors)
+    return Mesh(coords=mesh.coords, connectivity=conn, colors=colors)
+
+
+def renumber_nodes(mesh, method: str = "rcm") -> np.ndarray:
+    """Node permutation perm[new] = old (rcm | sfc | none)."""
+    from ._native import RENUMBER
+    if method not in RENUMBER:
+        raise ValueError(f"unknown renumber method {method!r}")
+    coords = np.ascontiguousarray(mesh.coords, dtype=np.float64)
+    conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int64)
+    perm = np.empty(coords.shape[0], dtype=np.int64)
+    check(lib().tal_renumber_nodes(ptr(coords), ptr(conn), coords.shape[0], conn.shape[0],
+                                   RENUMBER[method], ptr(perm)))
+    return perm
+
+
+def permute_nodes(mesh, perm: np.ndarray) -> Mesh:
+    """Mesh with node i' = perm[i'] of the input."""
+    perm = np.asarray(perm, dtype=np.int64)
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.size)
+    return Mesh(coords=np.asarray(mesh.coords)[perm], connectivity=inv[np.asarray(mesh.connectivity)])

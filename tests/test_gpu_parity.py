@@ -1,0 +1,293 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle and
+the reference's golden vectors.  Run on a B200 with ``pytest -m gpu``.
+
+Criteria (oracle.compare): the reference's max|d|/denominator <= 1e-12
+(variants.py:62-65, 653-711) AND north_star's rel-L2 <= 1e-12 and
+max|d| <= 1e-10 * ||oracle||_inf.  Atomic scatter is compared with these
+tolerances; 'private' and 'colored' must additionally rerun bitwise.
+"""
+import numpy as np
+import pytest
+
+import paper_2403_08777_b200 as tb
+from conftest import INITS, SMALL_DIMS, dims_key, init_key
+
+pytestmark = pytest.mark.gpu
+
+MODES = ["private", "private-atomic", "atomic", "colored"]
+P = tb.PhysParams()
+
+
+def run(mesh, u, params=P, **cfg):
+    return tb.assemble_rsp(mesh, u, params, tb.RunConfig(**cfg))
+
+
+def assert_parity(oracle, rhs, ref, mesh, u, params=P):
+    chk = oracle.compare(rhs, ref, mesh.coords, mesh.connectivity, u, params.rho, params.mu,
+                         params.c_vreman)
+    assert chk.passed, chk
+    return chk
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("init", INITS)
+@pytest.mark.parametrize("dims", SMALL_DIMS)
+def test_small_boxes_against_reference_goldens(oracle, golden_small, dims, init, mode):
+    m = tb.generate_box_mesh(*dims)
+    k, ik = dims_key(dims), init_key(init)
+    u = golden_small[f"u_{k}_{ik}"]
+    res = run(m, u, scatter=mode)
+    assert_parity(oracle, res.rhs, golden_small[f"oracle_{k}_{ik}"], m, u)
+    assert_parity(oracle, res.rhs, golden_small[f"rsp_{k}_{ik}"], m, u)
+
+
+@pytest.mark.parametrize("renumber", ["none", "rcm", "sfc"])
+@pytest.mark.parametrize("order", ["keep", "node", "sfc"])
+def test_renumbering_and_element_order(oracle, golden_mid, renumber, order):
+    m = tb.generate_box_mesh(8, 8, 8)
+    u = tb.make_velocity(m, "random:1")
+    for mode in MODES:
+        res = run(m, u, scatter=mode, renumber=renumber, element_order=order)
+        assert_parity(oracle, res.rhs, golden_mid["oracle_8_random"], m, u)
+
+
+@pytest.mark.parametrize("ce,cn", [(1, 4), (7, 16), (64, 128), (512, 1024), (1024, 2048),
+                                   (1024, 64)])
+def test_chunk_shape_invariance(oracle, golden_mid, ce, cn):
+    m = tb.generate_box_mesh(16, 16, 16)
+    u = tb.make_velocity(m, "taylor-green")
+    ref = golden_mid["rsp_16_taylor-green"]
+    for mode in ("private", "private-atomic"):
+        res = run(m, u, scatter=mode, chunk_elems=ce, chunk_nodes=cn)
+        assert_parity(oracle, res.rhs, ref, m, u)
+
+
+def test_mid_size_goldens(oracle, golden_mid):
+    for n in (8, 16):
+        m = tb.generate_box_mesh(n, n, n)
+        for init in ("random:1", "taylor-green"):
+            u = tb.make_velocity(m, init)
+            for mode in MODES:
+                rhs = run(m, u, scatter=mode).rhs
+                assert_parity(oracle, rhs, golden_mid[f"rsp_{n}_{init_key(init)}"], m, u)
+
+
+def test_32cubed_checksums(oracle, golden_checksums):
+    m = tb.generate_box_mesh(32, 32, 32)
+    for init in ("taylor-green", "random:1"):
+        u = tb.make_velocity(m, init)
+        ref = oracle.assemble_rsp(m.coords, m.connectivity, u, n_threads=oracle.default_threads())
+        s, sa, mx = golden_checksums[f"sum_32_{init_key(init)}"]
+        for mode in MODES:
+            rhs = run(m, u, scatter=mode).rhs
+            assert_parity(oracle, rhs, ref, m, u)
+            assert abs(np.abs(rhs).sum() - sa) <= 1e-12 * sa
+            assert abs(np.abs(rhs).max() - mx) <= 1e-12 * mx
+
+
+@pytest.mark.parametrize("mode", ["private", "colored"])
+def test_bitwise_reruns(mode):
+    m = tb.generate_box_mesh(12, 10, 9)
+    u = tb.make_velocity(m, "random:3")
+    a = run(m, u, scatter=mode).rhs
+    for _ in range(3):
+        np.testing.assert_array_equal(run(m, u, scatter=mode).rhs, a)
+
+
+def test_modes_agree():
+    m = tb.generate_box_mesh(10, 11, 12)
+    u = tb.make_velocity(m, "random:7")
+    base = run(m, u, scatter="private").rhs
+    scale = np.abs(base).max()
+    for mode in MODES[1:]:
+        assert np.abs(run(m, u, scatter=mode).rhs - base).max() <= 1e-12 * scale
+
+
+def test_reference_tet_single_element(oracle, golden_small):
+    m = tb.Mesh(coords=golden_small["reftet_coords"], connectivity=golden_small["reftet_conn"])
+    u = golden_small["reftet_u"]
+    for mode in MODES:
+        rhs = run(m, u, scatter=mode).rhs
+        assert_parity(oracle, rhs, golden_small["reftet_oracle"], m, u)
+
+
+def test_linear_field_analytic(golden_small):
+    """u=(x,0,0), rho=mu=1, c=0 on the reference tet (test_kernel.py:205-223)."""
+    m = tb.Mesh(coords=golden_small["reftet_coords"], connectivity=golden_small["reftet_conn"])
+    p = tb.PhysParams(rho=1.0, mu=1.0, c_vreman=0.0)
+    rhs = run(m, golden_small["reftet_linx_u"], p).rhs
+    np.testing.assert_allclose(rhs, golden_small["reftet_linx_oracle"], rtol=1e-13, atol=1e-18)
+
+
+def test_nondefault_physics(oracle, golden_small):
+    m = tb.generate_box_mesh(3, 3, 3)
+    rho, mu, cv = golden_small["phys_params"]
+    p = tb.PhysParams(rho=float(rho), mu=float(mu), c_vreman=float(cv))
+    u = golden_small["phys_u"]
+    for mode in MODES:
+        assert_parity(oracle, run(m, u, p, scatter=mode).rhs, golden_small["phys_oracle"], m, u, p)
+
+
+def test_permuted_numbering(oracle, golden_small):
+    m = tb.Mesh(coords=golden_small["perm6_coords"], connectivity=golden_small["perm6_conn"])
+    u = golden_small["perm6_u"]
+    for renumber in ("none", "rcm", "sfc"):
+        rhs = run(m, u, renumber=renumber).rhs
+        assert_parity(oracle, rhs, golden_small["perm6_oracle"], m, u)
+
+
+def test_translation_invariance(golden_small):
+    m = tb.generate_box_mesh(3, 3, 3)
+    sh = tb.Mesh(coords=m.coords + np.array([10.0, -20.0, 5.0]), connectivity=m.connectivity)
+    u = golden_small["shift_u"]
+    a, b = run(m, u).rhs, run(sh, u).rhs
+    assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
+
+
+def test_zero_and_constant_fields_exact():
+    m = tb.generate_box_mesh(4, 3, 5)
+    for spec in ("zero", "constant:0.9,0.1,-0.4"):
+        u = tb.make_velocity(m, spec)
+        for mode in MODES:
+            np.testing.assert_array_equal(run(m, u, scatter=mode).rhs, np.zeros((m.n_nodes, 3)))
+
+
+def test_shear_field_has_no_eddy_viscosity():
+    """Rank-1 gradient -> nu_t = 0 exactly (kernel.py:104-111): c_vreman is inert."""
+    m = tb.generate_box_mesh(5, 5, 5)
+    u = tb.make_velocity(m, "shear:1.5")
+    a = run(m, u, tb.PhysParams(c_vreman=0.07), scatter="private").rhs
+    b = run(m, u, tb.PhysParams(c_vreman=0.0), scatter="private").rhs
+    np.testing.assert_array_equal(a, b)
+
+
+def test_empty_mesh():
+    m = tb.Mesh(coords=np.array([[0.0, 0, 0], [1.0, 0, 0]]), connectivity=np.zeros((0, 4), np.int64))
+    for mode in MODES:
+        np.testing.assert_array_equal(run(m, np.zeros((2, 3)), scatter=mode).rhs, np.zeros((2, 3)))
+
+
+def test_isolated_nodes_are_zero(oracle):
+    """A node no element touches gets 0 in every mode (private merge writes it)."""
+    base = tb.generate_box_mesh(3, 3, 3)
+    coords = np.vstack([base.coords, [[5.0, 5.0, 5.0]]])
+    m = tb.Mesh(coords=coords, connectivity=base.connectivity)
+    u = np.random.default_rng(0).uniform(-1, 1, (m.n_nodes, 3))
+    ref = oracle.assemble_rsp(m.coords, m.connectivity, u)
+    for mode in MODES:
+        rhs = run(m, u, scatter=mode).rhs
+        assert np.all(rhs[-1] == 0.0)
+        assert_parity(oracle, rhs, ref, m, u)
+
+
+def test_precolored_mesh(oracle):
+    m = tb.color_elements(tb.generate_box_mesh(4, 4, 4))
+    u = tb.make_velocity(m, "random:2")
+    ref = oracle.assemble_rsp(m.coords, m.connectivity, u)
+    assert_parity(oracle, run(m, u, scatter="colored").rhs, ref, m, u)
+
+
+def test_general_pmat_kernel(oracle):
+    """A non-symmetric interpolation table takes the general-moment kernel."""
+    m = tb.generate_box_mesh(4, 3, 3)
+    u = tb.make_velocity(m, "random:5")
+    pm = np.random.default_rng(3).uniform(0.0, 0.5, (4, 4))
+    ids = np.arange(m.n_elems, dtype=np.int64)
+    ref = np.zeros((m.n_nodes, 3))
+    oracle.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, ref)
+    asm = tb.Assembler(m, tb.RunConfig())
+    rhs = np.empty((m.n_nodes, 3))
+    asm.assemble_into(u, P, rhs, "private", pmat=pm)
+    assert_parity(oracle, rhs, ref, m, u)
+    asm.close()
+
+
+def test_assemble_elements_seam_accumulates(oracle):
+    """Mirror of _rsp_kernels.assemble_elements: subset ids, += into rhs."""
+    m = tb.generate_box_mesh(4, 4, 3)
+    u = tb.make_velocity(m, "random:8")
+    pm = tb.interpolation_table()
+    ids = np.arange(1, m.n_elems, 3, dtype=np.int64)
+    start = np.random.default_rng(1).uniform(-1, 1, (m.n_nodes, 3))
+    ref = start.copy()
+    oracle.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, ref)
+    got = start.copy()
+    tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, got)
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    with pytest.raises(ValueError):
+        tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm,
+                             np.array([m.n_elems]), got)
+
+
+def test_device_resident_path_and_torch_views(oracle):
+    import torch
+    m = tb.generate_box_mesh(9, 8, 7)
+    u = tb.make_velocity(m, "random:4")
+    asm = tb.Assembler(m, tb.RunConfig())
+    rhs_host, _ = asm.assemble(u, P)
+    asm.set_velocity_host(u)
+    nl = asm.run(P)
+    assert nl >= 1
+    out = asm.get_rhs_host()
+    asm.synchronize()
+    np.testing.assert_array_equal(out, rhs_host)
+    views = asm.torch_views()
+    perm = np.arange(m.n_nodes) if asm.device_buffers()["perm"] is None else None
+    rx = views["rx"].cpu().numpy()
+    ids = asm.map_nodes(np.arange(m.n_nodes))
+    np.testing.assert_array_equal(rx[ids], rhs_host[:, 0])
+    assert perm is None or perm.size == m.n_nodes
+    # velocity written through the torch view drives the next run
+    views["ux"].zero_(); views["uy"].zero_(); views["uz"].zero_()
+    torch.cuda.synchronize()
+    asm.run(P)
+    np.testing.assert_array_equal(asm.get_rhs_host(), np.zeros((m.n_nodes, 3)))
+    asm.close()
+
+
+def test_result_fields():
+    m = tb.generate_box_mesh(2, 2, 2)
+    u = tb.make_velocity(m, "random:1")
+    res = run(m, u)
+    assert res.variant is tb.VariantId.RSP and res.wall_time > 0.0
+    assert res.elements_per_second == pytest.approx(m.n_elems / res.wall_time, rel=1e-9)
+    assert np.isfinite(res.rhs).all()
+    assert res.timings.kernel_launches >= 1
+
+
+def test_velocity_validation_on_gpu_path():
+    m = tb.generate_box_mesh(2, 2, 2)
+    u = np.zeros((m.n_nodes, 3))
+    u[3, 1] = np.nan
+    with pytest.raises(ValueError):
+        run(m, u)
+    with pytest.raises(ValueError):
+        run(m, np.zeros((3, m.n_nodes)))
+
+
+@pytest.mark.parametrize("init", ["random:1", "taylor-green"])
+def test_full_size_128(oracle, init):
+    """BASELINE config 2 at full size: 128^3 (12.58M tets), all modes,
+    against the threaded C oracle (same arithmetic as the reference)."""
+    m = tb.generate_box_mesh(128, 128, 128)
+    u = tb.make_velocity(m, init)
+    ref = oracle.assemble_rsp(m.coords, m.connectivity, u, n_threads=oracle.default_threads(),
+                              vector_dim=4096)
+    for mode in ("private", "private-atomic", "atomic"):
+        rhs = run(m, u, scatter=mode).rhs
+        assert_parity(oracle, rhs, ref, m, u)
+    tb.clear_cache()
+
+
+def test_full_size_128_random_permutation(oracle):
+    """BASELINE config 3: 128^3 with randomly permuted node numbering."""
+    base = tb.generate_box_mesh(128, 128, 128)
+    perm = np.random.default_rng(0).permutation(base.n_nodes)
+    m = tb.permute_nodes(base, perm)
+    u = tb.make_velocity(m, "random:1")
+    ref = oracle.assemble_rsp(m.coords, m.connectivity, u, n_threads=oracle.default_threads(),
+                              vector_dim=4096)
+    for renumber in ("none", "rcm"):
+        rhs = run(m, u, renumber=renumber, element_order="keep" if renumber == "none" else "sfc").rhs
+        assert_parity(oracle, rhs, ref, m, u)
+    tb.clear_cache()
