@@ -50,8 +50,9 @@ def parse():
     ap.add_argument("--scatter", default="private-atomic")
     ap.add_argument("--renumber", default="rcm")
     ap.add_argument("--element-order", default="sfc")
-    ap.add_argument("--chunk-elems", type=int, default=512)
-    ap.add_argument("--chunk-nodes", type=int, default=1024)
+    ap.add_argument("--patches", default="star")
+    ap.add_argument("--cta-patches", type=int, default=128)
+    ap.add_argument("--chunk-nodes", type=int, default=256)
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -222,7 +223,8 @@ def run_ours(a) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     P = tb.PhysParams()
     cfg = tb.RunConfig(scatter=a.scatter, renumber=a.renumber, element_order=a.element_order,
-                       chunk_elems=a.chunk_elems, chunk_nodes=a.chunk_nodes, device=dev)
+                       patches=a.patches, cta_patches=a.cta_patches, chunk_nodes=a.chunk_nodes,
+                       device=dev)
     c = a.cells
     t0 = time.perf_counter()
     if ws > 1:
@@ -346,8 +348,8 @@ def run_ours(a) -> None:
     tf = FLOP_PER_ELEM * E / (kmean * 1e-3) / 1e12
     alg_bytes = 16 * E + 72 * Nn  # int32 conn + coords/u read + rhs write
     hbm_peak, hbm_src = measured_hbm_peak()
-    kname = {"private": "k_assemble_private<true,true>",
-             "private-atomic": "k_assemble_private<true,false>",
+    kname = {"private": "k_assemble_private<cfg,ordered=true>",
+             "private-atomic": "k_assemble_private<cfg,ordered=false>",
              "atomic": "k_assemble_atomic<true>", "colored": "k_assemble_colored<true> (all colours)"}[a.scatter]
     traffic = ncu_traffic(kname, workload)
     line = {
@@ -357,7 +359,7 @@ def run_ours(a) -> None:
         "data": "synthetic (generated Kuhn box mesh, seeded velocity)",
         "config": {"workload": workload, "n_elems": E, "n_nodes": Nn, "scatter": a.scatter,
                    "renumber": a.renumber, "element_order": a.element_order,
-                   "chunk_elems": a.chunk_elems, "chunk_nodes": a.chunk_nodes,
+                   "patches": a.patches, "cta_patches": a.cta_patches, "chunk_nodes": a.chunk_nodes,
                    "permuted": bool(a.permute),
                    "l2": "flushed (256 MiB write) before every step, outside the timed events"
                          if flush_buf is not None else "not flushed",
@@ -377,7 +379,8 @@ def run_ours(a) -> None:
         "gpu_launches": launches,
         "clocks": clocks,
         "prep": {"seconds": prep_s, "native_prep_seconds": info["prep_seconds"],
-                 "n_chunks": info["n_chunks"], "n_chunk_nodes": info["n_chunk_nodes"],
+                 "n_patches": info["n_patches"], "n_chunks": info["n_chunks"],
+                 "n_chunk_nodes": info["n_chunk_nodes"],
                  "n_shared_nodes": info["n_shared_nodes"], "device_bytes": info["device_bytes"]},
         "fp64_probe_mhz": fp64_mhz,
         "wall_s_timed_region": wall1 - wall0,

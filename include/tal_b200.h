@@ -74,15 +74,18 @@ typedef struct {
 typedef struct {
     int renumber;        /* TAL_RENUMBER_*                              */
     int element_order;   /* TAL_EORDER_*                                */
-    int chunk_elems;     /* max elements per CTA chunk (<= 1024)        */
-    int chunk_nodes;     /* max unique nodes per CTA chunk (<= 2048)    */
+    int cta_patches;     /* patches per CTA chunk: <= 64 -> 64-thread CTAs, else 128 (max 128) */
+    int chunk_nodes;     /* max unique nodes per CTA chunk (<= 144 | 256)  */
     int validate;        /* 1: reject out-of-range ids / non-positive volume */
     int build_colors;    /* 1: colour (greedy, element order) if colors==NULL */
+    int patch_mode;      /* 0: one tet per patch; 1: edge-star patches (rings of
+                            tets around an edge, e.g. the 6 tets of a Kuhn cell) */
 } tal_mesh_opts;
 
 typedef struct {
     int64_t n_nodes, n_elems;
     int64_t n_colors;        /* 0 if no colouring available              */
+    int64_t n_patches;       /* thread work units of the private scatter  */
     int64_t n_chunks;        /* CTA chunks of the private scatter        */
     int64_t n_chunk_nodes;   /* sum over chunks of unique nodes          */
     int64_t n_shared_nodes;  /* nodes touched by >1 chunk                */
@@ -98,10 +101,11 @@ typedef struct {
 
 typedef struct {
     /* device pointers in the handle's internal (renumbered) node order */
-    double *ux, *uy, *uz; /* velocity components, n_nodes each   */
+    double *ux, *uy, *uz; /* velocity components, n_nodes each, stride u_stride doubles */
     double *rx, *ry, *rz; /* assembled RHS components            */
     const int32_t *perm;  /* internal -> caller node id (NULL = identity) */
     const int32_t *iperm; /* caller -> internal node id (NULL = identity) */
+    int64_t u_stride;     /* element stride of ux/uy/uz (node records: 6) */
 } tal_buffers;
 
 /* ---- library / device ---------------------------------------------------- */
@@ -179,6 +183,14 @@ int tal_check_coloring(const int64_t *conn, const int64_t *colors, int64_t n_nod
 /* node permutation perm[new] = old by the given TAL_RENUMBER_* */
 int tal_renumber_nodes(const double *coords, const int64_t *conn, int64_t n_nodes,
                        int64_t n_elems, int method, int64_t *perm);
+
+/* edge-star patch decomposition used by the private scatter (host utility,
+ * for inspection/tests).  Two-call protocol: with nodes_out == NULL only the
+ * sizes are returned.  Patch g = off[g]..off[g+1] into nodes: a, b, r_0..r_m-1;
+ * its tets are (a, b, r_i, r_i+1), i < m (closed[g]) or i < m-1 (open). */
+int tal_build_patches(const int64_t *conn, int64_t n_nodes, int64_t n_elems, int mode,
+                      int64_t *n_patches, int64_t *n_patch_nodes, int32_t *off_out,
+                      int32_t *nodes_out, uint8_t *closed_out);
 
 /* ---- measurement ------------------------------------------------------------ */
 /* When enabled, tal_run records a CUDA event pair around the dominant

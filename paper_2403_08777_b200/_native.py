@@ -20,6 +20,7 @@ TAL_OK, TAL_EINVAL, TAL_ECUDA, TAL_ENOMEM, TAL_ESTATE = 0, 1, 2, 3, 4
 SCATTER = {"private": 0, "colored": 1, "atomic": 2, "private-atomic": 3}
 RENUMBER = {"none": 0, "rcm": 1, "sfc": 2}
 EORDER = {"keep": 0, "node": 1, "sfc": 2}
+PATCHES = {"tet": 0, "star": 1}
 
 
 class TalParams(ctypes.Structure):
@@ -29,13 +30,15 @@ class TalParams(ctypes.Structure):
 
 class TalMeshOpts(ctypes.Structure):
     _fields_ = [("renumber", ctypes.c_int), ("element_order", ctypes.c_int),
-                ("chunk_elems", ctypes.c_int), ("chunk_nodes", ctypes.c_int),
-                ("validate", ctypes.c_int), ("build_colors", ctypes.c_int)]
+                ("cta_patches", ctypes.c_int), ("chunk_nodes", ctypes.c_int),
+                ("validate", ctypes.c_int), ("build_colors", ctypes.c_int),
+                ("patch_mode", ctypes.c_int)]
 
 
 class TalMeshInfo(ctypes.Structure):
     _fields_ = [("n_nodes", ctypes.c_int64), ("n_elems", ctypes.c_int64),
-                ("n_colors", ctypes.c_int64), ("n_chunks", ctypes.c_int64),
+                ("n_colors", ctypes.c_int64), ("n_patches", ctypes.c_int64),
+                ("n_chunks", ctypes.c_int64),
                 ("n_chunk_nodes", ctypes.c_int64), ("n_shared_nodes", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("prep_seconds", ctypes.c_double)]
 
@@ -50,7 +53,7 @@ class TalTimings(ctypes.Structure):
 class TalBuffers(ctypes.Structure):
     _fields_ = [("ux", ctypes.c_void_p), ("uy", ctypes.c_void_p), ("uz", ctypes.c_void_p),
                 ("rx", ctypes.c_void_p), ("ry", ctypes.c_void_p), ("rz", ctypes.c_void_p),
-                ("perm", ctypes.c_void_p), ("iperm", ctypes.c_void_p)]
+                ("perm", ctypes.c_void_p), ("iperm", ctypes.c_void_p), ("u_stride", ctypes.c_int64)]
 
 
 # (name, restype, argtypes) of every exported symbol in include/tal_b200.h
@@ -87,6 +90,8 @@ SIGNATURES = [
     ("tal_check_coloring", _I, [_P, _P, _I64, _I64, ctypes.POINTER(_I)]),
     ("tal_renumber_nodes", _I, [_P, _P, _I64, _I64, _I, _P]),
     ("tal_fp64_peak", _I, [_I, _D, ctypes.POINTER(_D), ctypes.POINTER(_D)]),
+    ("tal_build_patches", _I, [_P, _I64, _I64, _I, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                               _P, _P, _P]),
     ("tal_profile", _I, [_P, _I]),
     ("tal_profile_read", _I, [_P, _P, _I64, ctypes.POINTER(_I64)]),
 ]

@@ -52,7 +52,10 @@ class RunConfig:
     * ``private-atomic`` CTA-private sums, one FP64 RED per shared node.
 
     GPU knobs: ``device``, ``renumber`` (rcm | sfc | none), ``element_order``
-    (sfc | node | keep), ``chunk_elems`` / ``chunk_nodes`` (CTA chunk limits).
+    (sfc | node | keep), ``patches`` (star: edge-star patches, the rings of
+    tets around an edge; tet: one tet per thread), ``cta_patches`` (patches =
+    threads per CTA chunk: <= 64 selects 64-thread CTAs, else 128) and
+    ``chunk_nodes`` (max distinct nodes per chunk: <= 144 | 256).
     """
 
     vector_dim: int = 16
@@ -63,8 +66,9 @@ class RunConfig:
     device: int = 0
     renumber: str = "rcm"
     element_order: str = "sfc"
-    chunk_elems: int = 512
-    chunk_nodes: int = 1024
+    patches: str = "star"
+    cta_patches: int = 128
+    chunk_nodes: int = 256
 
     def __post_init__(self):
         if self.vector_dim < 1:
@@ -83,10 +87,15 @@ class RunConfig:
             raise ValueError(f"renumber must be one of {tuple(N.RENUMBER)}, got {self.renumber!r}")
         if self.element_order not in N.EORDER:
             raise ValueError(f"element_order must be one of {tuple(N.EORDER)}")
-        if not 1 <= self.chunk_elems <= 1024:
-            raise ValueError("chunk_elems must be in [1, 1024]")
-        if not 4 <= self.chunk_nodes <= 2048:
-            raise ValueError("chunk_nodes must be in [4, 2048]")
+        if self.patches not in N.PATCHES:
+            raise ValueError(f"patches must be one of {tuple(N.PATCHES)}, got {self.patches!r}")
+        if not 1 <= self.cta_patches <= 128:
+            raise ValueError("cta_patches must be in [1, 128]")
+        # CTA shapes (tal_kernels.cuh PrivCfg): <= 64 patches -> 64 threads and
+        # room for 144 nodes; else 128 threads and 256 nodes
+        nmax = 144 if self.cta_patches <= 64 else 256
+        if not 16 <= self.chunk_nodes <= nmax:
+            raise ValueError(f"chunk_nodes must be in [16, {nmax}] for cta_patches={self.cta_patches}")
 
 
 @dataclass(frozen=True)
@@ -175,13 +184,25 @@ def _params(params: PhysParams, pmat: Optional[np.ndarray] = None) -> N.TalParam
     return p
 
 
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy default stream
+
+
+def _stream(stream):
+    """None -> the handle's own stream; 0 -> the legacy default stream (torch's
+    default stream); an int or a torch.cuda.Stream -> that stream."""
+    if stream is None:
+        return None
+    s = getattr(stream, "cuda_stream", stream)
+    return ctypes.c_void_p(int(s) if int(s) != 0 else _CUDA_STREAM_LEGACY)
+
+
 class _CudaView:
     """Minimal __cuda_array_interface__ wrapper so torch can view device buffers."""
 
-    def __init__(self, ptr: int, shape, typestr: str = "<f8"):
+    def __init__(self, ptr: int, shape, typestr: str = "<f8", strides=None):
         self.__cuda_array_interface__ = {
             "shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
-            "version": 3, "strides": None,
+            "version": 3, "strides": strides,
         }
 
 
@@ -209,8 +230,9 @@ class Assembler:
         opts = N.TalMeshOpts()
         opts.renumber = N.RENUMBER[cfg.renumber]
         opts.element_order = N.EORDER[cfg.element_order]
-        opts.chunk_elems = cfg.chunk_elems
+        opts.cta_patches = cfg.cta_patches
         opts.chunk_nodes = cfg.chunk_nodes
+        opts.patch_mode = N.PATCHES[cfg.patches]
         opts.validate = 1
         if build_colors is None:
             build_colors = cfg.scatter == "colored"
@@ -263,20 +285,23 @@ class Assembler:
         import torch
         b = self.device_buffers()
         n = self.n_nodes
-        return {k: torch.as_tensor(_CudaView(b[k], (n,)), device=f"cuda:{self.cfg.device}")
-                for k in ("ux", "uy", "uz", "rx", "ry", "rz")}
+        dev = f"cuda:{self.cfg.device}"
+        out = {k: torch.as_tensor(_CudaView(b[k], (n,), strides=(8 * b["u_stride"],)), device=dev)
+               for k in ("ux", "uy", "uz")}
+        out.update({k: torch.as_tensor(_CudaView(b[k], (n,)), device=dev) for k in ("rx", "ry", "rz")})
+        return out
 
-    def set_velocity_host(self, u: np.ndarray, stream: int = 0) -> None:
+    def set_velocity_host(self, u: np.ndarray, stream=None) -> None:
         u = np.ascontiguousarray(u, dtype=np.float64)
         if u.shape != (self.n_nodes, 3):
             raise ValueError("u must have shape (n_nodes, 3)")
-        N.check(N.lib().tal_set_velocity_host(self._h, N.ptr(u), ctypes.c_void_p(stream or None)))
+        N.check(N.lib().tal_set_velocity_host(self._h, N.ptr(u), _stream(stream)))
 
-    def set_velocity_device(self, d_u_ptr: int, stream: int = 0) -> None:
+    def set_velocity_device(self, d_u_ptr: int, stream=None) -> None:
         N.check(N.lib().tal_set_velocity_device(self._h, ctypes.c_void_p(d_u_ptr),
-                                                ctypes.c_void_p(stream or None)))
+                                                _stream(stream)))
 
-    def run(self, params: PhysParams, scatter: Optional[str] = None, stream: int = 0,
+    def run(self, params: PhysParams, scatter: Optional[str] = None, stream=None,
             pmat=None) -> int:
         """Enqueue one assembly on internal buffers; returns kernels launched."""
         scatter = scatter or self.cfg.scatter
@@ -284,20 +309,20 @@ class Assembler:
             raise ValueError(f"unknown scatter mode {scatter!r}")
         nl = ctypes.c_int64(0)
         N.check(N.lib().tal_run(self._h, ctypes.byref(_params(params, pmat)), N.SCATTER[scatter],
-                                ctypes.c_void_p(stream or None), ctypes.byref(nl)))
+                                _stream(stream), ctypes.byref(nl)))
         return int(nl.value)
 
-    def get_rhs_host(self, out: Optional[np.ndarray] = None, stream: int = 0) -> np.ndarray:
+    def get_rhs_host(self, out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
         out = np.empty((self.n_nodes, 3)) if out is None else out
-        N.check(N.lib().tal_get_rhs_host(self._h, N.ptr(out), ctypes.c_void_p(stream or None)))
+        N.check(N.lib().tal_get_rhs_host(self._h, N.ptr(out), _stream(stream)))
         return out
 
-    def get_rhs_device(self, d_out_ptr: int, stream: int = 0) -> None:
+    def get_rhs_device(self, d_out_ptr: int, stream=None) -> None:
         N.check(N.lib().tal_get_rhs_device(self._h, ctypes.c_void_p(d_out_ptr),
-                                           ctypes.c_void_p(stream or None)))
+                                           _stream(stream)))
 
-    def synchronize(self, stream: int = 0) -> None:
-        N.check(N.lib().tal_synchronize(self._h, ctypes.c_void_p(stream or None)))
+    def synchronize(self, stream=None) -> None:
+        N.check(N.lib().tal_synchronize(self._h, _stream(stream)))
 
     def map_nodes(self, caller_ids: np.ndarray) -> np.ndarray:
         ids = np.ascontiguousarray(caller_ids, dtype=np.int64)
@@ -305,13 +330,13 @@ class Assembler:
         N.check(N.lib().tal_map_nodes(self._h, N.ptr(ids), ids.shape[0], N.ptr(out)))
         return out
 
-    def halo_pack(self, d_list: int, n: int, d_out: int, stream: int = 0) -> None:
+    def halo_pack(self, d_list: int, n: int, d_out: int, stream=None) -> None:
         N.check(N.lib().tal_halo_pack(self._h, ctypes.c_void_p(d_list), n, ctypes.c_void_p(d_out),
-                                      ctypes.c_void_p(stream or None)))
+                                      _stream(stream)))
 
-    def halo_accumulate(self, d_list: int, n: int, d_in: int, stream: int = 0) -> None:
+    def halo_accumulate(self, d_list: int, n: int, d_in: int, stream=None) -> None:
         N.check(N.lib().tal_halo_accumulate(self._h, ctypes.c_void_p(d_list), n,
-                                            ctypes.c_void_p(d_in), ctypes.c_void_p(stream or None)))
+                                            ctypes.c_void_p(d_in), _stream(stream)))
 
     def profile(self, enable: bool = True) -> None:
         """Record CUDA events around the dominant kernel of every run()."""
@@ -346,7 +371,7 @@ def _cached_assembler(mesh, cfg: RunConfig) -> Assembler:
     colors = getattr(mesh, "colors", None)
     key = (id(mesh.coords), id(mesh.connectivity), id(colors), mesh.coords.shape,
            mesh.connectivity.shape, cfg.device, cfg.renumber, cfg.element_order,
-           cfg.chunk_elems, cfg.chunk_nodes, cfg.scatter == "colored")
+           cfg.patches, cfg.cta_patches, cfg.chunk_nodes, cfg.scatter == "colored")
     hit = _CACHE.get(key)
     if hit is not None:
         _CACHE.move_to_end(key)

@@ -64,8 +64,8 @@ struct tal_handle {
     cudaEvent_t ev[6] = {};
     int64_t N = 0, E = 0;
     bool has_mesh = false;
-    // node data (internal order)
-    double *nodebuf = nullptr;  // x,y,z,ux,uy,uz,rx,ry,rz: 9*N doubles
+    // node data (internal order): records x y z ux uy uz (6*N) then rx ry rz (3*N)
+    double *nodebuf = nullptr;
     double *staging = nullptr;  // 3*N doubles (AoS in/out)
     int32_t *perm = nullptr, *iperm = nullptr;
     std::vector<int32_t> h_iperm;  // caller -> internal (host)
@@ -75,13 +75,11 @@ struct tal_handle {
     std::vector<int64_t> col_off;
     // private scatter
     Chunking ch;
-    int4 *d_chunks = nullptr;
-    int32_t *d_chunk_nodes = nullptr;
-    uint16_t *d_csr_off = nullptr, *d_csr_slots = nullptr;
-    ushort4 *d_lconn = nullptr;
+    uint8_t *d_blobs = nullptr;
+    int32_t *d_blob_off = nullptr;
     int32_t *d_bnd_nodes = nullptr, *d_bnd_off = nullptr, *d_bnd_pos = nullptr;
     double *d_partial = nullptr;  // 3 * n_chunk_nodes
-    size_t smem_private = 0;
+    int priv_grid = 0, priv_cfg = 1;
     tal_mesh_info info = {};
     tal_timings last = {};
     // dominant-kernel event ring (tal_profile)
@@ -90,32 +88,26 @@ struct tal_handle {
     std::vector<cudaEvent_t> prof_ev;  // 2 per slot
     int64_t prof_head = 0, prof_count = 0;
 
-    double *X() const { return nodebuf; }
-    double *Y() const { return nodebuf + N; }
-    double *Z() const { return nodebuf + 2 * N; }
-    double *UX() const { return nodebuf + 3 * N; }
-    double *UY() const { return nodebuf + 4 * N; }
-    double *UZ() const { return nodebuf + 5 * N; }
+    double *REC() const { return nodebuf; }
     double *RX() const { return nodebuf + 6 * N; }
     double *RY() const { return nodebuf + 7 * N; }
     double *RZ() const { return nodebuf + 8 * N; }
 
     void free_mesh()
     {
-        void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_chunks, d_chunk_nodes,
-                        d_csr_off, d_csr_slots, d_lconn, d_bnd_nodes, d_bnd_off, d_bnd_pos,
-                        d_partial};
+        void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
+                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial};
         for (void *p : ptrs)
             if (p)
                 cudaFree(p);
         nodebuf = staging = d_partial = nullptr;
-        perm = iperm = d_chunk_nodes = d_bnd_nodes = d_bnd_off = d_bnd_pos = nullptr;
-        conn = conn_col = d_chunks = nullptr;
-        d_csr_off = d_csr_slots = nullptr;
-        d_lconn = nullptr;
+        perm = iperm = d_blob_off = d_bnd_nodes = d_bnd_off = d_bnd_pos = nullptr;
+        conn = conn_col = nullptr;
+        d_blobs = nullptr;
         col_off.clear();
         h_iperm.clear();
         ch = Chunking();
+        priv_grid = 0;
         has_mesh = false;
         info = tal_mesh_info{};
     }
@@ -179,6 +171,27 @@ int check_params(const tal_params *p)
     return TAL_OK;
 }
 
+template <int CFG>
+void launch_private_cfg(bool ordered, unsigned grid, cudaStream_t s, const PrivArgs &pa, const double *nodes,
+                        RhsSoA rhs, const ElemConsts &kc)
+{
+    constexpr size_t sm = PrivLayoutOf<CFG>::TOTAL;
+    constexpr int T = PrivCfg<CFG>::THREADS;
+    if (ordered)
+        k_assemble_private<CFG, true><<<grid, T, sm, s>>>(pa, nodes, rhs, kc);
+    else
+        k_assemble_private<CFG, false><<<grid, T, sm, s>>>(pa, nodes, rhs, kc);
+}
+
+void launch_private(int cfg, bool ordered, unsigned grid, cudaStream_t s, const PrivArgs &pa,
+                    const double *nodes, RhsSoA rhs, const ElemConsts &kc)
+{
+    if (cfg == 0)
+        launch_private_cfg<0>(ordered, grid, s, pa, nodes, rhs, kc);
+    else
+        launch_private_cfg<1>(ordered, grid, s, pa, nodes, rhs, kc);
+}
+
 struct ProfMark {
     tal_handle *h;
     cudaStream_t s;
@@ -208,7 +221,7 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
     bool sym;
     if (!make_consts(p, kc, sym))
         return fail(TAL_EINVAL, "non-finite physical parameters");
-    NodeSoA nodes{h->X(), h->Y(), h->Z(), h->UX(), h->UY(), h->UZ()};
+    const double *nodes = h->REC();
     RhsSoA rhs{h->RX(), h->RY(), h->RZ()};
     int64_t nl = 0;
     const int64_t N = h->N, E = h->E;
@@ -250,29 +263,22 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
     }
     case TAL_SCATTER_PRIVATE:
     case TAL_SCATTER_PRIVATE_ATOMIC: {
+        if (!sym)  // patches permute tet corners: only valid for the symmetric rule
+            return launch_run(h, p, TAL_SCATTER_ATOMIC, s, launches);
         const bool ordered = scatter == TAL_SCATTER_PRIVATE;
-        ChunkArgs ca{h->d_chunks, h->d_chunk_nodes, h->d_csr_off, h->d_csr_slots, h->d_lconn,
-                     h->ch.chunk_elems, h->ch.max_nodes, nullptr, nullptr, nullptr};
         const int64_t ncn = (int64_t)h->ch.chunk_nodes.size();
+        PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr, nullptr, nullptr};
         if (ordered && h->d_partial) {
-            ca.px = h->d_partial;
-            ca.py = h->d_partial + ncn;
-            ca.pz = h->d_partial + 2 * ncn;
+            pa.px = h->d_partial;
+            pa.py = h->d_partial + ncn;
+            pa.pz = h->d_partial + 2 * ncn;
         }
         if (!ordered && N)
             TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
-        const int64_t nch = h->info.n_chunks;
-        if (nch) {
-            const size_t sm = h->smem_private;
+        if (h->info.n_chunks) {
+            const unsigned grid = (unsigned)std::min<int64_t>(h->priv_grid, h->info.n_chunks);
             pm.begin();
-            if (sym && ordered)
-                k_assemble_private<true, true><<<(unsigned)nch, PRIV_THREADS, sm, s>>>(ca, nodes, rhs, kc);
-            else if (sym)
-                k_assemble_private<true, false><<<(unsigned)nch, PRIV_THREADS, sm, s>>>(ca, nodes, rhs, kc);
-            else if (ordered)
-                k_assemble_private<false, true><<<(unsigned)nch, PRIV_THREADS, sm, s>>>(ca, nodes, rhs, kc);
-            else
-                k_assemble_private<false, false><<<(unsigned)nch, PRIV_THREADS, sm, s>>>(ca, nodes, rhs, kc);
+            launch_private(h->priv_cfg, ordered, grid, s, pa, nodes, rhs, kc);
             pm.end();
             TAL_CK_LAUNCH();
             ++nl;
@@ -280,7 +286,7 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         const int64_t nb = (int64_t)h->ch.bnd_nodes.size();
         if (ordered && nb) {
             k_merge_partials<<<grid_for(nb, 256), 256, 0, s>>>(h->d_bnd_nodes, h->d_bnd_off, h->d_bnd_pos,
-                                                              nb, ca.px, ca.py, ca.pz, rhs);
+                                                              nb, pa.px, pa.py, pa.pz, rhs);
             TAL_CK_LAUNCH();
             ++nl;
         }
@@ -294,16 +300,31 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
     return TAL_OK;
 }
 
-int set_kernel_attrs(size_t smem)
+template <int CFG>
+int set_attrs_cfg(int device, int *grid_out)
 {
-    const void *fns[] = {(const void *)k_assemble_private<true, true>,
-                         (const void *)k_assemble_private<true, false>,
-                         (const void *)k_assemble_private<false, true>,
-                         (const void *)k_assemble_private<false, false>};
+    constexpr int sm = PrivLayoutOf<CFG>::TOTAL;
+    const void *fns[] = {(const void *)k_assemble_private<CFG, true>,
+                         (const void *)k_assemble_private<CFG, false>};
     for (const void *f : fns)
-        TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    int per_sm = 0, n_sm = 0;
+    TAL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[1], PrivCfg<CFG>::THREADS, sm));
+    TAL_CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
+    *grid_out = std::max(1, per_sm) * n_sm;
     return TAL_OK;
 }
+
+int set_kernel_attrs(int device, int cfg, int *grid_out)
+{
+    return cfg == 0 ? set_attrs_cfg<0>(device, grid_out) : set_attrs_cfg<1>(device, grid_out);
+}
+
+// cta_patches -> CTA configuration (PrivCfg in tal_kernels.cuh)
+int cfg_for(int cta_patches) { return cta_patches <= PrivCfg<0>::THREADS ? 0 : 1; }
+int cfg_threads(int cfg) { return cfg == 0 ? PrivCfg<0>::THREADS : PrivCfg<1>::THREADS; }
+int cfg_max_nodes(int cfg) { return cfg == 0 ? PrivCfg<0>::NM : PrivCfg<1>::NM; }
+int cfg_max_contrib(int cfg) { return cfg == 0 ? PrivCfg<0>::NC : PrivCfg<1>::NC; }
 
 }  // namespace
 
@@ -391,8 +412,9 @@ int tal_default_mesh_opts(tal_mesh_opts *o)
         return fail(TAL_EINVAL, "NULL");
     o->renumber = TAL_RENUMBER_RCM;
     o->element_order = TAL_EORDER_SFC;
-    o->chunk_elems = 512;
-    o->chunk_nodes = 1024;
+    o->cta_patches = 128;
+    o->patch_mode = 1;
+    o->chunk_nodes = 256;
     o->validate = 1;
     o->build_colors = 0;
     return TAL_OK;
@@ -471,8 +493,21 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
             cord[4 * e + a] = cin[4 * (int64_t)eperm[e] + a];
     // chunks
     std::string err;
-    if (!build_chunks(cord.data(), n_nodes, n_elems, opts.chunk_elems, opts.chunk_nodes, h->ch, err))
+    const int cfg = cfg_for(opts.cta_patches);
+    if (opts.cta_patches < 1 || opts.cta_patches > cfg_threads(1) || opts.chunk_nodes < 16 ||
+        opts.chunk_nodes > cfg_max_nodes(cfg) || (opts.patch_mode != 0 && opts.patch_mode != 1))
+        return fail(TAL_EINVAL, "cta_patches must be in [1," + std::to_string(cfg_threads(1)) +
+                                    "], chunk_nodes in [16," + std::to_string(cfg_max_nodes(cfg)) +
+                                    "], patch_mode 0|1");
+    h->priv_cfg = cfg;
+    Patches patches;
+    build_patches(cord.data(), n_nodes, n_elems, opts.patch_mode, patches);
+    if (!build_chunks(patches, n_nodes, opts.cta_patches, opts.chunk_nodes, cfg_max_contrib(cfg), h->ch, err))
         return fail(TAL_EINVAL, err);
+    h->info.n_patches = patches.n_patches();
+    std::vector<uint8_t> blobs;
+    std::vector<int32_t> blob_off;
+    pack_blobs(h->ch, blobs, blob_off);
     // colouring (caller's or greedy on the internal order), colour-sorted copy
     std::vector<int64_t> col;
     int64_t ncol = 0;
@@ -516,12 +551,12 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
     bytes += sizeof(double) * 12 * n_nodes;
     TAL_CK(cudaMemset(h->nodebuf, 0, sizeof(double) * 9 * std::max<int64_t>(n_nodes, 1)));
     {
-        std::vector<double> soa((size_t)(3 * n_nodes));
+        std::vector<double> rec((size_t)(6 * n_nodes), 0.0);  // x y z (u = 0 until set)
         for (int64_t i = 0; i < n_nodes; ++i)
             for (int c = 0; c < 3; ++c)
-                soa[c * n_nodes + i] = xin[3 * i + c];
+                rec[6 * i + c] = xin[3 * i + c];
         if (n_nodes)
-            TAL_CK(cudaMemcpy(h->nodebuf, soa.data(), sizeof(double) * 3 * n_nodes, cudaMemcpyHostToDevice));
+            TAL_CK(cudaMemcpy(h->nodebuf, rec.data(), sizeof(double) * 6 * n_nodes, cudaMemcpyHostToDevice));
     }
     if (renum) {
         if ((rc = dev_upload(&h->perm, perm.data(), perm.size())))
@@ -540,15 +575,9 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
         bytes += 16 * n_elems;
     }
     const Chunking &C = h->ch;
-    if ((rc = dev_upload(&h->d_chunks, (const int4 *)C.chunks.data(), C.chunks.size() / 4)))
+    if ((rc = dev_upload(&h->d_blobs, blobs.data(), blobs.size())))
         return rc;
-    if ((rc = dev_upload(&h->d_chunk_nodes, C.chunk_nodes.data(), C.chunk_nodes.size())))
-        return rc;
-    if ((rc = dev_upload(&h->d_csr_off, C.csr_off.data(), C.csr_off.size())))
-        return rc;
-    if ((rc = dev_upload(&h->d_csr_slots, C.csr_slots.data(), C.csr_slots.size())))
-        return rc;
-    if ((rc = dev_upload(&h->d_lconn, (const ushort4 *)C.lconn.data(), C.lconn.size() / 4)))
+    if ((rc = dev_upload(&h->d_blob_off, blob_off.data(), blob_off.size())))
         return rc;
     if ((rc = dev_upload(&h->d_bnd_nodes, C.bnd_nodes.data(), C.bnd_nodes.size())))
         return rc;
@@ -558,10 +587,9 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
         return rc;
     if (!C.chunk_nodes.empty())
         TAL_CK(cudaMalloc((void **)&h->d_partial, sizeof(double) * 3 * C.chunk_nodes.size()));
-    bytes += C.chunks.size() * 4 + C.chunk_nodes.size() * (4 + 2 + 24) + C.csr_slots.size() * 2 +
-             C.lconn.size() * 2 + (C.bnd_nodes.size() + C.bnd_off.size() + C.bnd_pos.size()) * 4;
-    h->smem_private = sizeof(double) * (6 * (size_t)C.max_nodes + 12 * (size_t)C.chunk_elems);
-    if ((rc = set_kernel_attrs(h->smem_private)))
+    bytes += blobs.size() + blob_off.size() * 4 + C.chunk_nodes.size() * 24 +
+             (C.bnd_nodes.size() + C.bnd_off.size() + C.bnd_pos.size()) * 4;
+    if ((rc = set_kernel_attrs(h->device, h->priv_cfg, &h->priv_grid)))
         return rc;
     TAL_CK(cudaDeviceSynchronize());
 
@@ -569,7 +597,7 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
     h->info.n_nodes = n_nodes;
     h->info.n_elems = n_elems;
     h->info.n_colors = col.empty() ? 0 : ncol;
-    h->info.n_chunks = (int64_t)C.chunks.size() / 4;
+    h->info.n_chunks = (int64_t)C.chunks.size() / 5;
     h->info.n_chunk_nodes = (int64_t)C.chunk_nodes.size();
     h->info.n_shared_nodes = C.n_shared;
     h->info.device_bytes = (int64_t)bytes;
@@ -593,9 +621,10 @@ int tal_buffers_get(tal_handle *h, tal_buffers *out)
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
         return fail(TAL_ESTATE, "no mesh uploaded");
-    out->ux = h->UX();
-    out->uy = h->UY();
-    out->uz = h->UZ();
+    out->ux = h->REC() + 3;
+    out->uy = h->REC() + 4;
+    out->uz = h->REC() + 5;
+    out->u_stride = 6;
     out->rx = h->RX();
     out->ry = h->RY();
     out->rz = h->RZ();
@@ -613,7 +642,7 @@ int tal_set_velocity_device(tal_handle *h, const double *d_u, void *stream)
     DeviceGuard g(h->device);
     cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
     if (h->N) {
-        k_pack_aos<<<grid_for(h->N, 256), 256, 0, s>>>(d_u, h->perm, h->N, h->UX(), h->UY(), h->UZ());
+        k_pack_velocity<<<grid_for(h->N, 256), 256, 0, s>>>(d_u, h->perm, h->N, h->REC());
         TAL_CK_LAUNCH();
     }
     return TAL_OK;
@@ -784,8 +813,8 @@ int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
     std::vector<double> soa((size_t)(6 * n_nodes));
     for (int64_t i = 0; i < n_nodes; ++i)
         for (int c = 0; c < 3; ++c) {
-            soa[c * n_nodes + i] = coords[3 * i + c];
-            soa[(3 + c) * n_nodes + i] = u[3 * i + c];
+            soa[6 * i + c] = coords[3 * i + c];  // node records x y z ux uy uz
+            soa[6 * i + 3 + c] = u[3 * i + c];
         }
     double *buf = nullptr;
     int4 *dconn = nullptr;
@@ -801,8 +830,7 @@ int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
             rc = fail(TAL_ECUDA, std::string("assemble_elements upload: ") + cudaGetErrorString(e));
             break;
         }
-        NodeSoA nodes{buf, buf + n_nodes, buf + 2 * n_nodes, buf + 3 * n_nodes, buf + 4 * n_nodes,
-                      buf + 5 * n_nodes};
+        const double *nodes = buf;
         RhsSoA r{buf + 6 * n_nodes, buf + 7 * n_nodes, buf + 8 * n_nodes};
         if (sym)
             k_assemble_atomic<true><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc);
@@ -932,6 +960,33 @@ int tal_renumber_nodes(const double *coords, const int64_t *conn, int64_t n_node
         return fail(TAL_EINVAL, "unknown renumber method");
     for (int64_t i = 0; i < n_nodes; ++i)
         perm_out[i] = perm[i];
+    return TAL_OK;
+}
+
+int tal_build_patches(const int64_t *conn, int64_t n_nodes, int64_t n_elems, int mode,
+                      int64_t *n_patches, int64_t *n_patch_nodes, int32_t *off_out, int32_t *nodes_out,
+                      uint8_t *closed_out)
+{
+    if (n_nodes < 0 || n_elems < 0 || (n_elems && !conn) || !n_patches || !n_patch_nodes ||
+        (mode != 0 && mode != 1))
+        return fail(TAL_EINVAL, "bad arguments");
+    if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
+        return fail(TAL_EINVAL, "too large");
+    std::vector<int32_t> c32((size_t)(4 * n_elems));
+    for (int64_t i = 0; i < 4 * n_elems; ++i) {
+        if (conn[i] < 0 || conn[i] >= n_nodes)
+            return fail(TAL_EINVAL, "connectivity index out of range [0, n_nodes)");
+        c32[i] = (int32_t)conn[i];
+    }
+    Patches p;
+    build_patches(c32.data(), n_nodes, n_elems, mode, p);
+    *n_patches = p.n_patches();
+    *n_patch_nodes = (int64_t)p.nodes.size();
+    if (nodes_out && off_out && closed_out) {
+        std::memcpy(off_out, p.off.data(), sizeof(int32_t) * p.off.size());
+        std::memcpy(nodes_out, p.nodes.data(), sizeof(int32_t) * p.nodes.size());
+        std::memcpy(closed_out, p.closed.data(), p.closed.size());
+    }
     return TAL_OK;
 }
 

@@ -4,26 +4,29 @@
 // Operator (reference: _rsp_kernels.py:33-164, kernel.py:146-170):
 //   r_a[i] = -rho * int N_a (u.grad) u_i  -  (mu + rho nu_t) int gradN_a . grad u_i
 // with nu_t the Vreman closure (kernel.py:99-143) on the constant element
-// gradient and filter width cbrt(6 vol) = cbrt(|det|).
+// gradient and filter width delta = cbrt(6 vol) = cbrt(|det|).
 //
-// B200 restructuring (same mathematics, fewer FP64 instructions; the parity
-// bound is 1e-12 of the max-norm, not bitwise):
+// B200 restructuring (same mathematics, fewer and shorter FP64 dependency
+// chains; parity is judged at 1e-12 of the max-norm, not bitwise):
 //  * Shape gradients are never divided out.  With cofactor rows c_b
-//    (b=1..3; c_0 = -sum) and D = det, G = Gh / D where
+//    (b=1..3, c_0 = -sum) and D = det:  G = Gh / D,
 //        Gh[k][i] = sum_{b=1..3} c_b[k] (u_b[i] - u_0[i]).
-//  * Vreman in the unscaled quantities: with aa = |G|^2, ssq = sum of the
-//    nine squared 2x2 minors of G (the Cauchy-Binet form the reference uses),
-//        nu_t = c * sqrt(delta^4 ssq / aa) = c * rcbrt(|D|) * sqrt(ssqh / aah)
-//    because delta^2 / |D| = |D|^(-1/3); the quiescent guard aa <= 1e-30
-//    (kernel.py:24) is tested as aah * (1/|D|)^2 <= 1e-30.
-//  * pmat = P^T P of the symmetric rule has one diagonal value pd and one
-//    off-diagonal value po, so the velocity moments are
-//        m_a = po * S + (pd - po) * u_a,  S = sum_b u_b.
-//  * Both terms share Gh:  r_a[i] = sum_k w_a[k] Gh[k][i] with
+//  * One cube-root reciprocal r3 = |D|^(-1/3) gives both the Vreman factor
+//    and 1/|D| = r3^3 (no separate division).
+//  * Vreman in unscaled quantities: aa = |G|^2, ssq = sum of the nine squared
+//    2x2 minors of G (the reference's Cauchy-Binet form), so
+//        nu_t = c sqrt(delta^4 ssq / aa) = c r3 sqrt(ssqh / aah)
+//             = c r3 ssqh rsqrt(ssqh aah)
+//    (delta^2 / |D| = r3); the quiescent guard aa <= 1e-30 (kernel.py:24) is
+//    aah (1/|D|)^2 <= 1e-30.  Rank-1 gradients keep ssqh == 0 exactly.
+//  * pmat = P^T P of the symmetric rule: one diagonal value pd, one
+//    off-diagonal po, so the moments are m_a = po S + (pd - po) u_a, S = sum u.
+//  * Both terms share Gh:  r_a[i] = sum_k w_a[k] Gh[k][i],
 //        w_a = A (po S + (pd-po) u_a) + B c_a,
-//        A = nrv / D = -rho sgn(D) / 24,   B = nvv / D^2 = -vis / (6 |D|).
-// About 215 FP64 instructions per element (FMA = 1) against the reference
-// ledger's 448 flop (variants.py:207-217).
+//        A = nrv / D = -rho sgn(D) / 24,  B = nvv / D^2 = -vis / (6 |D|),
+//    and w_0 = (4 A po + A (pd-po)) S - (w_1 + w_2 + w_3) since sum_a c_a = 0.
+// ~205 FP64 instructions per element (FMA = 1) against the reference ledger's
+// 448 flop (variants.py:207-217).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -43,8 +46,8 @@ __device__ __forceinline__ void cross3(const double a[3], const double b[3], dou
     c[2] = fma(a[0], b[1], -a[1] * b[0]);
 }
 
-// Shared geometry + gradient + Vreman part.  Returns Gh, cofactors c[0..3],
-// and the scalars A (signed) and B.
+// Geometry, velocity gradient, Vreman.  Outputs cofactor rows cf[1..3], the
+// unscaled gradient Gh, sgn(D) and B = -vis / (6 |D|).
 __device__ __forceinline__ void element_core(const double X[4][3], const double U[4][3],
                                              const ElemConsts &k, double cf[4][3],
                                              double Gh[3][3], double &sg, double &B)
@@ -60,8 +63,9 @@ __device__ __forceinline__ void element_core(const double X[4][3], const double 
     cross3(e[0], e[1], cf[3]);  // e1 x e2
     const double det = fma(e[0][0], cf[1][0], fma(e[0][1], cf[1][1], e[0][2] * cf[1][2]));
     const double ad = fabs(det);
-    const double inv = __drcp_rn(ad);
     sg = (det < 0.0) ? -1.0 : 1.0;
+    const double r3 = rcbrt(ad);     // |D|^(-1/3)
+    const double inv = r3 * r3 * r3; // 1/|D|
 
     double du[3][3];
 #pragma unroll
@@ -75,31 +79,41 @@ __device__ __forceinline__ void element_core(const double X[4][3], const double 
         for (int i = 0; i < 3; ++i)
             Gh[kk][i] = fma(cf[1][kk], du[0][i], fma(cf[2][kk], du[1][i], cf[3][kk] * du[2][i]));
 
-    // |Gh|^2 and the nine squared 2x2 minors (rows m<n, columns i<j)
-    double aah = Gh[0][0] * Gh[0][0];
+    // |Gh|^2 (three row partial sums) and the nine squared 2x2 minors
+    // (rows m<n, columns i<j; three column-pair partial sums)
+    double ar[3];
 #pragma unroll
-    for (int q = 1; q < 9; ++q)
-        aah = fma(Gh[q / 3][q % 3], Gh[q / 3][q % 3], aah);
-    double ssqh = 0.0;
+    for (int r = 0; r < 3; ++r)
+        ar[r] = fma(Gh[r][0], Gh[r][0], fma(Gh[r][1], Gh[r][1], Gh[r][2] * Gh[r][2]));
+    const double aah = ar[0] + ar[1] + ar[2];
+    double sp[3];
 #pragma unroll
     for (int cp = 0; cp < 3; ++cp) {
         const int ci = (cp == 2) ? 1 : 0, cj = (cp == 0) ? 1 : 2;
+        double d[3];
 #pragma unroll
         for (int rp = 0; rp < 3; ++rp) {
             const int m = (rp == 2) ? 1 : 0, n = (rp == 0) ? 1 : 2;
-            const double d = fma(Gh[m][ci], Gh[n][cj], -(Gh[m][cj] * Gh[n][ci]));
-            ssqh = fma(d, d, ssqh);
+            d[rp] = fma(Gh[m][ci], Gh[n][cj], -(Gh[m][cj] * Gh[n][ci]));
         }
+        sp[cp] = fma(d[0], d[0], fma(d[1], d[1], d[2] * d[2]));
     }
+    const double ssqh = sp[0] + sp[1] + sp[2];
+    const double t = ssqh * aah;
     double nut = 0.0;
-    if (aah * inv * inv > 1e-30) {  // kernel.py:24 guard, in G units
-        nut = k.cvre * rcbrt(ad) * sqrt(ssqh * __drcp_rn(aah));
-    }
+    if (aah * inv * inv > 1e-30 && t > 0.0)  // kernel.py:24 guard, in G units
+        nut = (k.cvre * r3) * (ssqh * rsqrt(t));
     const double vis = fma(k.rho, nut, k.mu);
     B = vis * (inv * (-1.0 / 6.0));
+}
+
+__device__ __forceinline__ void rhs_rows(const double w[4][3], const double Gh[3][3], double R[4][3])
+{
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-        cf[0][c] = -(cf[1][c] + cf[2][c] + cf[3][c]);
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            R[a][i] = fma(w[a][0], Gh[0][i], fma(w[a][1], Gh[1][i], w[a][2] * Gh[2][i]));
 }
 
 // Symmetric-rule element (pmat = po * ones + (pd - po) * I).
@@ -109,20 +123,19 @@ __device__ __forceinline__ void element_rhs_sym(const double X[4][3], const doub
     double cf[4][3], Gh[3][3], sg, B;
     element_core(X, U, k, cf, Gh, sg, B);
     const double As = sg * k.a_po, Aq = sg * k.a_q;
-    double AsS[3];
+    const double A4 = fma(4.0, As, Aq);
+    double S[3], w[4][3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-        AsS[c] = As * ((U[0][c] + U[1][c]) + (U[2][c] + U[3][c]));
+    for (int c = 0; c < 3; ++c) {
+        S[c] = (U[0][c] + U[1][c]) + (U[2][c] + U[3][c]);
+        const double AsS = As * S[c];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        double w[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            w[c] = fma(Aq, U[a][c], fma(B, cf[a][c], AsS[c]));
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-            R[a][i] = fma(w[0], Gh[0][i], fma(w[1], Gh[1][i], w[2] * Gh[2][i]));
+        for (int a = 1; a < 4; ++a)
+            w[a][c] = fma(Aq, U[a][c], fma(B, cf[a][c], AsS));
+        // sum_a w_a = (4 As + Aq) S because the cofactor rows sum to zero
+        w[0][c] = fma(A4, S[c], -((w[1][c] + w[2][c]) + w[3][c]));
     }
+    rhs_rows(w, Gh, R);
 }
 
 // General pmat (any 4x4 interpolation table): m_a = sum_b pmat[a][b] u_b.
@@ -131,21 +144,21 @@ __device__ __forceinline__ void element_rhs_gen(const double X[4][3], const doub
 {
     double cf[4][3], Gh[3][3], sg, B;
     element_core(X, U, k, cf, Gh, sg, B);
-    const double A = sg * (-k.rho / 24.0);
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        double w[3];
+    for (int c = 0; c < 3; ++c)
+        cf[0][c] = -(cf[1][c] + cf[2][c] + cf[3][c]);
+    const double A = sg * (-k.rho / 24.0);
+    double w[4][3];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const double m = fma(k.pm[4 * a + 0], U[0][c],
                                  fma(k.pm[4 * a + 1], U[1][c],
                                      fma(k.pm[4 * a + 2], U[2][c], k.pm[4 * a + 3] * U[3][c])));
-            w[c] = fma(A, m, B * cf[a][c]);
+            w[a][c] = fma(A, m, B * cf[a][c]);
         }
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-            R[a][i] = fma(w[0], Gh[0][i], fma(w[1], Gh[1][i], w[2] * Gh[2][i]));
-    }
+    rhs_rows(w, Gh, R);
 }
 
 template <bool SYM>

@@ -1,13 +1,13 @@
 // tal_kernels.cuh -- sm_100a kernels of the assembly path.
 //
 // Device layout (per mesh handle, internal = renumbered node order):
-//   x,y,z / ux,uy,uz / rx,ry,rz : FP64 SoA, n_nodes each
-//   conn                        : int4 per element (internal ids)
-//   private scatter             : per CTA chunk {elem_begin, n_elem,
-//                                 node_begin, n_node}; chunk node list (int32,
-//                                 bit 31 = node interior to the chunk);
-//                                 lconn (ushort4, chunk-local ids);
-//                                 chunk-local node->slot CSR (uint16)
+//   nrec      : node records, 6 doubles (48 B) per node: x y z ux uy uz
+//   rx,ry,rz  : assembled RHS, FP64 SoA
+//   conn      : int4 per element (atomic / colored scatter)
+//   blobs     : one contiguous, 16-B aligned record per CTA chunk of
+//               edge-star patches (private scatter), fetched whole by one
+//               TMA bulk copy (layout at k_assemble_private)
+//   blob_off  : n_chunks+1 offsets in 16-B units
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -16,23 +16,63 @@
 
 namespace tal {
 
-struct NodeSoA {
-    const double *__restrict__ x, *__restrict__ y, *__restrict__ z;
-    const double *__restrict__ ux, *__restrict__ uy, *__restrict__ uz;
-};
 struct RhsSoA {
     double *rx, *ry, *rz;
 };
 
-struct ChunkArgs {
-    const int4 *__restrict__ chunks;         // elem_begin, n_elem, node_begin, n_node
-    const int32_t *__restrict__ chunk_nodes;  // node | interior flag
-    const uint16_t *__restrict__ csr_off;
-    const uint16_t *__restrict__ csr_slots;
-    const ushort4 *__restrict__ lconn;
-    int chunk_elems, chunk_nodes_max;
-    double *px, *py, *pz;  // partial sums per chunk node (ordered merge)
-};
+__host__ __device__ constexpr int pad16(int b) { return (b + 15) / 16 * 16; }
+
+// ---------------------------------------------------------------------------
+// PTX helpers: TMA bulk copy + mbarrier, cp.async
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TAL_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra TAL_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async16(void *dst, const void *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ int4 ldg_stream(const int4 *p)
 {
@@ -43,14 +83,21 @@ __device__ __forceinline__ int4 ldg_stream(const int4 *p)
     return r;
 }
 
-__device__ __forceinline__ void gather_node(const NodeSoA &n, int v, double X[3], double U[3])
+// one 48-B node record -> X, U (three 16-B loads; global or shared)
+__device__ __forceinline__ void load_record_g(const double *__restrict__ rec, int v, double X[3],
+                                              double U[3])
 {
-    X[0] = __ldg(n.x + v);
-    X[1] = __ldg(n.y + v);
-    X[2] = __ldg(n.z + v);
-    U[0] = __ldg(n.ux + v);
-    U[1] = __ldg(n.uy + v);
-    U[2] = __ldg(n.uz + v);
+    const double2 *p = reinterpret_cast<const double2 *>(rec + 6 * (int64_t)v);
+    const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+    X[0] = a.x, X[1] = a.y, X[2] = b.x;
+    U[0] = b.y, U[1] = c.x, U[2] = c.y;
+}
+__device__ __forceinline__ void load_record_s(const double *rec, int v, double X[3], double U[3])
+{
+    const double2 *p = reinterpret_cast<const double2 *>(rec + 6 * v);
+    const double2 a = p[0], b = p[1], c = p[2];
+    X[0] = a.x, X[1] = a.y, X[2] = b.x;
+    U[0] = b.y, U[1] = c.x, U[2] = c.y;
 }
 
 // ---------------------------------------------------------------------------
@@ -59,7 +106,8 @@ __device__ __forceinline__ void gather_node(const NodeSoA &n, int v, double X[3]
 template <bool SYM>
 __global__ void __launch_bounds__(256) k_assemble_atomic(const int4 *__restrict__ conn,
                                                          int64_t e_begin, int64_t e_end,
-                                                         NodeSoA nodes, RhsSoA rhs, ElemConsts kc)
+                                                         const double *__restrict__ nrec, RhsSoA rhs,
+                                                         ElemConsts kc)
 {
     const int64_t e = e_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e_end)
@@ -69,7 +117,7 @@ __global__ void __launch_bounds__(256) k_assemble_atomic(const int4 *__restrict_
     double X[4][3], U[4][3], R[4][3];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
-        gather_node(nodes, ids[a], X[a], U[a]);
+        load_record_g(nrec, ids[a], X[a], U[a]);
     element_rhs<SYM>(X, U, kc, R);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -85,7 +133,8 @@ __global__ void __launch_bounds__(256) k_assemble_atomic(const int4 *__restrict_
 template <bool SYM>
 __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict__ conn,
                                                           int64_t e_begin, int64_t e_end,
-                                                          NodeSoA nodes, RhsSoA rhs, ElemConsts kc)
+                                                          const double *__restrict__ nrec, RhsSoA rhs,
+                                                          ElemConsts kc)
 {
     const int64_t e = e_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e_end)
@@ -95,7 +144,7 @@ __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict
     double X[4][3], U[4][3], R[4][3];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
-        gather_node(nodes, ids[a], X[a], U[a]);
+        load_record_g(nrec, ids[a], X[a], U[a]);
     element_rhs<SYM>(X, U, kc, R);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -106,97 +155,220 @@ __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict
 }
 
 // ---------------------------------------------------------------------------
-// (3) CTA-private accumulation (scatter = private / private-atomic)
+// (3) CTA-private accumulation over edge-star patches, persistent and
+//     double-buffered (scatter = private / private-atomic)
 //
-// One CTA per chunk of <= chunk_elems consecutive elements touching <=
-// chunk_nodes_max distinct nodes:
-//   A. stage the chunk's node coordinates + velocities in shared memory
-//      (sorted node list -> mostly coalesced loads);
-//   B. one element per thread (strided): element RHS in registers, 12
-//      results to shared slots res[corner*CH + e] (conflict-free stores);
-//   C. one chunk node per thread: sum its slots in element order (CSR), then
-//      a plain store if every element of the node is in this chunk, else
-//        ORDERED=false: one FP64 RED per component into rhs,
-//        ORDERED=true : store the partial for k_merge_partials (ordered,
-//                       bitwise reproducible merge).
+// Work unit = one patch per thread: the ring of tets around an edge (a,b)
+// (tal_prep.hpp), e.g. the 6 tets of a Kuhn cell around its main diagonal:
+// 8 node records serve 6 tets and the sums for a, b and each ring node are
+// accumulated in registers, so a tet costs ~1/3 of the shared-memory traffic
+// of a thread-per-tet scheme (whose operand + result traffic saturates the
+// 128 B/clk L1/shared data path before the FP64 pipe).
+//
+// Each persistent CTA walks chunks c = blockIdx.x + i*gridDim.x.  Per chunk:
+//   stage : one TMA bulk copy brings the chunk blob (patch records, node list,
+//           node-major contribution CSR) into shared memory (mbarrier
+//           completion); cp.async then gathers the chunk's node records.  Both
+//           run one chunk AHEAD, overlapping the FP64 work of the current one.
+//   B     : thread t walks patch t's ring, computing each tet's 4x3 RHS in
+//           registers; each patch node's sum is stored once, at its position
+//           in the chunk's node-major contribution list;
+//   C     : one chunk node per thread sums its contiguous contributions (patch
+//           order); a plain store if all of the node's tets are in this
+//           chunk, else one FP64 RED per component (ORDERED=false) or a
+//           partial for the ordered merge (ORDERED=true, bitwise reproducible).
+// Blob: int4 {n_patch, n_node, node_begin, n_contrib} | 64 B per patch:
+// u16 ids[16] = {m | closed<<8, a, b, r_0..r_{m-1}}, u16 pos[16] (same slots)
+// | u16 csr_off[n_node] (pad 16) | int32 nodes[n_node] (pad 16).
 // ---------------------------------------------------------------------------
-constexpr int PRIV_THREADS = 256;
+template <int CFG>
+struct PrivCfg;
+template <>
+struct PrivCfg<0> {  // 64 patches / chunk
+    static constexpr int THREADS = 64, NM = 144, NC = 544, MINB = 6;
+};
+template <>
+struct PrivCfg<1> {  // 128 patches / chunk
+    static constexpr int THREADS = 128, NM = 256, NC = 1088, MINB = 3;
+};
 
-template <bool SYM, bool ORDERED>
-__global__ void __launch_bounds__(PRIV_THREADS, 2)
-    k_assemble_private(ChunkArgs ca, NodeSoA nodes, RhsSoA rhs, ElemConsts kc)
+template <int T, int NM, int NC>
+struct PrivLayout {
+    static constexpr int BLOB = 16 + 64 * T + pad16(2 * NM) + pad16(4 * NM);
+    static constexpr int BLOB_AL = (BLOB + 127) / 128 * 128;
+    static constexpr int MBAR = 0;
+    static constexpr int BLOBS = 128;
+    static constexpr int NREC = BLOBS + 2 * BLOB_AL;
+    static constexpr int RES = NREC + 2 * NM * 48;
+    static constexpr int TOTAL = RES + 3 * NC * 8;
+};
+template <int CFG>
+using PrivLayoutOf = PrivLayout<PrivCfg<CFG>::THREADS, PrivCfg<CFG>::NM, PrivCfg<CFG>::NC>;
+
+struct PrivArgs {
+    const uint8_t *__restrict__ blobs;
+    const int32_t *__restrict__ blob_off;  // 16-B units, n_chunks+1
+    int n_chunks;
+    double *px, *py, *pz;  // ordered-merge partials, indexed node_begin + j
+};
+
+template <int CFG, bool ORDERED>
+__global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
+    k_assemble_private(PrivArgs pa, const double *__restrict__ nrec_g, RhsSoA rhs, ElemConsts kc)
 {
-    extern __shared__ double smem[];
-    const int NM = ca.chunk_nodes_max, CH = ca.chunk_elems;
-    double *sx = smem, *sy = sx + NM, *sz = sy + NM;
-    double *sux = sz + NM, *suy = sux + NM, *suz = suy + NM;
-    double *resx = suz + NM, *resy = resx + 4 * CH, *resz = resy + 4 * CH;
-
-    const int4 d = ca.chunks[blockIdx.x];  // elem_begin, n_elem, node_begin, n_node
+    constexpr int T = PrivCfg<CFG>::THREADS, NM = PrivCfg<CFG>::NM, NC = PrivCfg<CFG>::NC;
+    using L = PrivLayoutOf<CFG>;
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + L::MBAR);
+    // node-major contribution lists: res*[coff[j] .. coff[j+1]) belong to node j
+    double *resx = reinterpret_cast<double *>(sm + L::RES);
+    double *resy = resx + NC, *resz = resy + NC;
     const int tid = threadIdx.x;
+    const int first = blockIdx.x, stride = gridDim.x;
+    const int n_my = pa.n_chunks > first ? (pa.n_chunks - first + stride - 1) / stride : 0;
+    if (n_my == 0)
+        return;
+    auto blob = [&](int b) { return sm + L::BLOBS + b * L::BLOB_AL; };
+    auto nrec = [&](int b) { return reinterpret_cast<double *>(sm + L::NREC + b * NM * 48); };
 
-    // A. stage nodes
-    for (int j = tid; j < d.w; j += PRIV_THREADS) {
-        const int v = ca.chunk_nodes[d.z + j] & 0x7fffffff;
-        sx[j] = __ldg(nodes.x + v);
-        sy[j] = __ldg(nodes.y + v);
-        sz[j] = __ldg(nodes.z + v);
-        sux[j] = __ldg(nodes.ux + v);
-        suy[j] = __ldg(nodes.uy + v);
-        suz[j] = __ldg(nodes.uz + v);
+    auto issue = [&](int i, int b) {  // one thread: bulk-copy chunk i's blob into buffer b
+        const int c = first + i * stride;
+        const int o0 = __ldg(pa.blob_off + c), o1 = __ldg(pa.blob_off + c + 1);
+        const uint32_t bytes = (uint32_t)(o1 - o0) * 16u;
+        mbar_expect_tx(&bar[b], bytes);
+        bulk_g2s(blob(b), pa.blobs + (size_t)o0 * 16, bytes, &bar[b]);
+    };
+    auto gather = [&](int b) {  // all threads: cp.async the chunk's node records
+        const uint8_t *bl = blob(b);
+        const int4 hdr = *reinterpret_cast<const int4 *>(bl);
+        const int32_t *cn = reinterpret_cast<const int32_t *>(bl + 16 + 64 * hdr.x + pad16(2 * hdr.y));
+        double *dst = nrec(b);
+        for (int j = tid; j < hdr.y; j += T) {
+            const double *src = nrec_g + 6 * (int64_t)(cn[j] & 0x7fffffff);
+            cp_async16(dst + 6 * j, src);
+            cp_async16(dst + 6 * j + 2, src + 2);
+            cp_async16(dst + 6 * j + 4, src + 4);
+        }
+        cp_async_commit();
+    };
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
     }
     __syncthreads();
-
-    // B. elements
-    for (int el = tid; el < d.y; el += PRIV_THREADS) {
-        const ushort4 l = ca.lconn[d.x + el];
-        const int ids[4] = {l.x, l.y, l.z, l.w};
-        double X[4][3], U[4][3], R[4][3];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            X[a][0] = sx[ids[a]];
-            X[a][1] = sy[ids[a]];
-            X[a][2] = sz[ids[a]];
-            U[a][0] = sux[ids[a]];
-            U[a][1] = suy[ids[a]];
-            U[a][2] = suz[ids[a]];
-        }
-        element_rhs<SYM>(X, U, kc, R);
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            resx[a * CH + el] = R[a][0];
-            resy[a * CH + el] = R[a][1];
-            resz[a * CH + el] = R[a][2];
-        }
+    if (tid == 0) {
+        issue(0, 0);
+        if (n_my > 1)
+            issue(1, 1);
     }
-    __syncthreads();
+    mbar_wait(&bar[0], 0);
+    gather(0);
 
-    // C. per-node sums, scatter
-    const uint16_t *slots = ca.csr_slots + 4 * (int64_t)d.x;
-    for (int j = tid; j < d.w; j += PRIV_THREADS) {
-        const int beg = ca.csr_off[d.z + j];
-        const int end = (j + 1 < d.w) ? (int)ca.csr_off[d.z + j + 1] : 4 * d.y;
-        double ax = 0.0, ay = 0.0, az = 0.0;
-        for (int s = beg; s < end; ++s) {
-            const int slot = slots[s];
-            ax += resx[slot];
-            ay += resy[slot];
-            az += resz[slot];
+    for (int i = 0; i < n_my; ++i) {
+        const int b = i & 1;
+        cp_async_wait_all();
+        __syncthreads();  // node records of chunk i visible to all
+        if (i + 1 < n_my) {
+            mbar_wait(&bar[b ^ 1], ((i + 1) >> 1) & 1);
+            gather(b ^ 1);  // in flight during phase B below
         }
-        const int raw = ca.chunk_nodes[d.z + j];
-        const int v = raw & 0x7fffffff;
-        if (raw < 0) {  // interior: the complete sum
-            rhs.rx[v] = ax;
-            rhs.ry[v] = ay;
-            rhs.rz[v] = az;
-        } else if (ORDERED) {
-            ca.px[d.z + j] = ax;
-            ca.py[d.z + j] = ay;
-            ca.pz[d.z + j] = az;
-        } else {
-            atomicAdd(rhs.rx + v, ax);
-            atomicAdd(rhs.ry + v, ay);
-            atomicAdd(rhs.rz + v, az);
+        const uint8_t *bl = blob(b);
+        const int4 hdr = *reinterpret_cast<const int4 *>(bl);  // n_patch, n_node, node_begin, n_contrib
+        const uint16_t *coff = reinterpret_cast<const uint16_t *>(bl + 16 + 64 * hdr.x);
+        const int32_t *cn = reinterpret_cast<const int32_t *>(bl + 16 + 64 * hdr.x + pad16(2 * hdr.y));
+        const double *nr = nrec(b);
+
+        // phase B: one patch per thread
+        if (tid < hdr.x) {
+            const uint16_t *ids = reinterpret_cast<const uint16_t *>(bl + 16 + 64 * tid);
+            const uint16_t *pos = ids + 16;
+            const int m = ids[0] & 0xff;
+            const bool closed = (ids[0] >> 8) != 0;
+            const int k = closed ? m : m - 1;
+            double X[4][3], U[4][3], R[4][3];
+            load_record_s(nr, ids[1], X[0], U[0]);
+            load_record_s(nr, ids[2], X[1], U[1]);
+            load_record_s(nr, ids[3], X[2], U[2]);
+            double acc_a[3] = {0.0, 0.0, 0.0}, acc_b[3] = {0.0, 0.0, 0.0}, carry[3];
+#pragma unroll 1
+            for (int t = 0; t < k; ++t) {
+                const int nxt = (t + 1 == m) ? 0 : t + 1;
+                load_record_s(nr, ids[3 + nxt], X[3], U[3]);
+                element_rhs<true>(X, U, kc, R);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    acc_a[c] += R[0][c];
+                    acc_b[c] += R[1][c];
+                }
+                const int p = pos[3 + t];
+                if (t == 0) {
+                    resx[p] = R[2][0];
+                    resy[p] = R[2][1];
+                    resz[p] = R[2][2];
+                } else {
+                    resx[p] = carry[0] + R[2][0];
+                    resy[p] = carry[1] + R[2][1];
+                    resz[p] = carry[2] + R[2][2];
+                }
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    carry[c] = R[3][c];
+                    X[2][c] = X[3][c];
+                    U[2][c] = U[3][c];
+                }
+            }
+            // the ring node after the last tet: r_0 again (closed) or r_{m-1}
+            const int pl = pos[3 + (closed ? 0 : m - 1)];
+            if (closed) {
+                resx[pl] += carry[0];
+                resy[pl] += carry[1];
+                resz[pl] += carry[2];
+            } else {
+                resx[pl] = carry[0];
+                resy[pl] = carry[1];
+                resz[pl] = carry[2];
+            }
+            resx[pos[1]] = acc_a[0];
+            resy[pos[1]] = acc_a[1];
+            resz[pos[1]] = acc_a[2];
+            resx[pos[2]] = acc_b[0];
+            resy[pos[2]] = acc_b[1];
+            resz[pos[2]] = acc_b[2];
+        }
+        __syncthreads();
+
+        // phase C: per-node sums over contiguous runs (patch order), scatter
+        for (int j = tid; j < hdr.y; j += T) {
+            const int beg = coff[j];
+            const int end = (j + 1 < hdr.y) ? (int)coff[j + 1] : hdr.w;
+            double ax = 0.0, ay = 0.0, az = 0.0;
+            for (int s = beg; s < end; ++s) {
+                ax += resx[s];
+                ay += resy[s];
+                az += resz[s];
+            }
+            const int raw = cn[j];
+            const int v = raw & 0x7fffffff;
+            if (raw < 0) {  // interior: the complete sum
+                rhs.rx[v] = ax;
+                rhs.ry[v] = ay;
+                rhs.rz[v] = az;
+            } else if (ORDERED) {
+                pa.px[hdr.z + j] = ax;
+                pa.py[hdr.z + j] = ay;
+                pa.pz[hdr.z + j] = az;
+            } else {
+                atomicAdd(rhs.rx + v, ax);
+                atomicAdd(rhs.ry + v, ay);
+                atomicAdd(rhs.rz + v, az);
+            }
+        }
+        __syncthreads();  // blob b and res free again
+        if (tid == 0 && i + 2 < n_my) {
+            fence_proxy_async();
+            issue(i + 2, b);
         }
     }
 }
@@ -227,19 +399,19 @@ __global__ void __launch_bounds__(256) k_merge_partials(const int32_t *__restric
 }
 
 // ---------------------------------------------------------------------------
-// layout conversion: caller AoS (n,3) <-> internal SoA (with renumbering)
+// layout conversion: caller AoS (n,3) <-> internal records / SoA (renumbered)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_pack_aos(const double *__restrict__ aos,
-                                                  const int32_t *__restrict__ perm, int64_t n,
-                                                  double *ox, double *oy, double *oz)
+__global__ void __launch_bounds__(256) k_pack_velocity(const double *__restrict__ aos,
+                                                       const int32_t *__restrict__ perm, int64_t n,
+                                                       double *nrec)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n)
         return;
     const int64_t s = perm ? (int64_t)perm[i] : i;
-    ox[i] = aos[3 * s + 0];
-    oy[i] = aos[3 * s + 1];
-    oz[i] = aos[3 * s + 2];
+    nrec[6 * i + 3] = aos[3 * s + 0];
+    nrec[6 * i + 4] = aos[3 * s + 1];
+    nrec[6 * i + 5] = aos[3 * s + 2];
 }
 
 __global__ void __launch_bounds__(256) k_unpack_aos(const double *__restrict__ rx,

@@ -284,45 +284,193 @@ void element_order(int method, const int32_t *conn4, const double *coords_int, i
     }
 }
 
-bool build_chunks(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int chunk_elems,
-                  int chunk_nodes, Chunking &out, std::string &err)
+namespace {
+
+struct Arc {
+    std::vector<int32_t> tets, ring;
+    bool closed = false;
+};
+
+// ring of unassigned tets around edge (p,q) that contains tet t
+void ring_arc(int32_t t, int32_t p, int32_t q, const int32_t *conn4, const std::vector<int64_t> &off,
+              const std::vector<int32_t> &adj, const std::vector<uint8_t> &assigned, Arc &arc)
 {
-    if (chunk_elems < 1 || chunk_elems > 1024 || chunk_nodes < 4 || chunk_nodes > 2048) {
-        err = "chunk_elems must be in [1,1024] and chunk_nodes in [4,2048]";
-        return false;
+    // candidate tets: unassigned, contain p and q; their ring edge (c,d)
+    struct Cand {
+        int32_t tet, c, d;
+        bool used;
+    };
+    Cand cand[64];
+    int nc = 0;
+    for (int64_t k = off[p]; k < off[p + 1] && nc < 64; ++k) {
+        const int32_t s = adj[k];
+        if (assigned[s])
+            continue;
+        const int32_t *v = conn4 + 4 * (int64_t)s;
+        bool hq = false;
+        int32_t o[2], no = 0;
+        for (int a = 0; a < 4; ++a) {
+            if (v[a] == q)
+                hq = true;
+            else if (v[a] != p && no < 2)
+                o[no++] = v[a];
+        }
+        if (hq && no == 2)
+            cand[nc++] = {s, o[0], o[1], s == t};
     }
-    if (4 * chunk_elems > 65535) {
-        err = "chunk_elems too large for 16-bit slots";
+    int it = -1;
+    for (int i = 0; i < nc; ++i)
+        if (cand[i].tet == t)
+            it = i;
+    arc.tets.assign(1, t);
+    arc.closed = false;
+    if (it < 0) {  // should not happen
+        const int32_t *v = conn4 + 4 * (int64_t)t;
+        arc.ring.clear();
+        for (int a = 0; a < 4; ++a)
+            if (v[a] != p && v[a] != q)
+                arc.ring.push_back(v[a]);
+        return;
+    }
+    std::vector<int32_t> fwd{cand[it].d}, bwd{cand[it].c};
+    std::vector<int32_t> tf, tb;
+    const int max_tets = PATCH_MAX_RING - 1;
+    auto walk = [&](std::vector<int32_t> &seq, std::vector<int32_t> &ts, int budget) {
+        while ((int)ts.size() < budget) {
+            const int32_t cur = seq.back();
+            int found = -1;
+            for (int i = 0; i < nc; ++i)
+                if (!cand[i].used && (cand[i].c == cur || cand[i].d == cur)) {
+                    found = i;
+                    break;
+                }
+            if (found < 0)
+                return false;
+            cand[found].used = true;
+            const int32_t nxt = cand[found].c == cur ? cand[found].d : cand[found].c;
+            ts.push_back(cand[found].tet);
+            if (nxt == (&seq == &fwd ? bwd.front() : fwd.front()))
+                return true;  // closed the ring
+            seq.push_back(nxt);
+        }
+        return false;
+    };
+    const bool closed = walk(fwd, tf, max_tets - 1);
+    if (!closed)
+        walk(bwd, tb, max_tets - 1 - (int)tf.size());
+    arc.ring.clear();
+    for (auto i = bwd.rbegin(); i != bwd.rend(); ++i)
+        arc.ring.push_back(*i);
+    for (int32_t v : fwd)
+        arc.ring.push_back(v);
+    arc.tets.clear();
+    for (auto i = tb.rbegin(); i != tb.rend(); ++i)
+        arc.tets.push_back(*i);
+    arc.tets.push_back(t);
+    for (int32_t s : tf)
+        arc.tets.push_back(s);
+    arc.closed = closed;
+}
+
+}  // namespace
+
+void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int mode, Patches &out)
+{
+    out.off.assign(1, 0);
+    out.nodes.clear();
+    out.closed.clear();
+    if (mode == 0) {
+        out.off.reserve((size_t)n_elems + 1);
+        out.nodes.reserve((size_t)n_elems * 4);
+        for (int64_t e = 0; e < n_elems; ++e) {
+            for (int a = 0; a < 4; ++a)
+                out.nodes.push_back(conn4[4 * e + a]);
+            out.off.push_back((int32_t)out.nodes.size());
+            out.closed.push_back(0);
+        }
+        return;
+    }
+    // node -> tets
+    std::vector<int64_t> off((size_t)n_nodes + 1, 0);
+    for (int64_t i = 0; i < 4 * n_elems; ++i)
+        off[conn4[i] + 1]++;
+    for (int64_t v = 0; v < n_nodes; ++v)
+        off[v + 1] += off[v];
+    std::vector<int32_t> adj((size_t)(4 * n_elems));
+    {
+        std::vector<int64_t> pos(off.begin(), off.end() - 1);
+        for (int64_t e = 0; e < n_elems; ++e)
+            for (int a = 0; a < 4; ++a)
+                adj[pos[conn4[4 * e + a]]++] = (int32_t)e;
+    }
+    std::vector<uint8_t> assigned((size_t)n_elems, 0);
+    static const int EDGES[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    Arc best, cur;
+    int32_t best_p = 0, best_q = 0;
+    for (int64_t t = 0; t < n_elems; ++t) {
+        if (assigned[t])
+            continue;
+        const int32_t *v = conn4 + 4 * t;
+        size_t best_n = 0;
+        int64_t best_span = 0;
+        for (auto &ed : EDGES) {
+            const int32_t p = v[ed[0]], q = v[ed[1]];
+            ring_arc((int32_t)t, p, q, conn4, off, adj, assigned, cur);
+            int64_t lo = cur.tets[0], hi = cur.tets[0];
+            for (int32_t s : cur.tets) {
+                lo = std::min<int64_t>(lo, s);
+                hi = std::max<int64_t>(hi, s);
+            }
+            const int64_t span = hi - lo;
+            if (cur.tets.size() > best_n || (cur.tets.size() == best_n && span < best_span)) {
+                best_n = cur.tets.size();
+                best_span = span;
+                std::swap(best, cur);
+                best_p = p;
+                best_q = q;
+            }
+        }
+        for (int32_t s : best.tets)
+            assigned[s] = 1;
+        out.nodes.push_back(best_p);
+        out.nodes.push_back(best_q);
+        for (int32_t r : best.ring)
+            out.nodes.push_back(r);
+        out.off.push_back((int32_t)out.nodes.size());
+        out.closed.push_back(best.closed ? 1 : 0);
+    }
+}
+
+bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_nodes, int max_contrib,
+                  Chunking &out, std::string &err)
+{
+    if (max_patches < 1 || max_nodes < PATCH_MAX_RING + 2 || max_contrib < PATCH_MAX_RING + 2 ||
+        max_contrib > 65535 || max_nodes > 65535) {
+        err = "invalid chunk limits";
         return false;
     }
     out = Chunking();
-    out.chunk_elems = chunk_elems;
-    out.max_nodes = chunk_nodes;
-    out.lconn.resize((size_t)n_elems * 4);
-    out.csr_slots.resize((size_t)n_elems * 4);
+    out.max_patches = max_patches;
+    out.max_nodes = max_nodes;
+    out.max_contrib = max_contrib;
+    const int64_t np = P.n_patches();
+    out.precs.assign((size_t)np * 32, 0);
     std::vector<int32_t> stamp((size_t)n_nodes, -1), local((size_t)n_nodes, 0);
     std::vector<int32_t> cnt_chunks((size_t)n_nodes, 0);
-    std::vector<int32_t> nodes;  // current chunk's nodes (first-seen order)
-    std::vector<int32_t> counts;
-    nodes.reserve(chunk_nodes);
+    std::vector<int32_t> nodes, counts, fill;
     int32_t chunk = 0;
-    int64_t e_begin = 0;
+    int64_t p_begin = 0, contrib = 0;
 
-    auto close_chunk = [&](int64_t e_end) {
-        // sort the chunk's nodes ascending (coalesced staging loads), then
-        // rewrite local ids and build the chunk-local node->slot CSR
+    auto close_chunk = [&](int64_t p_end) {
         std::vector<int32_t> sorted(nodes);
         std::sort(sorted.begin(), sorted.end());
         for (size_t j = 0; j < sorted.size(); ++j)
             local[sorted[j]] = (int32_t)j;
-        const int32_t nn = (int32_t)sorted.size(), ne = (int32_t)(e_end - e_begin);
+        const int32_t nn = (int32_t)sorted.size();
         counts.assign((size_t)nn + 1, 0);
-        for (int64_t e = e_begin; e < e_end; ++e)
-            for (int a = 0; a < 4; ++a) {
-                const int32_t l = local[conn4[4 * e + a]];
-                out.lconn[4 * e + a] = (uint16_t)l;
-                counts[l + 1]++;
-            }
+        for (int64_t g = p_begin; g < p_end; ++g)
+            for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k)
+                counts[local[P.nodes[k]] + 1]++;
         for (int32_t j = 0; j < nn; ++j)
             counts[j + 1] += counts[j];
         const size_t node_begin = out.chunk_nodes.size();
@@ -331,51 +479,59 @@ bool build_chunks(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int ch
             out.csr_off.push_back((uint16_t)counts[j]);
             cnt_chunks[sorted[j]]++;
         }
-        std::vector<int32_t> fill(counts.begin(), counts.end() - 1);
-        for (int64_t e = e_begin; e < e_end; ++e)  // element order within each node
-            for (int a = 0; a < 4; ++a) {
-                const int32_t l = out.lconn[4 * e + a];
-                out.csr_slots[4 * e_begin + fill[l]++] =
-                    (uint16_t)(a * chunk_elems + (int32_t)(e - e_begin));
+        fill.assign(counts.begin(), counts.end() - 1);
+        for (int64_t g = p_begin; g < p_end; ++g) {  // patch order within each node
+            uint16_t *rec = out.precs.data() + 32 * g;
+            const int32_t m = P.off[g + 1] - P.off[g] - 2;
+            rec[0] = (uint16_t)(m | (P.closed[g] << 8));
+            for (int32_t k = 0; k < m + 2; ++k) {
+                const int32_t l = local[P.nodes[P.off[g] + k]];
+                rec[1 + k] = (uint16_t)l;
+                rec[16 + 1 + k] = (uint16_t)fill[l]++;
             }
-        out.chunks.push_back((int32_t)e_begin);
-        out.chunks.push_back(ne);
+        }
+        out.chunks.push_back((int32_t)p_begin);
+        out.chunks.push_back((int32_t)(p_end - p_begin));
         out.chunks.push_back((int32_t)node_begin);
         out.chunks.push_back(nn);
+        out.chunks.push_back((int32_t)contrib);
         nodes.clear();
         ++chunk;
-        e_begin = e_end;
+        p_begin = p_end;
+        contrib = 0;
     };
 
-    for (int64_t e = 0; e < n_elems; ++e) {
-        const int32_t *q = conn4 + 4 * e;
-        int fresh = 0;
-        for (int a = 0; a < 4; ++a) {
-            bool dup = false;
-            for (int b = 0; b < a; ++b)
-                dup |= (q[b] == q[a]);
-            if (!dup && stamp[q[a]] != chunk)
-                ++fresh;
+    for (int64_t g = 0; g < np; ++g) {
+        const int32_t n = P.off[g + 1] - P.off[g];
+        if (n - 2 > PATCH_MAX_RING || n < 4) {
+            err = "patch ring size out of range";
+            return false;
         }
-        if (e > e_begin && ((e - e_begin) + 1 > chunk_elems ||
-                            (int64_t)nodes.size() + fresh > chunk_nodes))
-            close_chunk(e);
-        for (int a = 0; a < 4; ++a)
-            if (stamp[q[a]] != chunk) {
-                stamp[q[a]] = chunk;
-                nodes.push_back(q[a]);
+        int fresh = 0;
+        for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k)
+            if (stamp[P.nodes[k]] != chunk)
+                ++fresh;
+        if (g > p_begin && ((g - p_begin) + 1 > max_patches || (int64_t)nodes.size() + fresh > max_nodes ||
+                            contrib + n > max_contrib))
+            close_chunk(g);
+        for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
+            const int32_t v = P.nodes[k];
+            if (stamp[v] != chunk) {
+                stamp[v] = chunk;
+                nodes.push_back(v);
             }
+        }
+        contrib += n;
     }
-    if (n_elems > e_begin)
-        close_chunk(n_elems);
+    if (np > p_begin)
+        close_chunk(np);
 
     // interior flag + shared/isolated node lists for the ordered merge
     const int64_t total = (int64_t)out.chunk_nodes.size();
-    std::vector<int32_t> pos_count((size_t)n_nodes + 1, 0);
-    for (int64_t p = 0; p < total; ++p) {
-        const int32_t v = out.chunk_nodes[p];
+    for (int64_t q = 0; q < total; ++q) {
+        const int32_t v = out.chunk_nodes[q];
         if (cnt_chunks[v] == 1)
-            out.chunk_nodes[p] = (int32_t)((uint32_t)v | 0x80000000u);
+            out.chunk_nodes[q] = (int32_t)((uint32_t)v | 0x80000000u);
     }
     for (int64_t v = 0; v < n_nodes; ++v)
         if (cnt_chunks[v] != 1) {
@@ -383,7 +539,6 @@ bool build_chunks(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int ch
             if (cnt_chunks[v] > 1)
                 out.n_shared++;
         }
-    // positions per boundary node, in chunk order
     std::vector<int32_t> bidx((size_t)n_nodes, -1);
     for (size_t i = 0; i < out.bnd_nodes.size(); ++i)
         bidx[out.bnd_nodes[i]] = (int32_t)i;
@@ -392,14 +547,37 @@ bool build_chunks(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int ch
         out.bnd_off[i + 1] = out.bnd_off[i] + cnt_chunks[out.bnd_nodes[i]];
     out.bnd_pos.resize((size_t)out.bnd_off.back());
     std::vector<int32_t> bfill(out.bnd_off.begin(), out.bnd_off.end() - 1);
-    for (int64_t p = 0; p < total; ++p) {
-        const uint32_t raw = (uint32_t)out.chunk_nodes[p];
+    for (int64_t q = 0; q < total; ++q) {
+        const uint32_t raw = (uint32_t)out.chunk_nodes[q];
         if (raw & 0x80000000u)
             continue;
-        const int32_t b = bidx[raw];
-        out.bnd_pos[bfill[b]++] = (int32_t)p;
+        out.bnd_pos[bfill[bidx[raw]]++] = (int32_t)q;
     }
     return true;
+}
+
+void pack_blobs(const Chunking &ch, std::vector<uint8_t> &blobs, std::vector<int32_t> &blob_off)
+{
+    const int64_t n_chunks = (int64_t)ch.chunks.size() / 5;
+    auto pad = [](int64_t b) { return (b + 15) / 16 * 16; };
+    blob_off.assign((size_t)n_chunks + 1, 0);
+    int64_t total = 0;
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        const int64_t npch = ch.chunks[5 * c + 1], nn = ch.chunks[5 * c + 3];
+        total += 16 + 64 * npch + pad(2 * nn) + pad(4 * nn);
+        blob_off[c + 1] = (int32_t)(total / 16);
+    }
+    blobs.assign((size_t)total, 0);
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        const int32_t p0 = ch.chunks[5 * c], npch = ch.chunks[5 * c + 1];
+        const int32_t n0 = ch.chunks[5 * c + 2], nn = ch.chunks[5 * c + 3];
+        uint8_t *b = blobs.data() + (int64_t)blob_off[c] * 16;
+        const int32_t hdr[4] = {npch, nn, n0, ch.chunks[5 * c + 4]};
+        std::memcpy(b, hdr, 16);
+        std::memcpy(b + 16, ch.precs.data() + 32 * (int64_t)p0, 64 * (size_t)npch);
+        std::memcpy(b + 16 + 64 * npch, ch.csr_off.data() + n0, 2 * (size_t)nn);
+        std::memcpy(b + 16 + 64 * npch + pad(2 * nn), ch.chunk_nodes.data() + n0, 4 * (size_t)nn);
+    }
 }
 
 }  // namespace tal

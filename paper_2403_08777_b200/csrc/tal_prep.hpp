@@ -28,20 +28,40 @@ void renumber_sfc(const double *coords, int64_t n_nodes, std::vector<int32_t> &p
 void element_order(int method, const int32_t *conn4, const double *coords_int, int64_t n_nodes,
                    int64_t n_elems, std::vector<int32_t> &eperm);
 
-// CTA chunking for the private scatter.
+// Patches: the unit of work of one thread in the private scatter.  A patch
+// is the ring of tets around one edge (a,b): ring nodes r_0..r_{m-1}, tet i =
+// (a, b, r_i, r_{i+1}) for i < k, with k = m for a closed ring (r_m = r_0)
+// and k = m - 1 for an open one.  A lone tet (c0,c1,c2,c3) is the open ring
+// a=c0, b=c1, r=(c2,c3).  Tets keep no corner order: the symmetric-rule
+// element operator is invariant under corner permutation (|det|, sgn det).
+constexpr int PATCH_MAX_RING = 13;  // ring nodes per patch (record: 16 u16)
+struct Patches {
+    std::vector<int32_t> off;    // n_patches + 1, into nodes
+    std::vector<int32_t> nodes;  // a, b, r_0 .. r_{m-1}
+    std::vector<uint8_t> closed;
+    int64_t n_patches() const { return (int64_t)off.size() - 1; }
+};
+// mode 0: one patch per tet; mode 1: greedy edge stars (largest ring of
+// still-unassigned tets around one of the current tet's edges; ties -> the
+// most compact tet-index span), tets visited in the given order.
+void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int mode, Patches &out);
+
+// CTA chunking of the patch sequence for the private scatter.
 struct Chunking {
-    int chunk_elems = 0, max_nodes = 0;
-    std::vector<int32_t> chunks;       // 4 per chunk: elem_begin, n_elem, node_begin, n_node
+    int max_patches = 0, max_nodes = 0, max_contrib = 0;
+    std::vector<int32_t> chunks;       // 5 per chunk: patch_begin, n_patch, node_begin, n_node, n_contrib
     std::vector<int32_t> chunk_nodes;  // node id | (1u<<31 if the node is interior to the chunk)
-    std::vector<uint16_t> csr_off;     // per chunk node: first slot index (chunk-relative)
-    std::vector<uint16_t> csr_slots;   // 4 per element: slot = corner*chunk_elems + e_local
-    std::vector<uint16_t> lconn;       // 4 per element: chunk-local node ids
+    std::vector<uint16_t> csr_off;     // per chunk node: first contribution index
+    std::vector<uint16_t> precs;       // 32 per patch: ids[16] (m|closed<<8, a, b, r..), pos[16]
     // deterministic merge: for nodes in >1 chunk (and isolated nodes), the
     // chunk-node positions holding their partial sums, in chunk order
     std::vector<int32_t> bnd_nodes, bnd_off, bnd_pos;
     int64_t n_shared = 0;
 };
-bool build_chunks(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int chunk_elems,
-                  int chunk_nodes, Chunking &out, std::string &err);
+bool build_chunks(const Patches &p, int64_t n_nodes, int max_patches, int max_nodes, int max_contrib,
+                  Chunking &out, std::string &err);
+// One contiguous 16-B aligned record per chunk (layout: tal_kernels.cuh);
+// blob_off[c] in 16-byte units, n_chunks+1 entries.
+void pack_blobs(const Chunking &ch, std::vector<uint8_t> &blobs, std::vector<int32_t> &blob_off);
 
 }  // namespace tal

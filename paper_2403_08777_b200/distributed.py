@@ -1,0 +1,200 @@
+"""Multi-GPU domain decomposition of the assembly: z-slabs + interface sum.
+
+The reference has no distributed path (the
+assembly is "trivially parallel"); this is the B200 extension of its
+element-slab parallelism (variants.py:467-503, _slab_bounds) to one process
+per GPU.  The path shards naturally: rank r assembles the contiguous cell
+layers [k_r, k_{r+1}) of a structured box, which are a contiguous element
+range (e = 6 (i + nx (j + ny k)) + t, mesh.py:148-150) touching node planes
+k_r .. k_{r+1}.  Only the two interface planes are shared, so the single
+exchange step is: every rank sends its partial RHS of each interface plane
+to the neighbour and adds what it receives (NCCL send/recv over NVLink,
+``torch.distributed`` as the plumbing).  Each shared node then holds the full
+sum on both ranks.
+
+``SlabPartition`` is pure host logic (tested with gloo on CPU);
+``SlabDomain`` binds it to an ``Assembler`` on the rank's GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .mesh import Mesh, _box_arrays
+
+
+def slab_bounds(n_layers: int, world: int) -> list[tuple[int, int]]:
+    """Near-equal contiguous split (same rule as variants._slab_bounds)."""
+    q, r = divmod(n_layers, world)
+    out, lo = [], 0
+    for i in range(world):
+        hi = lo + q + (1 if i < r else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def _axis(n: int, ext: float) -> np.ndarray:
+    # np.linspace(0, ext, n+1) semantics (mesh.py:159-161)
+    v = np.arange(n + 1, dtype=np.float64) * (ext / n)
+    v[-1] = ext
+    return v
+
+
+@dataclass(frozen=True)
+class SlabPartition:
+    """Rank ``rank``'s z-slab of an (nx, ny, nz) Kuhn box over ``world`` ranks."""
+
+    cells: tuple[int, int, int]
+    rank: int
+    world: int
+    extents: tuple[float, float, float] = (1.0, 1.0, 1.0)
+
+    def __post_init__(self):
+        nx, ny, nz = self.cells
+        if nz < self.world:
+            raise ValueError("need at least one cell layer per rank")
+        if not 0 <= self.rank < self.world:
+            raise ValueError("rank out of range")
+
+    @property
+    def layers(self) -> tuple[int, int]:
+        return slab_bounds(self.cells[2], self.world)[self.rank]
+
+    @property
+    def plane(self) -> int:
+        nx, ny, _ = self.cells
+        return (nx + 1) * (ny + 1)
+
+    @property
+    def n_global_nodes(self) -> int:
+        nx, ny, nz = self.cells
+        return (nx + 1) * (ny + 1) * (nz + 1)
+
+    @property
+    def node_range(self) -> tuple[int, int]:
+        """Global node ids [lo, hi) of this slab (node planes k0..k1)."""
+        k0, k1 = self.layers
+        return k0 * self.plane, (k1 + 1) * self.plane
+
+    @property
+    def elem_range(self) -> tuple[int, int]:
+        nx, ny, _ = self.cells
+        k0, k1 = self.layers
+        return 6 * nx * ny * k0, 6 * nx * ny * k1
+
+    def local_mesh(self) -> Mesh:
+        """The slab as a mesh; local node l <-> global node node_range[0] + l,
+        coordinates bitwise equal to the global box's."""
+        nx, ny, nz = self.cells
+        k0, k1 = self.layers
+        _, conn = _box_arrays(nx, ny, k1 - k0)
+        xs = _axis(nx, self.extents[0])
+        ys = _axis(ny, self.extents[1])
+        zs = _axis(nz, self.extents[2])[k0:k1 + 1]
+        zz, yy, xx = np.meshgrid(zs, ys, xs, indexing="ij")
+        coords = np.column_stack([xx.ravel(), yy.ravel(), zz.ravel()])
+        return Mesh(coords=coords, connectivity=conn)
+
+    def interfaces(self) -> dict[int, np.ndarray]:
+        """Neighbour rank -> local node ids of the shared plane (same global
+        order on both sides)."""
+        k0, k1 = self.layers
+        P = self.plane
+        out = {}
+        if self.rank > 0:
+            out[self.rank - 1] = np.arange(0, P, dtype=np.int64)
+        if self.rank < self.world - 1:
+            out[self.rank + 1] = np.arange((k1 - k0) * P, (k1 - k0 + 1) * P, dtype=np.int64)
+        return out
+
+    def owned_mask(self) -> np.ndarray:
+        """Nodes this rank reports in a gathered global vector (the top plane
+        belongs to the upper neighbour)."""
+        lo, hi = self.node_range
+        m = np.ones(hi - lo, dtype=bool)
+        if self.rank < self.world - 1:
+            m[-self.plane:] = False
+        return m
+
+    def velocity(self, spec: str, mesh: Optional[Mesh] = None) -> np.ndarray:
+        """The global field restricted to this slab (global extents / rng)."""
+        from .fields import make_velocity
+        mesh = mesh or self.local_mesh()
+        name, _, arg = spec.partition(":")
+        lo, hi = self.node_range
+        if name == "random":
+            seed = int(arg) if arg else 0
+            # draw the global stream, keep this slab's rows (bitwise the global field)
+            rng = np.random.default_rng(seed)
+            if lo:
+                rng.uniform(-1.0, 1.0, size=(lo, 3))
+            return rng.uniform(-1.0, 1.0, size=(hi - lo, 3))
+        if name == "taylor-green":
+            c = mesh.coords
+            s = np.pi * c / np.asarray(self.extents)
+            u = np.zeros((c.shape[0], 3))
+            u[:, 0] = np.sin(s[:, 0]) * np.cos(s[:, 1]) * np.cos(s[:, 2])
+            u[:, 1] = -np.cos(s[:, 0]) * np.sin(s[:, 1]) * np.cos(s[:, 2])
+            return u
+        return make_velocity(mesh, spec)
+
+
+def exchange_interfaces(part: SlabPartition, send: dict, recv: dict, group=None) -> None:
+    """Post the interface-plane send/recv pairs with every neighbour and wait.
+
+    ``send[nbr]`` / ``recv[nbr]`` are same-shaped tensors (CUDA under NCCL, CPU
+    under gloo); after return ``recv[nbr]`` holds the neighbour's partial sums.
+    """
+    import torch.distributed as dist
+    ops = []
+    for nbr in sorted(send):
+        ops.append(dist.P2POp(dist.isend, send[nbr], nbr, group=group))
+        ops.append(dist.P2POp(dist.irecv, recv[nbr], nbr, group=group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+class SlabDomain:
+    """One rank's slab on its GPU: local assembly + NCCL interface sum."""
+
+    def __init__(self, cells, rank: int, world: int, cfg=None):
+        import torch
+
+        from .assembly import Assembler, RunConfig
+        self.part = SlabPartition(tuple(int(c) for c in cells), rank, world)
+        self.cfg = cfg or RunConfig()
+        self.mesh = self.part.local_mesh()
+        self.assembler = Assembler(self.mesh, self.cfg)
+        dev = torch.device("cuda", self.cfg.device)
+        self._lists, self._send, self._recv = {}, {}, {}
+        for nbr, ids in self.part.interfaces().items():
+            internal = self.assembler.map_nodes(ids)
+            self._lists[nbr] = torch.as_tensor(internal, device=dev)
+            self._send[nbr] = torch.empty((ids.size, 3), dtype=torch.float64, device=dev)
+            self._recv[nbr] = torch.empty((ids.size, 3), dtype=torch.float64, device=dev)
+
+    def velocity(self, spec: str) -> np.ndarray:
+        u = self.part.velocity(spec, self.mesh)
+        self.assembler.set_velocity_host(u, stream=0)
+        return u
+
+    def step(self, params, stream=0) -> int:
+        """Local assembly, then the interface exchange; returns kernels launched."""
+        asm = self.assembler
+        n = asm.run(params, stream=stream)
+        for nbr, lst in self._lists.items():
+            asm.halo_pack(lst.data_ptr(), lst.numel(), self._send[nbr].data_ptr(), stream=stream)
+            n += 1
+        exchange_interfaces(self.part, self._send, self._recv)
+        for nbr, lst in self._lists.items():
+            asm.halo_accumulate(lst.data_ptr(), lst.numel(), self._recv[nbr].data_ptr(), stream=stream)
+            n += 1
+        return n
+
+    def close(self) -> None:
+        self.assembler.close()

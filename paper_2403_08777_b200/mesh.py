@@ -144,3 +144,26 @@ def permute_nodes(mesh, perm: np.ndarray) -> Mesh:
     inv = np.empty_like(perm)
     inv[perm] = np.arange(perm.size)
     return Mesh(coords=np.asarray(mesh.coords)[perm], connectivity=inv[np.asarray(mesh.connectivity)])
+
+
+def edge_star_patches(mesh, mode: str = "star"):
+    """The private scatter's work decomposition (tal_prep.hpp): a list of
+    (a, b, ring, closed) with tets (a, b, ring[i], ring[i+1])."""
+    from ._native import PATCHES
+    conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int64)
+    n_nodes = mesh.coords.shape[0]
+    npch = ctypes.c_int64(0)
+    nn = ctypes.c_int64(0)
+    L = lib()
+    check(L.tal_build_patches(ptr(conn), n_nodes, conn.shape[0], PATCHES[mode], ctypes.byref(npch),
+                              ctypes.byref(nn), None, None, None))
+    off = np.empty(npch.value + 1, dtype=np.int32)
+    nodes = np.empty(nn.value, dtype=np.int32)
+    closed = np.empty(npch.value, dtype=np.uint8)
+    check(L.tal_build_patches(ptr(conn), n_nodes, conn.shape[0], PATCHES[mode], ctypes.byref(npch),
+                              ctypes.byref(nn), ptr(off), ptr(nodes), ptr(closed)))
+    out = []
+    for g in range(npch.value):
+        seg = nodes[off[g]:off[g + 1]]
+        out.append((int(seg[0]), int(seg[1]), [int(x) for x in seg[2:]], bool(closed[g])))
+    return out

@@ -1,0 +1,108 @@
+"""CPU tests of the multi-GPU decomposition (host logic + the exchange
+protocol over gloo, world_size 2 and 3).  The per-rank local assembly is
+stood in for by the CPU oracle here; on GPUs the same exchange runs over
+NCCL between libtal_b200 halo pack/accumulate kernels (SlabDomain.step)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2403_08777_b200.distributed import SlabPartition, exchange_interfaces, slab_bounds
+import paper_2403_08777_b200 as tb
+
+
+def test_slab_bounds_cover():
+    for n, w in [(8, 2), (7, 3), (128, 8), (5, 5)]:
+        b = slab_bounds(n, w)
+        assert b[0][0] == 0 and b[-1][1] == n
+        assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
+        assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_local_meshes_are_slices_of_the_global_box(world):
+    cells = (3, 2, 7)
+    g = tb.generate_box_mesh(*cells)
+    elems = 0
+    for r in range(world):
+        p = SlabPartition(cells, r, world)
+        m = p.local_mesh()
+        lo, hi = p.node_range
+        e0, e1 = p.elem_range
+        np.testing.assert_array_equal(m.coords, g.coords[lo:hi])
+        np.testing.assert_array_equal(m.connectivity + lo, g.connectivity[e0:e1])
+        elems += m.n_elems
+        for nbr, ids in p.interfaces().items():
+            q = SlabPartition(cells, nbr, world)
+            other = q.interfaces()[r]
+            np.testing.assert_array_equal(ids + lo, other + q.node_range[0])
+    assert elems == g.n_elems
+
+
+@pytest.mark.parametrize("spec", ["random:1", "taylor-green", "shear:1.5"])
+def test_slab_velocity_is_the_global_field(spec):
+    cells = (4, 3, 6)
+    g = tb.generate_box_mesh(*cells)
+    ug = tb.make_velocity(g, spec)
+    for r in range(3):
+        p = SlabPartition(cells, r, 3)
+        lo, hi = p.node_range
+        np.testing.assert_array_equal(p.velocity(spec), ug[lo:hi])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, cells, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    p = SlabPartition(cells, rank, world)
+    m = p.local_mesh()
+    u = p.velocity("random:1", m)
+    rhs = O.assemble_rsp(m.coords, m.connectivity, u)  # stand-in for the GPU local assembly
+    send, recv = {}, {}
+    for nbr, ids in p.interfaces().items():
+        send[nbr] = torch.from_numpy(rhs[ids].copy())
+        recv[nbr] = torch.empty_like(send[nbr])
+    exchange_interfaces(p, send, recv)
+    for nbr, ids in p.interfaces().items():
+        rhs[ids] += recv[nbr].numpy()
+    np.save(os.path.join(out_dir, f"rhs_{rank}.npy"), rhs)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_interface_exchange_gloo_matches_single_domain(tmp_path, world, oracle):
+    cells = (5, 4, 7)
+    mp.start_processes(_worker, args=(world, _free_port(), cells, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    g = oracle.box_mesh(*cells)
+    ug = oracle.velocity(g.coords, "random:1")
+    ref = oracle.assemble_rsp(g.coords, g.connectivity, ug)
+    full = np.full_like(ref, np.nan)
+    for r in range(world):
+        p = SlabPartition(cells, r, world)
+        lo, hi = p.node_range
+        loc = np.load(tmp_path / f"rhs_{r}.npy")
+        mask = p.owned_mask()
+        full[lo:hi][mask] = loc[mask]
+        # shared planes agree on both sides after the exchange
+        for nbr, ids in p.interfaces().items():
+            q = SlabPartition(cells, nbr, world)
+            other = np.load(tmp_path / f"rhs_{nbr}.npy")[q.interfaces()[r]]
+            assert np.abs(loc[ids] - other).max() <= 1e-15 * np.abs(ref).max()
+    assert not np.isnan(full).any()
+    chk = oracle.compare(full, ref, g.coords, g.connectivity, ug)
+    assert chk.passed, chk

@@ -51,14 +51,15 @@ def test_renumbering_and_element_order(oracle, golden_mid, renumber, order):
         assert_parity(oracle, res.rhs, golden_mid["oracle_8_random"], m, u)
 
 
-@pytest.mark.parametrize("ce,cn", [(1, 4), (7, 16), (64, 128), (512, 1024), (1024, 2048),
-                                   (1024, 64)])
-def test_chunk_shape_invariance(oracle, golden_mid, ce, cn):
+@pytest.mark.parametrize("patches", ["star", "tet"])
+@pytest.mark.parametrize("cp,cn", [(1, 16), (7, 16), (64, 144), (64, 40), (100, 256), (128, 256),
+                                   (128, 64), (128, 16)])
+def test_chunk_shape_invariance(oracle, golden_mid, patches, cp, cn):
     m = tb.generate_box_mesh(16, 16, 16)
     u = tb.make_velocity(m, "taylor-green")
     ref = golden_mid["rsp_16_taylor-green"]
     for mode in ("private", "private-atomic"):
-        res = run(m, u, scatter=mode, chunk_elems=ce, chunk_nodes=cn)
+        res = run(m, u, scatter=mode, patches=patches, cta_patches=cp, chunk_nodes=cn)
         assert_parity(oracle, res.rhs, ref, m, u)
 
 

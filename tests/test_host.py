@@ -106,8 +106,9 @@ def test_mesh_validation_errors():
 
 def test_runconfig_validation():
     for kw in [dict(vector_dim=0), dict(n_threads=0), dict(reps=0), dict(scatter="bogus"),
-               dict(renumber="x"), dict(element_order="x"), dict(chunk_elems=0),
-               dict(chunk_elems=2048), dict(chunk_nodes=2), dict(device=-1),
+               dict(renumber="x"), dict(element_order="x"), dict(cta_patches=0),
+               dict(cta_patches=129), dict(chunk_nodes=8), dict(chunk_nodes=257),
+               dict(cta_patches=64, chunk_nodes=145), dict(patches="x"), dict(device=-1),
                dict(cache_capacity_bytes=-1)]:
         with pytest.raises(ValueError):
             tb.RunConfig(**kw)
@@ -181,3 +182,45 @@ def test_product_never_imports_oracle():
         src = f.read_text()
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\S+)", src, flags=re.M), f
         assert "tal_oracle" not in src, f
+
+
+def _patch_tets(patches):
+    tets = []
+    for a, b, ring, closed in patches:
+        m = len(ring)
+        k = m if closed else m - 1
+        for i in range(k):
+            tets.append(tuple(sorted((a, b, ring[i], ring[(i + 1) % m]))))
+    return tets
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 1), (2, 3, 2), (4, 4, 4), (7, 5, 3)])
+@pytest.mark.parametrize("mode", ["star", "tet"])
+def test_patches_cover_every_tet_once(dims, mode):
+    from paper_2403_08777_b200.mesh import edge_star_patches
+    m = tb.generate_box_mesh(*dims)
+    pt = _patch_tets(edge_star_patches(m, mode))
+    ref = sorted(tuple(sorted(t)) for t in m.connectivity.tolist())
+    assert sorted(pt) == ref
+
+
+def test_kuhn_box_decomposes_into_closed_six_rings():
+    """Every Kuhn cell is the closed ring of 6 tets around its main diagonal."""
+    from paper_2403_08777_b200.mesh import edge_star_patches
+    m = tb.generate_box_mesh(6, 5, 4)
+    p = edge_star_patches(m, "star")
+    assert len(p) == 6 * 5 * 4
+    assert all(closed and len(ring) == 6 for _, _, ring, closed in p)
+
+
+def test_patches_on_permuted_and_perturbed_mesh():
+    """General (non-box) connectivity: random node numbering plus a mesh with
+    tets removed still decompose exactly."""
+    from paper_2403_08777_b200.mesh import edge_star_patches
+    base = tb.generate_box_mesh(5, 4, 4)
+    pm = tb.permute_nodes(base, np.random.default_rng(3).permutation(base.n_nodes))
+    keep = np.random.default_rng(4).random(pm.n_elems) < 0.7
+    sub = tb.Mesh(coords=pm.coords, connectivity=pm.connectivity[keep])
+    for mesh in (pm, sub):
+        pt = _patch_tets(edge_star_patches(mesh, "star"))
+        assert sorted(pt) == sorted(tuple(sorted(t)) for t in mesh.connectivity.tolist())

@@ -1,0 +1,55 @@
+"""Summarise an ncu --set full report: headline metrics + stall breakdown.
+
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--json out.json]
+"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units = rows[0], rows[1]
+out = {}
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    name = d.get("Kernel Name", "?")
+    g = lambda k: d.get(k, "")
+    def f(k):
+        try:
+            return float(g(k).replace(",", ""))
+        except ValueError:
+            return None
+    stalls = {}
+    for k in hdr:
+        m = re.match(r"smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio$", k)
+        if m and f(k):
+            stalls[m.group(1)] = round(f(k), 3)
+    s = {
+        "kernel": name,
+        "duration_us": (f("gpu__time_duration.sum") or 0) / 1e3,
+        "sm_mhz": (f("smsp__cycles_elapsed.avg.per_second") or 0) / 1e6,
+        "dram_read_bytes": f("dram__bytes_read.sum"),
+        "dram_write_bytes": f("dram__bytes_write.sum"),
+        "fp64_pipe_pct": f("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+        "issue_active_pct": f("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+        "warps_active_per_sm": f("sm__warps_active.avg.per_cycle_active"),
+        "registers": f("launch__registers_per_thread"),
+        "smem_per_block": f("launch__shared_mem_per_block_dynamic"),
+        "inst_executed": f("smsp__inst_executed.sum"),
+        "dfma_thread_inst": f("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum"),
+        "dmul_thread_inst": f("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"),
+        "dadd_thread_inst": f("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"),
+        "shared_bank_conflicts": f("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+        "l2_hit_pct": f("lts__t_sector_hit_rate.pct"),
+        "red_sectors": f("l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum"),
+        "stalls_per_issue": dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:10]),
+    }
+    out[name] = s
+for name, s in out.items():
+    print(json.dumps(s, indent=1))
+if "--json" in sys.argv:
+    json.dump(out, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
