@@ -13,7 +13,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libtal_b200.so"
+LIB_PATH = Path(os.environ.get("TAL_LIB_PATH") or Path(__file__).resolve().parent / "libtal_b200.so")
 
 TAL_OK, TAL_EINVAL, TAL_ECUDA, TAL_ENOMEM, TAL_ESTATE = 0, 1, 2, 3, 4
 

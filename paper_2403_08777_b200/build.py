@@ -44,21 +44,25 @@ def up_to_date() -> bool:
     return all(s.stat().st_mtime <= t for s in _sources())
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    if not force and up_to_date():
+def build(verbose: bool = False, force: bool = False, out: Path = OUT, defines=(),
+          tag: str = "") -> Path:
+    """Compile libtal_b200.so.  ``defines``/``out``/``tag`` build tuning
+    variants (e.g. ``TAL_RING_UNROLL=2``) side by side for A/B timing."""
+    if out == OUT and not defines and not force and up_to_date():
         return OUT
     BUILD.mkdir(exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     nvcc = _nvcc()
     objs = []
     log = []
     for src in sorted(CSRC.glob("*.cpp")):
-        obj = BUILD / (src.stem + ".o")
-        cmd = ["g++", "-O3", "-fPIC", "-std=c++17", "-Wall", "-c", str(src), "-o", str(obj)]
+        obj = BUILD / (src.stem + tag + ".o")
+        cmd = ["g++", "-O3", "-fPIC", "-std=c++17", "-Wall", *dflags, "-c", str(src), "-o", str(obj)]
         subprocess.run(cmd, check=True)
         objs.append(obj)
     for src in sorted(CSRC.glob("*.cu")):
-        obj = BUILD / (src.stem + ".o")
-        cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        obj = BUILD / (src.stem + tag + ".o")
+        cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *dflags,
                "-Xptxas", "-v", "--expt-relaxed-constexpr", "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, check=False, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
@@ -66,15 +70,17 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src.name}")
         objs.append(obj)
-    tmp = OUT.with_suffix(".so.tmp")
+    out = Path(out)
+    out.parent.mkdir(parents=True, exist_ok=True)
+    tmp = out.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs),
            "-lpthread"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, OUT)
-    (BUILD / "ptxas.log").write_text("".join(log))
+    os.replace(tmp, out)
+    (BUILD / f"ptxas{tag}.log").write_text("".join(log))
     if verbose:
         print("".join(log))
-    return OUT
+    return out
 
 
 def main() -> None:

@@ -266,7 +266,7 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         if (!sym)  // patches permute tet corners: only valid for the symmetric rule
             return launch_run(h, p, TAL_SCATTER_ATOMIC, s, launches);
         const bool ordered = scatter == TAL_SCATTER_PRIVATE;
-        const int64_t ncn = (int64_t)h->ch.chunk_nodes.size();
+        const int64_t ncn = (int64_t)h->ch.cnodes.size();
         PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr, nullptr, nullptr};
         if (ordered && h->d_partial) {
             pa.px = h->d_partial;
@@ -507,7 +507,7 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
     h->info.n_patches = patches.n_patches();
     std::vector<uint8_t> blobs;
     std::vector<int32_t> blob_off;
-    pack_blobs(h->ch, blobs, blob_off);
+    pack_blobs(h->ch, cfg_threads(cfg), blobs, blob_off);
     // colouring (caller's or greedy on the internal order), colour-sorted copy
     std::vector<int64_t> col;
     int64_t ncol = 0;
@@ -585,9 +585,9 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
         return rc;
     if ((rc = dev_upload(&h->d_bnd_pos, C.bnd_pos.data(), C.bnd_pos.size())))
         return rc;
-    if (!C.chunk_nodes.empty())
-        TAL_CK(cudaMalloc((void **)&h->d_partial, sizeof(double) * 3 * C.chunk_nodes.size()));
-    bytes += blobs.size() + blob_off.size() * 4 + C.chunk_nodes.size() * 24 +
+    if (!C.cnodes.empty())
+        TAL_CK(cudaMalloc((void **)&h->d_partial, sizeof(double) * 3 * C.cnodes.size()));
+    bytes += blobs.size() + blob_off.size() * 4 + C.cnodes.size() * 24 +
              (C.bnd_nodes.size() + C.bnd_off.size() + C.bnd_pos.size()) * 4;
     if ((rc = set_kernel_attrs(h->device, h->priv_cfg, &h->priv_grid)))
         return rc;
@@ -598,7 +598,7 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
     h->info.n_elems = n_elems;
     h->info.n_colors = col.empty() ? 0 : ncol;
     h->info.n_chunks = (int64_t)C.chunks.size() / 5;
-    h->info.n_chunk_nodes = (int64_t)C.chunk_nodes.size();
+    h->info.n_chunk_nodes = (int64_t)C.cnodes.size();
     h->info.n_shared_nodes = C.n_shared;
     h->info.device_bytes = (int64_t)bytes;
     h->info.prep_seconds = std::chrono::duration<double>(t1 - t0).count();

@@ -25,8 +25,10 @@
 //        w_a = A (po S + (pd-po) u_a) + B c_a,
 //        A = nrv / D = -rho sgn(D) / 24,  B = nvv / D^2 = -vis / (6 |D|),
 //    and w_0 = (4 A po + A (pd-po)) S - (w_1 + w_2 + w_3) since sum_a c_a = 0.
-// ~205 FP64 instructions per element (FMA = 1) against the reference ledger's
-// 448 flop (variants.py:207-217).
+//  * Special functions: MUFU seeds + one third-order correction each
+//    (rcbrt_fast, rsqrt_fast), branch-free in the normal range.
+// ~185 FP64 instructions per tet inside an edge-star ring (FMA = 1) against
+// the reference ledger's 448 flop (variants.py:207-217).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -46,38 +48,57 @@ __device__ __forceinline__ void cross3(const double a[3], const double b[3], dou
     c[2] = fma(a[0], b[1], -a[1] * b[0]);
 }
 
-// Geometry, velocity gradient, Vreman.  Outputs cofactor rows cf[1..3], the
-// unscaled gradient Gh, sgn(D) and B = -vis / (6 |D|).
-__device__ __forceinline__ void element_core(const double X[4][3], const double U[4][3],
-                                             const ElemConsts &k, double cf[4][3],
-                                             double Gh[3][3], double &sg, double &B)
+// |x|^(-1/3) for normal positive x: exponent split x = m 2^(3k), m in [1,8),
+// single-precision MUFU seed (lg2/ex2, ~1e-6), one third-order correction
+// y <- y (1 + e/3 + 2e^2/9 + 14e^3/81), e = 1 - m y^3 (error ~e^4 << 1 ulp).
+// Branch-free; 8 FP64 instructions.
+__device__ __forceinline__ double rcbrt_fast(double x)
 {
-    double e[3][3];
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            e[b][c] = X[b + 1][c] - X[0][c];
-    cross3(e[1], e[2], cf[1]);  // e2 x e3
-    cross3(e[2], e[0], cf[2]);  // e3 x e1
-    cross3(e[0], e[1], cf[3]);  // e1 x e2
-    const double det = fma(e[0][0], cf[1][0], fma(e[0][1], cf[1][1], e[0][2] * cf[1][2]));
-    const double ad = fabs(det);
-    sg = (det < 0.0) ? -1.0 : 1.0;
-    const double r3 = rcbrt(ad);     // |D|^(-1/3)
-    const double inv = r3 * r3 * r3; // 1/|D|
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    const int ex = ((hi >> 20) & 0x7ff) - 1023;
+    const int k = (ex + 1200) / 3 - 400;  // floor(ex / 3)
+    const double m = __hiloint2double(hi - ((3 * k) << 20), lo);
+    float l;
+    const float mf = __double2float_rn(m);
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(mf));
+    float y0;
+    const float a = l * (-1.0f / 3.0f);
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y0) : "f"(a));
+    double y = (double)y0;
+    const double e = fma(-m, (y * y) * y, 1.0);
+    const double p = fma(e, fma(e, 14.0 / 81.0, 2.0 / 9.0), 1.0 / 3.0);
+    y = fma(y * e, p, y);
+    return y * __hiloint2double((1023 - k) << 20, 0);
+}
 
-    double du[3][3];
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-            du[b][i] = U[b + 1][i] - U[0][i];
+// t^(-1/2) for normal positive t: MUFU.RSQ64H seed + one third-order
+// correction y <- y (1 + e/2 + 3e^2/8 + 5e^3/16), e = 1 - t y^2.
+__device__ __forceinline__ double rsqrt_fast(double t)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(t));
+    const double e = fma(-t, y * y, 1.0);
+    const double p = fma(e, fma(e, 5.0 / 16.0, 3.0 / 8.0), 0.5);
+    return fma(y * e, p, y);
+}
+
+// Everything after the cofactor rows: velocity gradient, Vreman, the two
+// weighted terms.  c[1..3] = cofactor rows, D = det, du[b] = u_b - u_0
+// (b = 1..3), U = the four corner velocities.  R = 4x3 element RHS.
+__device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3], const double c3[3],
+                                         double det, const double du1[3], const double du2[3],
+                                         const double du3[3], const double U0[3], const double U1[3],
+                                         const double U2[3], const double U3[3], const ElemConsts &k,
+                                         double R[4][3])
+{
+    const double ad = fabs(det);
+    const double sg = (det < 0.0) ? -1.0 : 1.0;
+    double Gh[3][3];
 #pragma unroll
     for (int kk = 0; kk < 3; ++kk)
 #pragma unroll
         for (int i = 0; i < 3; ++i)
-            Gh[kk][i] = fma(cf[1][kk], du[0][i], fma(cf[2][kk], du[1][i], cf[3][kk] * du[2][i]));
+            Gh[kk][i] = fma(c1[kk], du1[i], fma(c2[kk], du2[i], c3[kk] * du3[i]));
 
     // |Gh|^2 (three row partial sums) and the nine squared 2x2 minors
     // (rows m<n, columns i<j; three column-pair partial sums)
@@ -100,15 +121,32 @@ __device__ __forceinline__ void element_core(const double X[4][3], const double 
     }
     const double ssqh = sp[0] + sp[1] + sp[2];
     const double t = ssqh * aah;
-    double nut = 0.0;
-    if (aah * inv * inv > 1e-30 && t > 0.0)  // kernel.py:24 guard, in G units
-        nut = (k.cvre * r3) * (ssqh * rsqrt(t));
+    double r3, nut = 0.0;
+    if (ad > 1e-290 && ad < 1e290) {
+        r3 = rcbrt_fast(ad);
+    } else {
+        r3 = rcbrt(ad);
+    }
+    const double inv = (r3 * r3) * r3;  // 1/|D|
+    if (aah * inv * inv > 1e-30 && t > 0.0) {  // kernel.py:24 guard, in G units
+        const double rs = (t > 1e-300) ? rsqrt_fast(t) : rsqrt(t);
+        nut = (k.cvre * r3) * (ssqh * rs);
+    }
     const double vis = fma(k.rho, nut, k.mu);
-    B = vis * (inv * (-1.0 / 6.0));
-}
-
-__device__ __forceinline__ void rhs_rows(const double w[4][3], const double Gh[3][3], double R[4][3])
-{
+    const double B = vis * (inv * (-1.0 / 6.0));
+    const double As = sg * k.a_po, Aq = sg * k.a_q;
+    const double A4 = fma(4.0, As, Aq);
+    double w[4][3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+        const double S = (U0[cc] + U1[cc]) + (U2[cc] + U3[cc]);
+        const double AsS = As * S;
+        w[1][cc] = fma(Aq, U1[cc], fma(B, c1[cc], AsS));
+        w[2][cc] = fma(Aq, U2[cc], fma(B, c2[cc], AsS));
+        w[3][cc] = fma(Aq, U3[cc], fma(B, c3[cc], AsS));
+        // sum_a w_a = (4 As + Aq) S because the cofactor rows sum to zero
+        w[0][cc] = fma(A4, S, -((w[1][cc] + w[2][cc]) + w[3][cc]));
+    }
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -120,22 +158,76 @@ __device__ __forceinline__ void rhs_rows(const double w[4][3], const double Gh[3
 __device__ __forceinline__ void element_rhs_sym(const double X[4][3], const double U[4][3],
                                                 const ElemConsts &k, double R[4][3])
 {
-    double cf[4][3], Gh[3][3], sg, B;
-    element_core(X, U, k, cf, Gh, sg, B);
-    const double As = sg * k.a_po, Aq = sg * k.a_q;
-    const double A4 = fma(4.0, As, Aq);
-    double S[3], w[4][3];
+    double e[3][3], du[3][3], c1[3], c2[3], c3[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        S[c] = (U[0][c] + U[1][c]) + (U[2][c] + U[3][c]);
-        const double AsS = As * S[c];
+    for (int b = 0; b < 3; ++b)
 #pragma unroll
-        for (int a = 1; a < 4; ++a)
-            w[a][c] = fma(Aq, U[a][c], fma(B, cf[a][c], AsS));
-        // sum_a w_a = (4 As + Aq) S because the cofactor rows sum to zero
-        w[0][c] = fma(A4, S[c], -((w[1][c] + w[2][c]) + w[3][c]));
+        for (int c = 0; c < 3; ++c) {
+            e[b][c] = X[b + 1][c] - X[0][c];
+            du[b][c] = U[b + 1][c] - U[0][c];
+        }
+    cross3(e[1], e[2], c1);  // e2 x e3
+    cross3(e[2], e[0], c2);  // e3 x e1
+    cross3(e[0], e[1], c3);  // e1 x e2
+    const double det = fma(e[0][0], c1[0], fma(e[0][1], c1[1], e[0][2] * c1[2]));
+    tet_tail(c1, c2, c3, det, du[0], du[1], du[2], U[0], U[1], U[2], U[3], k, R);
+}
+
+// Geometry + gradient + Vreman for the general-pmat element: cofactor rows
+// cf[1..3], the unscaled gradient Gh, sgn(D) and B = -vis / (6 |D|).
+__device__ __forceinline__ void element_core(const double X[4][3], const double U[4][3],
+                                             const ElemConsts &k, double cf[4][3],
+                                             double Gh[3][3], double &sg, double &B)
+{
+    double e[3][3], du[3][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            e[b][c] = X[b + 1][c] - X[0][c];
+            du[b][c] = U[b + 1][c] - U[0][c];
+        }
+    cross3(e[1], e[2], cf[1]);
+    cross3(e[2], e[0], cf[2]);
+    cross3(e[0], e[1], cf[3]);
+    const double det = fma(e[0][0], cf[1][0], fma(e[0][1], cf[1][1], e[0][2] * cf[1][2]));
+    const double ad = fabs(det);
+    sg = (det < 0.0) ? -1.0 : 1.0;
+    const double r3 = rcbrt(ad);
+    const double inv = r3 * r3 * r3;
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            Gh[kk][i] = fma(cf[1][kk], du[0][i], fma(cf[2][kk], du[1][i], cf[3][kk] * du[2][i]));
+    double aah = 0.0, ssqh = 0.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q)
+        aah = fma(Gh[q / 3][q % 3], Gh[q / 3][q % 3], aah);
+#pragma unroll
+    for (int cp = 0; cp < 3; ++cp) {
+        const int ci = (cp == 2) ? 1 : 0, cj = (cp == 0) ? 1 : 2;
+#pragma unroll
+        for (int rp = 0; rp < 3; ++rp) {
+            const int m = (rp == 2) ? 1 : 0, n = (rp == 0) ? 1 : 2;
+            const double d = fma(Gh[m][ci], Gh[n][cj], -(Gh[m][cj] * Gh[n][ci]));
+            ssqh = fma(d, d, ssqh);
+        }
     }
-    rhs_rows(w, Gh, R);
+    double nut = 0.0;
+    if (aah * inv * inv > 1e-30 && ssqh > 0.0)
+        nut = k.cvre * r3 * sqrt(ssqh / aah);
+    const double vis = fma(k.rho, nut, k.mu);
+    B = vis * (inv * (-1.0 / 6.0));
+}
+
+__device__ __forceinline__ void rhs_rows(const double w[4][3], const double Gh[3][3], double R[4][3])
+{
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            R[a][i] = fma(w[a][0], Gh[0][i], fma(w[a][1], Gh[1][i], w[a][2] * Gh[2][i]));
 }
 
 // General pmat (any 4x4 interpolation table): m_a = sum_b pmat[a][b] u_b.

@@ -177,9 +177,13 @@ __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict
 //           order); a plain store if all of the node's tets are in this
 //           chunk, else one FP64 RED per component (ORDERED=false) or a
 //           partial for the ordered merge (ORDERED=true, bitwise reproducible).
-// Blob: int4 {n_patch, n_node, node_begin, n_contrib} | 64 B per patch:
-// u16 ids[16] = {m | closed<<8, a, b, r_0..r_{m-1}}, u16 pos[16] (same slots)
-// | u16 csr_off[n_node] (pad 16) | int32 nodes[n_node] (pad 16).
+// Blob: int4 {n_patch, n_node, node_begin, n_contrib}
+//     | u16 ids[16][T]  (patch p: {m | closed<<8, a, b, r_0..r_{m-1}}, lane-major)
+//     | u16 pos[16][T]  (contribution position of the same slots)
+//     | u16 lev[32]     (jagged level offsets, tal_prep.hpp)
+//     | int32 gather[n_node]  node ids in chunk-local order      (pad 16)
+//     | int32 cnode[n_node]   node id | bit31 interior, by rank   (pad 16)
+//     | u8 run[n_node]        contributions per node, by rank     (pad 16).
 // ---------------------------------------------------------------------------
 template <int CFG>
 struct PrivCfg;
@@ -187,14 +191,22 @@ template <>
 struct PrivCfg<0> {  // 64 patches / chunk
     static constexpr int THREADS = 64, NM = 144, NC = 544, MINB = 6;
 };
+#ifndef TAL_CFG1_MINB
+#define TAL_CFG1_MINB 3
+#endif
+#ifndef TAL_RING_UNROLL
+#define TAL_RING_UNROLL 3
+#endif
+constexpr int kRingUnroll = TAL_RING_UNROLL;
 template <>
 struct PrivCfg<1> {  // 128 patches / chunk
-    static constexpr int THREADS = 128, NM = 256, NC = 1088, MINB = 3;
+    static constexpr int THREADS = 128, NM = 256, NC = 1088, MINB = TAL_CFG1_MINB;
 };
 
+constexpr int BLOB_LEVELS = 32;
 template <int T, int NM, int NC>
 struct PrivLayout {
-    static constexpr int BLOB = 16 + 64 * T + pad16(2 * NM) + pad16(4 * NM);
+    static constexpr int BLOB = 16 + 64 * T + 2 * BLOB_LEVELS + 2 * pad16(4 * NM) + pad16(NM);
     static constexpr int BLOB_AL = (BLOB + 127) / 128 * 128;
     static constexpr int MBAR = 0;
     static constexpr int BLOBS = 128;
@@ -241,10 +253,10 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
     auto gather = [&](int b) {  // all threads: cp.async the chunk's node records
         const uint8_t *bl = blob(b);
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);
-        const int32_t *cn = reinterpret_cast<const int32_t *>(bl + 16 + 64 * hdr.x + pad16(2 * hdr.y));
+        const int32_t *gl = reinterpret_cast<const int32_t *>(bl + 16 + 64 * T + 2 * BLOB_LEVELS);
         double *dst = nrec(b);
         for (int j = tid; j < hdr.y; j += T) {
-            const double *src = nrec_g + 6 * (int64_t)(cn[j] & 0x7fffffff);
+            const double *src = nrec_g + 6 * (int64_t)gl[j];
             cp_async16(dst + 6 * j, src);
             cp_async16(dst + 6 * j + 2, src + 2);
             cp_async16(dst + 6 * j + 4, src + 4);
@@ -276,33 +288,60 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
         }
         const uint8_t *bl = blob(b);
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);  // n_patch, n_node, node_begin, n_contrib
-        const uint16_t *coff = reinterpret_cast<const uint16_t *>(bl + 16 + 64 * hdr.x);
-        const int32_t *cn = reinterpret_cast<const int32_t *>(bl + 16 + 64 * hdr.x + pad16(2 * hdr.y));
+        const uint16_t *lev = reinterpret_cast<const uint16_t *>(bl + 16 + 64 * T);
+        const uint8_t *tail = bl + 16 + 64 * T + 2 * BLOB_LEVELS + pad16(4 * hdr.y);
+        const int32_t *cn = reinterpret_cast<const int32_t *>(tail);
+        const uint8_t *run = tail + pad16(4 * hdr.y);
         const double *nr = nrec(b);
 
-        // phase B: one patch per thread
+        // phase B: one patch per thread (lane-major tables: slot s at [s*T + tid])
         if (tid < hdr.x) {
-            const uint16_t *ids = reinterpret_cast<const uint16_t *>(bl + 16 + 64 * tid);
-            const uint16_t *pos = ids + 16;
-            const int m = ids[0] & 0xff;
-            const bool closed = (ids[0] >> 8) != 0;
+            const uint16_t *ids = reinterpret_cast<const uint16_t *>(bl + 16) + tid;
+            const uint16_t *pos = ids + 16 * T;
+#define ID(s) ids[(s) * T]
+#define POS(s) pos[(s) * T]
+            const int m = ID(0) & 0xff;
+            const bool closed = (ID(0) >> 8) != 0;
             const int k = closed ? m : m - 1;
-            double X[4][3], U[4][3], R[4][3];
-            load_record_s(nr, ids[1], X[0], U[0]);
-            load_record_s(nr, ids[2], X[1], U[1]);
-            load_record_s(nr, ids[3], X[2], U[2]);
+            // ring recurrences for tet t = (a, b, r_t, r_t+1):
+            //   e1 = x_b - x_a, du1 = u_b - u_a (patch constants),
+            //   e2(t) = e3(t-1), du2(t) = du3(t-1), c3(t) = e1 x e2(t) = -c2(t-1)
+            double Xa[3], Ua[3], Ub[3], e1[3], du1[3], e2[3], du2[3], U2[3], c3[3];
+            {
+                double Xb[3], Xr[3];
+                load_record_s(nr, ID(1), Xa, Ua);
+                load_record_s(nr, ID(2), Xb, Ub);
+                load_record_s(nr, ID(3), Xr, U2);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    e1[q] = Xb[q] - Xa[q];
+                    du1[q] = Ub[q] - Ua[q];
+                    e2[q] = Xr[q] - Xa[q];
+                    du2[q] = U2[q] - Ua[q];
+                }
+                cross3(e1, e2, c3);
+            }
             double acc_a[3] = {0.0, 0.0, 0.0}, acc_b[3] = {0.0, 0.0, 0.0}, carry[3];
-#pragma unroll 1
+#pragma unroll kRingUnroll
             for (int t = 0; t < k; ++t) {
                 const int nxt = (t + 1 == m) ? 0 : t + 1;
-                load_record_s(nr, ids[3 + nxt], X[3], U[3]);
-                element_rhs<true>(X, U, kc, R);
+                double X3[3], U3[3], e3[3], du3[3], c1[3], c2[3], R[4][3];
+                load_record_s(nr, ID(3 + nxt), X3, U3);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    acc_a[c] += R[0][c];
-                    acc_b[c] += R[1][c];
+                for (int q = 0; q < 3; ++q) {
+                    e3[q] = X3[q] - Xa[q];
+                    du3[q] = U3[q] - Ua[q];
                 }
-                const int p = pos[3 + t];
+                cross3(e2, e3, c1);
+                cross3(e3, e1, c2);
+                const double det = fma(e1[0], c1[0], fma(e1[1], c1[1], e1[2] * c1[2]));
+                tet_tail(c1, c2, c3, det, du1, du2, du3, Ua, Ub, U2, U3, kc, R);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    acc_a[q] += R[0][q];
+                    acc_b[q] += R[1][q];
+                }
+                const int p = POS(3 + t);
                 if (t == 0) {
                     resx[p] = R[2][0];
                     resy[p] = R[2][1];
@@ -313,14 +352,16 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
                     resz[p] = carry[2] + R[2][2];
                 }
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    carry[c] = R[3][c];
-                    X[2][c] = X[3][c];
-                    U[2][c] = U[3][c];
+                for (int q = 0; q < 3; ++q) {
+                    carry[q] = R[3][q];
+                    e2[q] = e3[q];
+                    du2[q] = du3[q];
+                    U2[q] = U3[q];
+                    c3[q] = -c2[q];
                 }
             }
             // the ring node after the last tet: r_0 again (closed) or r_{m-1}
-            const int pl = pos[3 + (closed ? 0 : m - 1)];
+            const int pl = POS(3 + (closed ? 0 : m - 1));
             if (closed) {
                 resx[pl] += carry[0];
                 resy[pl] += carry[1];
@@ -330,35 +371,39 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
                 resy[pl] = carry[1];
                 resz[pl] = carry[2];
             }
-            resx[pos[1]] = acc_a[0];
-            resy[pos[1]] = acc_a[1];
-            resz[pos[1]] = acc_a[2];
-            resx[pos[2]] = acc_b[0];
-            resy[pos[2]] = acc_b[1];
-            resz[pos[2]] = acc_b[2];
+            resx[POS(1)] = acc_a[0];
+            resy[POS(1)] = acc_a[1];
+            resz[POS(1)] = acc_a[2];
+            resx[POS(2)] = acc_b[0];
+            resy[POS(2)] = acc_b[1];
+            resz[POS(2)] = acc_b[2];
+#undef ID
+#undef POS
         }
         __syncthreads();
 
-        // phase C: per-node sums over contiguous runs (patch order), scatter
-        for (int j = tid; j < hdr.y; j += T) {
-            const int beg = coff[j];
-            const int end = (j + 1 < hdr.y) ? (int)coff[j + 1] : hdr.w;
+        // phase C: one node per thread, nodes in rank order (contribution count
+        // descending); its s-th contribution sits at lev[s] + q, so a warp
+        // reads lane-contiguous addresses at every level
+        for (int q = tid; q < hdr.y; q += T) {
+            const int nr_ = run[q];
             double ax = 0.0, ay = 0.0, az = 0.0;
-            for (int s = beg; s < end; ++s) {
-                ax += resx[s];
-                ay += resy[s];
-                az += resz[s];
+            for (int s = 0; s < nr_; ++s) {
+                const int p = lev[s] + q;
+                ax += resx[p];
+                ay += resy[p];
+                az += resz[p];
             }
-            const int raw = cn[j];
+            const int raw = cn[q];
             const int v = raw & 0x7fffffff;
             if (raw < 0) {  // interior: the complete sum
                 rhs.rx[v] = ax;
                 rhs.ry[v] = ay;
                 rhs.rz[v] = az;
             } else if (ORDERED) {
-                pa.px[hdr.z + j] = ax;
-                pa.py[hdr.z + j] = ay;
-                pa.pz[hdr.z + j] = az;
+                pa.px[hdr.z + q] = ax;
+                pa.py[hdr.z + q] = ay;
+                pa.pz[hdr.z + q] = az;
             } else {
                 atomicAdd(rhs.rx + v, ax);
                 atomicAdd(rhs.ry + v, ay);

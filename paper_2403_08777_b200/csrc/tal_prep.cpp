@@ -454,42 +454,60 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
     out.max_nodes = max_nodes;
     out.max_contrib = max_contrib;
     const int64_t np = P.n_patches();
-    out.precs.assign((size_t)np * 32, 0);
-    std::vector<int32_t> stamp((size_t)n_nodes, -1), local((size_t)n_nodes, 0);
+    out.pids.assign((size_t)np * 16, 0);
+    out.ppos.assign((size_t)np * 16, 0);
+    std::vector<int32_t> stamp((size_t)n_nodes, -1), local((size_t)n_nodes, 0), cnt((size_t)n_nodes, 0);
     std::vector<int32_t> cnt_chunks((size_t)n_nodes, 0);
-    std::vector<int32_t> nodes, counts, fill;
+    std::vector<int32_t> nodes, order, rank, fill;
     int32_t chunk = 0;
     int64_t p_begin = 0, contrib = 0;
 
     auto close_chunk = [&](int64_t p_end) {
         std::vector<int32_t> sorted(nodes);
-        std::sort(sorted.begin(), sorted.end());
-        for (size_t j = 0; j < sorted.size(); ++j)
-            local[sorted[j]] = (int32_t)j;
+        std::sort(sorted.begin(), sorted.end());  // local ids: ascending node id (gather order)
         const int32_t nn = (int32_t)sorted.size();
-        counts.assign((size_t)nn + 1, 0);
-        for (int64_t g = p_begin; g < p_end; ++g)
-            for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k)
-                counts[local[P.nodes[k]] + 1]++;
         for (int32_t j = 0; j < nn; ++j)
-            counts[j + 1] += counts[j];
-        const size_t node_begin = out.chunk_nodes.size();
-        for (int32_t j = 0; j < nn; ++j) {
-            out.chunk_nodes.push_back(sorted[j]);
-            out.csr_off.push_back((uint16_t)counts[j]);
-            cnt_chunks[sorted[j]]++;
+            local[sorted[j]] = j;
+        // rank: by contribution count descending, then local id
+        order.resize(nn);
+        for (int32_t j = 0; j < nn; ++j)
+            order[j] = j;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t x, int32_t y) { return cnt[sorted[x]] > cnt[sorted[y]]; });
+        rank.assign(nn, 0);
+        for (int32_t q = 0; q < nn; ++q)
+            rank[order[q]] = q;
+        uint16_t lev[CHUNK_LEVELS] = {0};
+        for (int s = 1; s < CHUNK_LEVELS; ++s) {
+            int32_t alive = 0;  // nodes with more than s-1 contributions
+            for (int32_t q = 0; q < nn; ++q)
+                alive += cnt[sorted[order[q]]] > s - 1;
+            lev[s] = (uint16_t)(lev[s - 1] + alive);
         }
-        fill.assign(counts.begin(), counts.end() - 1);
-        for (int64_t g = p_begin; g < p_end; ++g) {  // patch order within each node
-            uint16_t *rec = out.precs.data() + 32 * g;
+        const size_t node_begin = out.cnodes.size();
+        for (int32_t j = 0; j < nn; ++j)
+            out.gather_nodes.push_back(sorted[j]);
+        for (int32_t q = 0; q < nn; ++q) {
+            const int32_t v = sorted[order[q]];
+            out.cnodes.push_back(v);
+            out.runs.push_back((uint8_t)cnt[v]);
+            cnt_chunks[v]++;
+        }
+        for (int s = 0; s < CHUNK_LEVELS; ++s)
+            out.levels.push_back(lev[s]);
+        fill.assign(nn, 0);  // contributions placed so far per local node (patch order)
+        for (int64_t g = p_begin; g < p_end; ++g) {
+            uint16_t *ids = out.pids.data() + 16 * g, *pos = out.ppos.data() + 16 * g;
             const int32_t m = P.off[g + 1] - P.off[g] - 2;
-            rec[0] = (uint16_t)(m | (P.closed[g] << 8));
+            ids[0] = (uint16_t)(m | (P.closed[g] << 8));
             for (int32_t k = 0; k < m + 2; ++k) {
                 const int32_t l = local[P.nodes[P.off[g] + k]];
-                rec[1 + k] = (uint16_t)l;
-                rec[16 + 1 + k] = (uint16_t)fill[l]++;
+                ids[1 + k] = (uint16_t)l;
+                pos[1 + k] = (uint16_t)(lev[fill[l]++] + rank[l]);
             }
         }
+        for (int32_t v : sorted)
+            cnt[v] = 0;
         out.chunks.push_back((int32_t)p_begin);
         out.chunks.push_back((int32_t)(p_end - p_begin));
         out.chunks.push_back((int32_t)node_begin);
@@ -508,11 +526,16 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
             return false;
         }
         int fresh = 0;
-        for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k)
-            if (stamp[P.nodes[k]] != chunk)
+        bool full_level = false;
+        for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
+            const int32_t v = P.nodes[k];
+            if (stamp[v] != chunk)
                 ++fresh;
+            else if (cnt[v] + 1 > CHUNK_LEVELS)
+                full_level = true;
+        }
         if (g > p_begin && ((g - p_begin) + 1 > max_patches || (int64_t)nodes.size() + fresh > max_nodes ||
-                            contrib + n > max_contrib))
+                            contrib + n > max_contrib || full_level))
             close_chunk(g);
         for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
             const int32_t v = P.nodes[k];
@@ -520,6 +543,7 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
                 stamp[v] = chunk;
                 nodes.push_back(v);
             }
+            cnt[v]++;
         }
         contrib += n;
     }
@@ -527,11 +551,11 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
         close_chunk(np);
 
     // interior flag + shared/isolated node lists for the ordered merge
-    const int64_t total = (int64_t)out.chunk_nodes.size();
+    const int64_t total = (int64_t)out.cnodes.size();
     for (int64_t q = 0; q < total; ++q) {
-        const int32_t v = out.chunk_nodes[q];
+        const int32_t v = out.cnodes[q];
         if (cnt_chunks[v] == 1)
-            out.chunk_nodes[q] = (int32_t)((uint32_t)v | 0x80000000u);
+            out.cnodes[q] = (int32_t)((uint32_t)v | 0x80000000u);
     }
     for (int64_t v = 0; v < n_nodes; ++v)
         if (cnt_chunks[v] != 1) {
@@ -548,7 +572,7 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
     out.bnd_pos.resize((size_t)out.bnd_off.back());
     std::vector<int32_t> bfill(out.bnd_off.begin(), out.bnd_off.end() - 1);
     for (int64_t q = 0; q < total; ++q) {
-        const uint32_t raw = (uint32_t)out.chunk_nodes[q];
+        const uint32_t raw = (uint32_t)out.cnodes[q];
         if (raw & 0x80000000u)
             continue;
         out.bnd_pos[bfill[bidx[raw]]++] = (int32_t)q;
@@ -556,15 +580,15 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
     return true;
 }
 
-void pack_blobs(const Chunking &ch, std::vector<uint8_t> &blobs, std::vector<int32_t> &blob_off)
+void pack_blobs(const Chunking &ch, int T, std::vector<uint8_t> &blobs, std::vector<int32_t> &blob_off)
 {
     const int64_t n_chunks = (int64_t)ch.chunks.size() / 5;
     auto pad = [](int64_t b) { return (b + 15) / 16 * 16; };
+    auto blob_bytes = [&](int64_t nn) { return 16 + 64 * (int64_t)T + 2 * CHUNK_LEVELS + 2 * pad(4 * nn) + pad(nn); };
     blob_off.assign((size_t)n_chunks + 1, 0);
     int64_t total = 0;
     for (int64_t c = 0; c < n_chunks; ++c) {
-        const int64_t npch = ch.chunks[5 * c + 1], nn = ch.chunks[5 * c + 3];
-        total += 16 + 64 * npch + pad(2 * nn) + pad(4 * nn);
+        total += blob_bytes(ch.chunks[5 * c + 3]);
         blob_off[c + 1] = (int32_t)(total / 16);
     }
     blobs.assign((size_t)total, 0);
@@ -574,9 +598,21 @@ void pack_blobs(const Chunking &ch, std::vector<uint8_t> &blobs, std::vector<int
         uint8_t *b = blobs.data() + (int64_t)blob_off[c] * 16;
         const int32_t hdr[4] = {npch, nn, n0, ch.chunks[5 * c + 4]};
         std::memcpy(b, hdr, 16);
-        std::memcpy(b + 16, ch.precs.data() + 32 * (int64_t)p0, 64 * (size_t)npch);
-        std::memcpy(b + 16 + 64 * npch, ch.csr_off.data() + n0, 2 * (size_t)nn);
-        std::memcpy(b + 16 + 64 * npch + pad(2 * nn), ch.chunk_nodes.data() + n0, 4 * (size_t)nn);
+        uint16_t *ids = reinterpret_cast<uint16_t *>(b + 16);
+        uint16_t *pos = ids + 16 * T;
+        for (int32_t g = 0; g < npch; ++g)
+            for (int s = 0; s < 16; ++s) {
+                ids[s * T + g] = ch.pids[16 * (int64_t)(p0 + g) + s];
+                pos[s * T + g] = ch.ppos[16 * (int64_t)(p0 + g) + s];
+            }
+        uint8_t *q = b + 16 + 64 * T;
+        std::memcpy(q, ch.levels.data() + CHUNK_LEVELS * c, 2 * CHUNK_LEVELS);
+        q += 2 * CHUNK_LEVELS;
+        std::memcpy(q, ch.gather_nodes.data() + n0, 4 * (size_t)nn);
+        q += pad(4 * nn);
+        std::memcpy(q, ch.cnodes.data() + n0, 4 * (size_t)nn);
+        q += pad(4 * nn);
+        std::memcpy(q, ch.runs.data() + n0, (size_t)nn);
     }
 }
 

@@ -46,22 +46,31 @@ struct Patches {
 // most compact tet-index span), tets visited in the given order.
 void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int mode, Patches &out);
 
-// CTA chunking of the patch sequence for the private scatter.
+// CTA chunking of the patch sequence for the private scatter.  Each node's
+// contributions inside a chunk (one per patch that touches it) are laid out
+// "jagged diagonal": nodes ranked by contribution count (descending), level s
+// holds the s-th contribution of every node with more than s of them, so the
+// node-per-thread reduction reads lane-contiguous addresses.
+constexpr int CHUNK_LEVELS = 32;  // max patches per node within one chunk
 struct Chunking {
     int max_patches = 0, max_nodes = 0, max_contrib = 0;
-    std::vector<int32_t> chunks;       // 5 per chunk: patch_begin, n_patch, node_begin, n_node, n_contrib
-    std::vector<int32_t> chunk_nodes;  // node id | (1u<<31 if the node is interior to the chunk)
-    std::vector<uint16_t> csr_off;     // per chunk node: first contribution index
-    std::vector<uint16_t> precs;       // 32 per patch: ids[16] (m|closed<<8, a, b, r..), pos[16]
+    // 5 per chunk: patch_begin, n_patch, node_begin, n_node, n_contrib
+    std::vector<int32_t> chunks;
+    std::vector<int32_t> gather_nodes;  // per chunk node, local-id order: node id
+    std::vector<int32_t> cnodes;        // per chunk node, rank order: node id | bit31 interior
+    std::vector<uint8_t> runs;          // per chunk node, rank order: contribution count
+    std::vector<uint16_t> levels;       // CHUNK_LEVELS per chunk: jagged level offsets
+    std::vector<uint16_t> pids, ppos;   // 16 per patch: ids {m|closed<<8, a, b, r..}, positions
     // deterministic merge: for nodes in >1 chunk (and isolated nodes), the
-    // chunk-node positions holding their partial sums, in chunk order
+    // chunk-node entries (node_begin + rank) holding their partial sums, in chunk order
     std::vector<int32_t> bnd_nodes, bnd_off, bnd_pos;
     int64_t n_shared = 0;
 };
 bool build_chunks(const Patches &p, int64_t n_nodes, int max_patches, int max_nodes, int max_contrib,
                   Chunking &out, std::string &err);
-// One contiguous 16-B aligned record per chunk (layout: tal_kernels.cuh);
-// blob_off[c] in 16-byte units, n_chunks+1 entries.
-void pack_blobs(const Chunking &ch, std::vector<uint8_t> &blobs, std::vector<int32_t> &blob_off);
+// One contiguous 16-B aligned record per chunk (layout: tal_kernels.cuh,
+// patch tables transposed with stride 'cta_threads'); blob_off in 16-B units.
+void pack_blobs(const Chunking &ch, int cta_threads, std::vector<uint8_t> &blobs,
+                std::vector<int32_t> &blob_off);
 
 }  // namespace tal
