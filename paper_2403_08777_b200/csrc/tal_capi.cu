@@ -134,6 +134,7 @@ bool make_consts(const tal_params *p, ElemConsts &kc, bool &sym)
     kc.rho = p->rho;
     kc.mu = p->mu;
     kc.cvre = p->c_vreman;
+    kc.rc = p->rho * p->c_vreman;
     for (int i = 0; i < 16; ++i)
         kc.pm[i] = p->pmat[i];
     double pd = 0.0, po = 0.0;

@@ -36,6 +36,7 @@ namespace tal {
 
 struct ElemConsts {
     double rho, mu, cvre;
+    double rc;    // rho * c_vreman
     double a_po;  // -rho * po / 24
     double a_q;   // -rho * (pd - po) / 24
     double pm[16];  // full pmat (general kernel only)
@@ -82,17 +83,33 @@ __device__ __forceinline__ double rsqrt_fast(double t)
     return fma(y * e, p, y);
 }
 
+// normal (not zero/subnormal/inf/nan) test on the exponent field: INT pipe only
+__device__ __forceinline__ bool is_normal_pos(double x)
+{
+    const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+    return e - 1u < 2046u;
+}
+
+// x with the sign of s flipped into it (x * sgn(s) for s != 0), integer ops only
+__device__ __forceinline__ double mul_sign(double x, double s)
+{
+    return __longlong_as_double(__double_as_longlong(x) ^
+                                (__double_as_longlong(s) & (long long)0x8000000000000000ULL));
+}
+
 // Everything after the cofactor rows: velocity gradient, Vreman, the two
 // weighted terms.  c[1..3] = cofactor rows, D = det, du[b] = u_b - u_0
-// (b = 1..3), U = the four corner velocities.  R = 4x3 element RHS.
+// (b = 1..3), U = the four corner velocities.  R = 4x3 element RHS; with
+// ACC the FMA chains of R start from R's incoming values (the ring kernel
+// folds its running sums into them instead of separate adds).
+template <bool ACC>
 __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3], const double c3[3],
                                          double det, const double du1[3], const double du2[3],
                                          const double du3[3], const double U0[3], const double U1[3],
-                                         const double U2[3], const double U3[3], const ElemConsts &k,
-                                         double R[4][3])
+                                         const double S01[3], const double U2[3], const double U3[3],
+                                         const ElemConsts &k, double R[4][3])
 {
     const double ad = fabs(det);
-    const double sg = (det < 0.0) ? -1.0 : 1.0;
     double Gh[3][3];
 #pragma unroll
     for (int kk = 0; kk < 3; ++kk)
@@ -121,25 +138,19 @@ __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3],
     }
     const double ssqh = sp[0] + sp[1] + sp[2];
     const double t = ssqh * aah;
-    double r3, nut = 0.0;
-    if (ad > 1e-290 && ad < 1e290) {
-        r3 = rcbrt_fast(ad);
-    } else {
-        r3 = rcbrt(ad);
-    }
+    const double r3 = is_normal_pos(ad) ? rcbrt_fast(ad) : rcbrt(ad);
     const double inv = (r3 * r3) * r3;  // 1/|D|
-    if (aah * inv * inv > 1e-30 && t > 0.0) {  // kernel.py:24 guard, in G units
-        const double rs = (t > 1e-300) ? rsqrt_fast(t) : rsqrt(t);
-        nut = (k.cvre * r3) * (ssqh * rs);
-    }
-    const double vis = fma(k.rho, nut, k.mu);
+    double f = 0.0;                     // rho * nu_t / ssqh
+    if (aah * inv * inv > 1e-30 && t > 0.0)  // kernel.py:24 guard, in G units
+        f = (k.rc * r3) * (is_normal_pos(t) ? rsqrt_fast(t) : rsqrt(t));
+    const double vis = fma(f, ssqh, k.mu);  // mu + rho nu_t
     const double B = vis * (inv * (-1.0 / 6.0));
-    const double As = sg * k.a_po, Aq = sg * k.a_q;
+    const double As = mul_sign(k.a_po, det), Aq = mul_sign(k.a_q, det);
     const double A4 = fma(4.0, As, Aq);
     double w[4][3];
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
-        const double S = (U0[cc] + U1[cc]) + (U2[cc] + U3[cc]);
+        const double S = S01[cc] + (U2[cc] + U3[cc]);  // S01 = u_0 + u_1
         const double AsS = As * S;
         w[1][cc] = fma(Aq, U1[cc], fma(B, c1[cc], AsS));
         w[2][cc] = fma(Aq, U2[cc], fma(B, c2[cc], AsS));
@@ -150,8 +161,10 @@ __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3],
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int i = 0; i < 3; ++i)
-            R[a][i] = fma(w[a][0], Gh[0][i], fma(w[a][1], Gh[1][i], w[a][2] * Gh[2][i]));
+        for (int i = 0; i < 3; ++i) {
+            const double last = ACC ? fma(w[a][2], Gh[2][i], R[a][i]) : w[a][2] * Gh[2][i];
+            R[a][i] = fma(w[a][0], Gh[0][i], fma(w[a][1], Gh[1][i], last));
+        }
 }
 
 // Symmetric-rule element (pmat = po * ones + (pd - po) * I).
@@ -170,7 +183,8 @@ __device__ __forceinline__ void element_rhs_sym(const double X[4][3], const doub
     cross3(e[2], e[0], c2);  // e3 x e1
     cross3(e[0], e[1], c3);  // e1 x e2
     const double det = fma(e[0][0], c1[0], fma(e[0][1], c1[1], e[0][2] * c1[2]));
-    tet_tail(c1, c2, c3, det, du[0], du[1], du[2], U[0], U[1], U[2], U[3], k, R);
+    const double S01[3] = {U[0][0] + U[1][0], U[0][1] + U[1][1], U[0][2] + U[1][2]};
+    tet_tail<false>(c1, c2, c3, det, du[0], du[1], du[2], U[0], U[1], S01, U[2], U[3], k, R);
 }
 
 // Geometry + gradient + Vreman for the general-pmat element: cofactor rows

@@ -166,10 +166,11 @@ __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict
 // 128 B/clk L1/shared data path before the FP64 pipe).
 //
 // Each persistent CTA walks chunks c = blockIdx.x + i*gridDim.x.  Per chunk:
-//   stage : one TMA bulk copy brings the chunk blob (patch records, node list,
-//           node-major contribution CSR) into shared memory (mbarrier
-//           completion); cp.async then gathers the chunk's node records.  Both
-//           run one chunk AHEAD, overlapping the FP64 work of the current one.
+//   stage : one TMA bulk copy brings the chunk blob (patch tables, node lists,
+//           contribution layout) into shared memory (mbarrier completion), two
+//           chunks ahead; cp.async gathers the chunk's node records one chunk
+//           ahead (issued after phase B of the previous chunk, so the blob it
+//           reads has had a whole phase B to arrive).
 //   B     : thread t walks patch t's ring, computing each tet's 4x3 RHS in
 //           registers; each patch node's sum is stored once, at its position
 //           in the chunk's node-major contribution list;
@@ -282,10 +283,6 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
         const int b = i & 1;
         cp_async_wait_all();
         __syncthreads();  // node records of chunk i visible to all
-        if (i + 1 < n_my) {
-            mbar_wait(&bar[b ^ 1], ((i + 1) >> 1) & 1);
-            gather(b ^ 1);  // in flight during phase B below
-        }
         const uint8_t *bl = blob(b);
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);  // n_patch, n_node, node_begin, n_contrib
         const uint16_t *lev = reinterpret_cast<const uint16_t *>(bl + 16 + 64 * T);
@@ -306,7 +303,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
             // ring recurrences for tet t = (a, b, r_t, r_t+1):
             //   e1 = x_b - x_a, du1 = u_b - u_a (patch constants),
             //   e2(t) = e3(t-1), du2(t) = du3(t-1), c3(t) = e1 x e2(t) = -c2(t-1)
-            double Xa[3], Ua[3], Ub[3], e1[3], du1[3], e2[3], du2[3], U2[3], c3[3];
+            double Xa[3], Ua[3], Ub[3], S01[3], e1[3], du1[3], e2[3], du2[3], U2[3], c3[3];
             {
                 double Xb[3], Xr[3];
                 load_record_s(nr, ID(1), Xa, Ua);
@@ -316,16 +313,20 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
                 for (int q = 0; q < 3; ++q) {
                     e1[q] = Xb[q] - Xa[q];
                     du1[q] = Ub[q] - Ua[q];
+                    S01[q] = Ua[q] + Ub[q];
                     e2[q] = Xr[q] - Xa[q];
                     du2[q] = U2[q] - Ua[q];
                 }
                 cross3(e1, e2, c3);
             }
-            double acc_a[3] = {0.0, 0.0, 0.0}, acc_b[3] = {0.0, 0.0, 0.0}, carry[3];
+            // R[0], R[1] carry the running sums of a and b, R[2] enters with the
+            // previous tet's contribution to r_t and leaves complete for r_t,
+            // R[3] (r_t+1) becomes the next tet's carry
+            double R[4][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
 #pragma unroll kRingUnroll
             for (int t = 0; t < k; ++t) {
                 const int nxt = (t + 1 == m) ? 0 : t + 1;
-                double X3[3], U3[3], e3[3], du3[3], c1[3], c2[3], R[4][3];
+                double X3[3], U3[3], e3[3], du3[3], c1[3], c2[3];
                 load_record_s(nr, ID(3 + nxt), X3, U3);
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
@@ -335,31 +336,22 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
                 cross3(e2, e3, c1);
                 cross3(e3, e1, c2);
                 const double det = fma(e1[0], c1[0], fma(e1[1], c1[1], e1[2] * c1[2]));
-                tet_tail(c1, c2, c3, det, du1, du2, du3, Ua, Ub, U2, U3, kc, R);
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    acc_a[q] += R[0][q];
-                    acc_b[q] += R[1][q];
-                }
+                tet_tail<true>(c1, c2, c3, det, du1, du2, du3, Ua, Ub, S01, U2, U3, kc, R);
                 const int p = POS(3 + t);
-                if (t == 0) {
-                    resx[p] = R[2][0];
-                    resy[p] = R[2][1];
-                    resz[p] = R[2][2];
-                } else {
-                    resx[p] = carry[0] + R[2][0];
-                    resy[p] = carry[1] + R[2][1];
-                    resz[p] = carry[2] + R[2][2];
-                }
+                resx[p] = R[2][0];
+                resy[p] = R[2][1];
+                resz[p] = R[2][2];
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
-                    carry[q] = R[3][q];
+                    R[2][q] = R[3][q];
+                    R[3][q] = 0.0;
                     e2[q] = e3[q];
                     du2[q] = du3[q];
                     U2[q] = U3[q];
                     c3[q] = -c2[q];
                 }
             }
+            double *carry = R[2], *acc_a = R[0], *acc_b = R[1];
             // the ring node after the last tet: r_0 again (closed) or r_{m-1}
             const int pl = POS(3 + (closed ? 0 : m - 1));
             if (closed) {
@@ -381,6 +373,12 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
 #undef POS
         }
         __syncthreads();
+        // records of chunk i+1 into the other buffer (free since chunk i-1's
+        // phase B): its blob has had all of phase B(i) to land
+        if (i + 1 < n_my) {
+            mbar_wait(&bar[b ^ 1], ((i + 1) >> 1) & 1);
+            gather(b ^ 1);
+        }
 
         // phase C: one node per thread, nodes in rank order (contribution count
         // descending); its s-th contribution sits at lev[s] + q, so a warp
