@@ -30,10 +30,11 @@ for r in rows[2:]:
             stalls[m.group(1)] = round(f(k), 3)
     s = {
         "kernel": name,
-        "duration_us": (f("gpu__time_duration.sum") or 0) / 1e3,
-        "sm_mhz": (f("smsp__cycles_elapsed.avg.per_second") or 0) / 1e6,
-        "dram_read_bytes": f("dram__bytes_read.sum"),
-        "dram_write_bytes": f("dram__bytes_write.sum"),
+        "duration": [f("gpu__time_duration.sum"), units[hdr.index("gpu__time_duration.sum")]],
+        "sm_clock": [f("smsp__cycles_elapsed.avg.per_second"),
+                     units[hdr.index("smsp__cycles_elapsed.avg.per_second")]],
+        "dram_read_mbytes": f("dram__bytes_read.sum"),
+        "dram_write_mbytes": f("dram__bytes_write.sum"),
         "fp64_pipe_pct": f("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
         "issue_active_pct": f("sm__inst_issued.avg.pct_of_peak_sustained_active"),
         "warps_active_per_sm": f("sm__warps_active.avg.per_cycle_active"),
