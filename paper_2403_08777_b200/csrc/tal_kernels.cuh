@@ -193,10 +193,10 @@ struct PrivCfg<0> {  // 64 patches / chunk
     static constexpr int THREADS = 64, NM = 144, NC = 544, MINB = 6;
 };
 #ifndef TAL_CFG1_MINB
-#define TAL_CFG1_MINB 3
+#define TAL_CFG1_MINB 4
 #endif
 #ifndef TAL_RING_UNROLL
-#define TAL_RING_UNROLL 3
+#define TAL_RING_UNROLL 1
 #endif
 constexpr int kRingUnroll = TAL_RING_UNROLL;
 template <>
@@ -204,15 +204,17 @@ struct PrivCfg<1> {  // 128 patches / chunk
     static constexpr int THREADS = 128, NM = 256, NC = 1088, MINB = TAL_CFG1_MINB;
 };
 
-constexpr int BLOB_LEVELS = 32;
+constexpr int BLOB_LEVELS = 32;  // = CHUNK_LEVELS (tal_prep.hpp)
+constexpr int SLOTS = 12;        // = PATCH_SLOTS (tal_prep.hpp)
 template <int T, int NM, int NC>
 struct PrivLayout {
-    static constexpr int BLOB = 16 + 64 * T + 2 * BLOB_LEVELS + 2 * pad16(4 * NM) + pad16(NM);
+    static constexpr int TABLES = 4 * SLOTS * T;  // u16 ids[SLOTS][T], pos[SLOTS][T]
+    static constexpr int BLOB = 16 + TABLES + 2 * BLOB_LEVELS + 2 * pad16(4 * NM) + pad16(NM);
     static constexpr int BLOB_AL = (BLOB + 127) / 128 * 128;
     static constexpr int MBAR = 0;
     static constexpr int BLOBS = 128;
-    static constexpr int NREC = BLOBS + 2 * BLOB_AL;
-    static constexpr int RES = NREC + 2 * NM * 48;
+    static constexpr int NREC = BLOBS + 2 * BLOB_AL;  // one buffer: gathered after phase B
+    static constexpr int RES = NREC + NM * 48;
     static constexpr int TOTAL = RES + 3 * NC * 8;
 };
 template <int CFG>
@@ -223,7 +225,21 @@ struct PrivArgs {
     const int32_t *__restrict__ blob_off;  // 16-B units, n_chunks+1
     int n_chunks;
     double *px, *py, *pz;  // ordered-merge partials, indexed node_begin + j
+    // in-kernel zeroing of rx|ry|rz before the first FP64 RED (private-atomic;
+    // cooperative launch: every CTA is resident, so the arrival counter is a
+    // safe grid barrier).  zero_n == 0 disables it.
+    double *zero_base;
+    int64_t zero_n;              // doubles to zero (3 * n_nodes)
+    unsigned long long *arrive;  // monotone arrival counter
+    unsigned long long target;   // value meaning "every CTA of this launch zeroed"
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 template <int CFG, bool ORDERED>
 __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
@@ -242,7 +258,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
     if (n_my == 0)
         return;
     auto blob = [&](int b) { return sm + L::BLOBS + b * L::BLOB_AL; };
-    auto nrec = [&](int b) { return reinterpret_cast<double *>(sm + L::NREC + b * NM * 48); };
+    double *const nrec_s = reinterpret_cast<double *>(sm + L::NREC);
 
     auto issue = [&](int i, int b) {  // one thread: bulk-copy chunk i's blob into buffer b
         const int c = first + i * stride;
@@ -254,8 +270,8 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
     auto gather = [&](int b) {  // all threads: cp.async the chunk's node records
         const uint8_t *bl = blob(b);
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);
-        const int32_t *gl = reinterpret_cast<const int32_t *>(bl + 16 + 64 * T + 2 * BLOB_LEVELS);
-        double *dst = nrec(b);
+        const int32_t *gl = reinterpret_cast<const int32_t *>(bl + 16 + L::TABLES + 2 * BLOB_LEVELS);
+        double *dst = nrec_s;
         for (int j = tid; j < hdr.y; j += T) {
             const double *src = nrec_g + 6 * (int64_t)gl[j];
             cp_async16(dst + 6 * j, src);
@@ -278,6 +294,26 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
     }
     mbar_wait(&bar[0], 0);
     gather(0);
+#ifndef TAL_ZERO_MODE
+#define TAL_ZERO_MODE 0
+#endif
+    auto zero_slice = [&]() {  // zero this CTA's slice of the RHS, then arrive
+        const int64_t n2 = pa.zero_n / 2;  // double2 stores (3 * n_nodes doubles, 16-B aligned base)
+        const int64_t per = (n2 + gridDim.x - 1) / gridDim.x;
+        const int64_t lo = per * blockIdx.x, hi = min(n2, lo + per);
+        double2 *z = reinterpret_cast<double2 *>(pa.zero_base);
+        for (int64_t q = lo + tid; q < hi; q += T)
+            z[q] = make_double2(0.0, 0.0);
+        if (blockIdx.x == 0 && tid == 0 && (pa.zero_n & 1))
+            pa.zero_base[pa.zero_n - 1] = 0.0;
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(pa.arrive, 1ull);
+        }
+    };
+    if (TAL_ZERO_MODE == 1 && !ORDERED && pa.zero_n)
+        zero_slice();
 
     for (int i = 0; i < n_my; ++i) {
         const int b = i & 1;
@@ -285,16 +321,16 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
         __syncthreads();  // node records of chunk i visible to all
         const uint8_t *bl = blob(b);
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);  // n_patch, n_node, node_begin, n_contrib
-        const uint16_t *lev = reinterpret_cast<const uint16_t *>(bl + 16 + 64 * T);
-        const uint8_t *tail = bl + 16 + 64 * T + 2 * BLOB_LEVELS + pad16(4 * hdr.y);
+        const uint16_t *lev = reinterpret_cast<const uint16_t *>(bl + 16 + L::TABLES);
+        const uint8_t *tail = bl + 16 + L::TABLES + 2 * BLOB_LEVELS + pad16(4 * hdr.y);
         const int32_t *cn = reinterpret_cast<const int32_t *>(tail);
         const uint8_t *run = tail + pad16(4 * hdr.y);
-        const double *nr = nrec(b);
+        const double *nr = nrec_s;
 
         // phase B: one patch per thread (lane-major tables: slot s at [s*T + tid])
         if (tid < hdr.x) {
             const uint16_t *ids = reinterpret_cast<const uint16_t *>(bl + 16) + tid;
-            const uint16_t *pos = ids + 16 * T;
+            const uint16_t *pos = ids + SLOTS * T;
 #define ID(s) ids[(s) * T]
 #define POS(s) pos[(s) * T]
             const int m = ID(0) & 0xff;
@@ -372,9 +408,15 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
 #undef ID
 #undef POS
         }
+        if (TAL_ZERO_MODE == 2 && !ORDERED && pa.zero_n && i == 0)
+            zero_slice();
+        if (!ORDERED && pa.zero_n && i == 0 && tid == 0) {  // every slice zeroed?
+            while (ld_acquire_u64(pa.arrive) < pa.target)
+                __nanosleep(64);
+        }
         __syncthreads();
-        // records of chunk i+1 into the other buffer (free since chunk i-1's
-        // phase B): its blob has had all of phase B(i) to land
+        // records of chunk i+1 into the (single) record buffer, free now that
+        // phase B(i) is done; its blob has had all of phase B(i) to land
         if (i + 1 < n_my) {
             mbar_wait(&bar[b ^ 1], ((i + 1) >> 1) & 1);
             gather(b ^ 1);

@@ -454,8 +454,8 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
     out.max_nodes = max_nodes;
     out.max_contrib = max_contrib;
     const int64_t np = P.n_patches();
-    out.pids.assign((size_t)np * 16, 0);
-    out.ppos.assign((size_t)np * 16, 0);
+    out.pids.assign((size_t)np * PATCH_SLOTS, 0);
+    out.ppos.assign((size_t)np * PATCH_SLOTS, 0);
     std::vector<int32_t> stamp((size_t)n_nodes, -1), local((size_t)n_nodes, 0), cnt((size_t)n_nodes, 0);
     std::vector<int32_t> cnt_chunks((size_t)n_nodes, 0);
     std::vector<int32_t> nodes, order, rank, fill;
@@ -497,7 +497,7 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
             out.levels.push_back(lev[s]);
         fill.assign(nn, 0);  // contributions placed so far per local node (patch order)
         for (int64_t g = p_begin; g < p_end; ++g) {
-            uint16_t *ids = out.pids.data() + 16 * g, *pos = out.ppos.data() + 16 * g;
+            uint16_t *ids = out.pids.data() + PATCH_SLOTS * g, *pos = out.ppos.data() + PATCH_SLOTS * g;
             const int32_t m = P.off[g + 1] - P.off[g] - 2;
             ids[0] = (uint16_t)(m | (P.closed[g] << 8));
             for (int32_t k = 0; k < m + 2; ++k) {
@@ -584,7 +584,9 @@ void pack_blobs(const Chunking &ch, int T, std::vector<uint8_t> &blobs, std::vec
 {
     const int64_t n_chunks = (int64_t)ch.chunks.size() / 5;
     auto pad = [](int64_t b) { return (b + 15) / 16 * 16; };
-    auto blob_bytes = [&](int64_t nn) { return 16 + 64 * (int64_t)T + 2 * CHUNK_LEVELS + 2 * pad(4 * nn) + pad(nn); };
+    auto blob_bytes = [&](int64_t nn) {
+        return 16 + 4 * PATCH_SLOTS * (int64_t)T + 2 * CHUNK_LEVELS + 2 * pad(4 * nn) + pad(nn);
+    };
     blob_off.assign((size_t)n_chunks + 1, 0);
     int64_t total = 0;
     for (int64_t c = 0; c < n_chunks; ++c) {
@@ -599,13 +601,13 @@ void pack_blobs(const Chunking &ch, int T, std::vector<uint8_t> &blobs, std::vec
         const int32_t hdr[4] = {npch, nn, n0, ch.chunks[5 * c + 4]};
         std::memcpy(b, hdr, 16);
         uint16_t *ids = reinterpret_cast<uint16_t *>(b + 16);
-        uint16_t *pos = ids + 16 * T;
+        uint16_t *pos = ids + PATCH_SLOTS * T;
         for (int32_t g = 0; g < npch; ++g)
-            for (int s = 0; s < 16; ++s) {
-                ids[s * T + g] = ch.pids[16 * (int64_t)(p0 + g) + s];
-                pos[s * T + g] = ch.ppos[16 * (int64_t)(p0 + g) + s];
+            for (int s = 0; s < PATCH_SLOTS; ++s) {
+                ids[s * T + g] = ch.pids[PATCH_SLOTS * (int64_t)(p0 + g) + s];
+                pos[s * T + g] = ch.ppos[PATCH_SLOTS * (int64_t)(p0 + g) + s];
             }
-        uint8_t *q = b + 16 + 64 * T;
+        uint8_t *q = b + 16 + 4 * PATCH_SLOTS * T;
         std::memcpy(q, ch.levels.data() + CHUNK_LEVELS * c, 2 * CHUNK_LEVELS);
         q += 2 * CHUNK_LEVELS;
         std::memcpy(q, ch.gather_nodes.data() + n0, 4 * (size_t)nn);

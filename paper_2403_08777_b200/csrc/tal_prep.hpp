@@ -34,7 +34,8 @@ void element_order(int method, const int32_t *conn4, const double *coords_int, i
 // and k = m - 1 for an open one.  A lone tet (c0,c1,c2,c3) is the open ring
 // a=c0, b=c1, r=(c2,c3).  Tets keep no corner order: the symmetric-rule
 // element operator is invariant under corner permutation (|det|, sgn det).
-constexpr int PATCH_MAX_RING = 13;  // ring nodes per patch (record: 16 u16)
+constexpr int PATCH_SLOTS = 12;                    // u16 slots per patch table row
+constexpr int PATCH_MAX_RING = PATCH_SLOTS - 3;     // ring nodes per patch (m|closed, a, b, r..)
 struct Patches {
     std::vector<int32_t> off;    // n_patches + 1, into nodes
     std::vector<int32_t> nodes;  // a, b, r_0 .. r_{m-1}
@@ -60,7 +61,7 @@ struct Chunking {
     std::vector<int32_t> cnodes;        // per chunk node, rank order: node id | bit31 interior
     std::vector<uint8_t> runs;          // per chunk node, rank order: contribution count
     std::vector<uint16_t> levels;       // CHUNK_LEVELS per chunk: jagged level offsets
-    std::vector<uint16_t> pids, ppos;   // 16 per patch: ids {m|closed<<8, a, b, r..}, positions
+    std::vector<uint16_t> pids, ppos;   // PATCH_SLOTS per patch: ids {m|closed<<8, a, b, r..}, positions
     // deterministic merge: for nodes in >1 chunk (and isolated nodes), the
     // chunk-node entries (node_begin + rank) holding their partial sums, in chunk order
     std::vector<int32_t> bnd_nodes, bnd_off, bnd_pos;
