@@ -136,6 +136,16 @@ int tal_default_mesh_opts(tal_mesh_opts *out);
 int tal_assemble(tal_handle *h, const double *u, const tal_params *p,
                  double *rhs, int scatter, tal_timings *t);
 
+/* Pipelined host round trip for streams of fields (time loops with host-side
+ * I/O, ensembles): enqueues H2D(u) -> assembly -> D2H(rhs) on internal
+ * streams and returns; at most two calls are in flight (a third call first
+ * waits for the oldest), so the H2D of field n+1 and the D2H of result n-1
+ * overlap the assembly of field n.  u and rhs must stay untouched until
+ * tal_wait(ticket) (pinned host memory, tal_host_alloc, gives full overlap). */
+int tal_assemble_async(tal_handle *h, const double *u, const tal_params *p,
+                       double *rhs, int scatter, int64_t *ticket);
+int tal_wait(tal_handle *h, int64_t ticket);
+
 /* Device-resident path (no host copies).  'stream' is a cudaStream_t (or 0).
  * tal_set_velocity_*: caller-numbered AoS (n_nodes,3) -> internal SoA.
  * tal_run: assemble internal u -> internal rhs (overwrites).  Asynchronous.

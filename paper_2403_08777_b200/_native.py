@@ -73,6 +73,8 @@ SIGNATURES = [
     ("tal_mesh_info_get", _I, [_P, ctypes.POINTER(TalMeshInfo)]),
     ("tal_default_mesh_opts", _I, [ctypes.POINTER(TalMeshOpts)]),
     ("tal_assemble", _I, [_P, _P, ctypes.POINTER(TalParams), _P, _I, ctypes.POINTER(TalTimings)]),
+    ("tal_assemble_async", _I, [_P, _P, ctypes.POINTER(TalParams), _P, _I, ctypes.POINTER(_I64)]),
+    ("tal_wait", _I, [_P, _I64]),
     ("tal_buffers_get", _I, [_P, ctypes.POINTER(TalBuffers)]),
     ("tal_set_velocity_host", _I, [_P, _P, _P]),
     ("tal_set_velocity_device", _I, [_P, _P, _P]),

@@ -268,6 +268,27 @@ class Assembler:
         return Timings(t.h2d_ms, t.pack_ms, t.kernel_ms, t.unpack_ms, t.d2h_ms, t.total_ms,
                        int(t.kernel_launches))
 
+    def assemble_async(self, u: np.ndarray, params: PhysParams, rhs: np.ndarray,
+                       scatter: Optional[str] = None) -> int:
+        """Pipelined host round trip (tal_assemble_async): enqueue and return a
+        ticket; ``u`` and ``rhs`` (C-contiguous float64 (n_nodes,3), ideally
+        pinned) must stay untouched until ``wait(ticket)``.  Two calls overlap:
+        H2D of the next field and D2H of the previous result run beside the
+        assembly of the current one."""
+        scatter = scatter or self.cfg.scatter
+        if scatter not in N.SCATTER:
+            raise ValueError(f"unknown scatter mode {scatter!r}")
+        for a in (u, rhs):
+            if a.shape != (self.n_nodes, 3) or a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError("u and rhs must be C-contiguous float64 (n_nodes, 3)")
+        t = ctypes.c_int64(0)
+        N.check(N.lib().tal_assemble_async(self._h, N.ptr(u), ctypes.byref(_params(params)),
+                                           N.ptr(rhs), N.SCATTER[scatter], ctypes.byref(t)))
+        return int(t.value)
+
+    def wait(self, ticket: int) -> None:
+        N.check(N.lib().tal_wait(self._h, int(ticket)))
+
     def assemble(self, u: np.ndarray, params: PhysParams, scatter: Optional[str] = None):
         rhs = np.empty((self.n_nodes, 3))
         t = self.assemble_into(np.ascontiguousarray(u, dtype=np.float64), params, rhs, scatter)

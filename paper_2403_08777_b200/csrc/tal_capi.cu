@@ -64,6 +64,11 @@ struct tal_handle {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
+    // pipelined host round trip (tal_assemble_async): two slots, copy streams
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+    double *astage_u[2] = {}, *astage_r[2] = {};
+    int64_t async_next = 0;  // next ticket
     int64_t N = 0, E = 0;
     bool has_mesh = false;
     // node data (internal order): records x y z ux uy uz (6*N) then rx ry rz (3*N)
@@ -100,13 +105,16 @@ struct tal_handle {
     void free_mesh()
     {
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
-                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_arrive};
+                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_arrive,
+                        astage_u[0], astage_u[1], astage_r[0], astage_r[1]};
         for (void *p : ptrs)
             if (p)
                 cudaFree(p);
         nodebuf = staging = d_partial = nullptr;
         d_arrive = nullptr;
         arrive_target = 0;
+        astage_u[0] = astage_u[1] = astage_r[0] = astage_r[1] = nullptr;
+        async_next = 0;
         perm = iperm = d_blob_off = d_bnd_nodes = d_bnd_off = d_bnd_pos = nullptr;
         conn = conn_col = nullptr;
         d_blobs = nullptr;
@@ -390,6 +398,13 @@ int tal_create(int device, tal_handle **out)
     }
     for (auto &ev : h->ev)
         cudaEventCreate(&ev);
+    cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking);
+    for (int s = 0; s < 2; ++s) {
+        cudaEventCreateWithFlags(&h->ev_h2d[s], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&h->ev_comp[s], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&h->ev_d2h[s], cudaEventDisableTiming);
+    }
     *out = h;
     return TAL_OK;
 }
@@ -400,9 +415,18 @@ int tal_destroy(tal_handle *h)
         return TAL_OK;
     DeviceGuard g(h->device);
     cudaStreamSynchronize(h->stream);
+    cudaStreamSynchronize(h->s_h2d);
+    cudaStreamSynchronize(h->s_d2h);
     h->free_mesh();
     for (auto &ev : h->ev)
         cudaEventDestroy(ev);
+    for (int s = 0; s < 2; ++s) {
+        cudaEventDestroy(h->ev_h2d[s]);
+        cudaEventDestroy(h->ev_comp[s]);
+        cudaEventDestroy(h->ev_d2h[s]);
+    }
+    cudaStreamDestroy(h->s_h2d);
+    cudaStreamDestroy(h->s_d2h);
     for (auto &ev : h->prof_ev)
         cudaEventDestroy(ev);
     cudaStreamDestroy(h->stream);
@@ -733,6 +757,66 @@ int tal_synchronize(tal_handle *h, void *stream)
         return fail(TAL_EINVAL, "handle is NULL");
     DeviceGuard g(h->device);
     TAL_CK(cudaStreamSynchronize(stream ? (cudaStream_t)stream : h->stream));
+    return TAL_OK;
+}
+
+int tal_assemble_async(tal_handle *h, const double *u, const tal_params *p, double *rhs, int scatter,
+                       int64_t *ticket)
+{
+    if (!h || !ticket)
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    if (h->N && (!u || !rhs))
+        return fail(TAL_EINVAL, "NULL field arrays");
+    int rc = check_params(p);
+    if (rc)
+        return rc;
+    DeviceGuard g(h->device);
+    const int64_t n = h->async_next;
+    const int s = (int)(n & 1);
+    const size_t nb = sizeof(double) * 3 * (size_t)h->N;
+    if (nb && !h->astage_u[s]) {
+        TAL_CK(cudaMalloc((void **)&h->astage_u[s], nb));
+        TAL_CK(cudaMalloc((void **)&h->astage_r[s], nb));
+    }
+    // slot s was last used by ticket n-2: its host buffers must be free
+    if (n >= 2)
+        TAL_CK(cudaEventSynchronize(h->ev_d2h[s]));
+    if (n >= 2)
+        TAL_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_comp[s], 0));  // staging_u[s] consumed
+    if (nb)
+        TAL_CK(cudaMemcpyAsync(h->astage_u[s], u, nb, cudaMemcpyHostToDevice, h->s_h2d));
+    TAL_CK(cudaEventRecord(h->ev_h2d[s], h->s_h2d));
+    TAL_CK(cudaStreamWaitEvent(h->stream, h->ev_h2d[s], 0));
+    if ((rc = tal_set_velocity_device(h, h->astage_u[s], h->stream)))
+        return rc;
+    if ((rc = launch_run(h, p, scatter, h->stream, nullptr)))
+        return rc;
+    if (n >= 2)
+        TAL_CK(cudaStreamWaitEvent(h->stream, h->ev_d2h[s], 0));  // staging_r[s] drained
+    if ((rc = tal_get_rhs_device(h, h->astage_r[s], h->stream)))
+        return rc;
+    TAL_CK(cudaEventRecord(h->ev_comp[s], h->stream));
+    TAL_CK(cudaStreamWaitEvent(h->s_d2h, h->ev_comp[s], 0));
+    if (nb)
+        TAL_CK(cudaMemcpyAsync(rhs, h->astage_r[s], nb, cudaMemcpyDeviceToHost, h->s_d2h));
+    TAL_CK(cudaEventRecord(h->ev_d2h[s], h->s_d2h));
+    *ticket = n;
+    h->async_next = n + 1;
+    return TAL_OK;
+}
+
+int tal_wait(tal_handle *h, int64_t ticket)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (ticket < 0 || ticket >= h->async_next)
+        return fail(TAL_EINVAL, "unknown ticket");
+    if (ticket < h->async_next - 2)
+        return TAL_OK;  // its slot was reused, so it completed already
+    DeviceGuard g(h->device);
+    TAL_CK(cudaEventSynchronize(h->ev_d2h[ticket & 1]));
     return TAL_OK;
 }
 
