@@ -87,8 +87,6 @@ struct tal_handle {
     int32_t *d_bnd_nodes = nullptr, *d_bnd_off = nullptr, *d_bnd_pos = nullptr;
     double *d_partial = nullptr;  // 3 * n_chunk_nodes
     int priv_grid = 0, priv_cfg = 1;
-    unsigned long long *d_arrive = nullptr;  // grid-barrier counter of the private kernel
-    unsigned long long arrive_target = 0;
     tal_mesh_info info = {};
     tal_timings last = {};
     // dominant-kernel event ring (tal_profile)
@@ -105,14 +103,12 @@ struct tal_handle {
     void free_mesh()
     {
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
-                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_arrive,
+                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial,
                         astage_u[0], astage_u[1], astage_r[0], astage_r[1]};
         for (void *p : ptrs)
             if (p)
                 cudaFree(p);
         nodebuf = staging = d_partial = nullptr;
-        d_arrive = nullptr;
-        arrive_target = 0;
         astage_u[0] = astage_u[1] = astage_r[0] = astage_r[1] = nullptr;
         async_next = 0;
         perm = iperm = d_blob_off = d_bnd_nodes = d_bnd_off = d_bnd_pos = nullptr;
@@ -281,34 +277,25 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             return launch_run(h, p, TAL_SCATTER_ATOMIC, s, launches);
         const bool ordered = scatter == TAL_SCATTER_PRIVATE;
         const int64_t ncn = (int64_t)h->ch.cnodes.size();
-        PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr, nullptr, nullptr,
-                    nullptr, 0, h->d_arrive, 0};
+        PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr, nullptr, nullptr};
         if (ordered && h->d_partial) {
             pa.px = h->d_partial;
             pa.py = h->d_partial + ncn;
             pa.pz = h->d_partial + 2 * ncn;
         }
+        // shared nodes receive FP64 REDs: zero the RHS first (a separate memset
+        // measured 16 us at 128^3; zeroing inside the kernel, by thread or TMA
+        // bulk stores, measured ~45 us slower -- DESIGN.md)
+        if (!ordered && N)
+            TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
         if (h->info.n_chunks) {
             const unsigned grid = (unsigned)std::min<int64_t>(h->priv_grid, h->info.n_chunks);
-#ifndef TAL_ZERO_MODE
-#define TAL_ZERO_MODE 0
-#endif
-            if (TAL_ZERO_MODE == 0 && !ordered && N)
-                TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
-            if (TAL_ZERO_MODE != 0 && !ordered && N) {
-                pa.zero_base = h->RX();
-                pa.zero_n = 3 * N;
-                h->arrive_target += grid;
-                pa.target = h->arrive_target;
-            }
             pm.begin();
             const cudaError_t le = launch_private(h->priv_cfg, ordered, grid, s, pa, nodes, rhs, kc);
             pm.end();
             if (le != cudaSuccess)
                 return fail(TAL_ECUDA, std::string("private kernel launch: ") + cudaGetErrorString(le));
             ++nl;
-        } else if (!ordered && N) {
-            TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
         }
         const int64_t nb = (int64_t)h->ch.bnd_nodes.size();
         if (ordered && nb) {
@@ -634,9 +621,6 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
              (C.bnd_nodes.size() + C.bnd_off.size() + C.bnd_pos.size()) * 4;
     if ((rc = set_kernel_attrs(h->device, h->priv_cfg, &h->priv_grid)))
         return rc;
-    TAL_CK(cudaMalloc((void **)&h->d_arrive, sizeof(unsigned long long)));
-    TAL_CK(cudaMemset(h->d_arrive, 0, sizeof(unsigned long long)));
-    h->arrive_target = 0;
     TAL_CK(cudaDeviceSynchronize());
 
     h->has_mesh = true;

@@ -189,8 +189,11 @@ __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict
 template <int CFG>
 struct PrivCfg;
 template <>
+#ifndef TAL_CFG0_MINB
+#define TAL_CFG0_MINB 7
+#endif
 struct PrivCfg<0> {  // 64 patches / chunk
-    static constexpr int THREADS = 64, NM = 144, NC = 544, MINB = 6;
+    static constexpr int THREADS = 64, NM = 144, NC = 544, MINB = TAL_CFG0_MINB;
 };
 #ifndef TAL_CFG1_MINB
 #define TAL_CFG1_MINB 4
@@ -225,21 +228,7 @@ struct PrivArgs {
     const int32_t *__restrict__ blob_off;  // 16-B units, n_chunks+1
     int n_chunks;
     double *px, *py, *pz;  // ordered-merge partials, indexed node_begin + j
-    // in-kernel zeroing of rx|ry|rz before the first FP64 RED (private-atomic;
-    // cooperative launch: every CTA is resident, so the arrival counter is a
-    // safe grid barrier).  zero_n == 0 disables it.
-    double *zero_base;
-    int64_t zero_n;              // doubles to zero (3 * n_nodes)
-    unsigned long long *arrive;  // monotone arrival counter
-    unsigned long long target;   // value meaning "every CTA of this launch zeroed"
 };
-
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p)
-{
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 template <int CFG, bool ORDERED>
 __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
@@ -294,26 +283,6 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
     }
     mbar_wait(&bar[0], 0);
     gather(0);
-#ifndef TAL_ZERO_MODE
-#define TAL_ZERO_MODE 0
-#endif
-    auto zero_slice = [&]() {  // zero this CTA's slice of the RHS, then arrive
-        const int64_t n2 = pa.zero_n / 2;  // double2 stores (3 * n_nodes doubles, 16-B aligned base)
-        const int64_t per = (n2 + gridDim.x - 1) / gridDim.x;
-        const int64_t lo = per * blockIdx.x, hi = min(n2, lo + per);
-        double2 *z = reinterpret_cast<double2 *>(pa.zero_base);
-        for (int64_t q = lo + tid; q < hi; q += T)
-            z[q] = make_double2(0.0, 0.0);
-        if (blockIdx.x == 0 && tid == 0 && (pa.zero_n & 1))
-            pa.zero_base[pa.zero_n - 1] = 0.0;
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            atomicAdd(pa.arrive, 1ull);
-        }
-    };
-    if (TAL_ZERO_MODE == 1 && !ORDERED && pa.zero_n)
-        zero_slice();
 
     for (int i = 0; i < n_my; ++i) {
         const int b = i & 1;
@@ -407,12 +376,6 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
             resz[POS(2)] = acc_b[2];
 #undef ID
 #undef POS
-        }
-        if (TAL_ZERO_MODE == 2 && !ORDERED && pa.zero_n && i == 0)
-            zero_slice();
-        if (!ORDERED && pa.zero_n && i == 0 && tid == 0) {  // every slice zeroed?
-            while (ld_acquire_u64(pa.arrive) < pa.target)
-                __nanosleep(64);
         }
         __syncthreads();
         // records of chunk i+1 into the (single) record buffer, free now that
