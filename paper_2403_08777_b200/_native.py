@@ -147,8 +147,9 @@ def device_count() -> int:
     return n.value if rc == TAL_OK else 0
 
 
-def fp64_peak(device: int = 0, ms_target: float = 50.0) -> tuple[float, float]:
-    """Measured FP64 FMA throughput (TFLOP/s) and the implied SM clock (MHz)."""
+def fp64_peak(device: int = 0, ms_target: float = 0.5) -> tuple[float, float]:
+    """Burst FP64 FMA throughput (TFLOP/s) and the SM clock (MHz) measured in
+    the best probe launch."""
     tf = ctypes.c_double(0.0)
     mhz = ctypes.c_double(0.0)
     check(lib().tal_fp64_peak(device, ms_target, ctypes.byref(tf), ctypes.byref(mhz)))

@@ -1116,6 +1116,9 @@ int tal_profile_read(tal_handle *h, double *ms_out, int64_t cap, int64_t *n_out)
 
 int tal_fp64_peak(int device, double ms_target, double *tflops, double *sm_clock_mhz)
 {
+    // Burst FP64 FMA throughput: launches sized to ~ms_target (comparable to
+    // one assembly), best of 20; the SM clock of the best launch is measured
+    // in-kernel (clock64 cycles / globaltimer ns of block 0).
     if (!tflops)
         return fail(TAL_EINVAL, "NULL output");
     int n = 0;
@@ -1126,45 +1129,49 @@ int tal_fp64_peak(int device, double ms_target, double *tflops, double *sm_clock
     TAL_CK(cudaGetDeviceProperties(&prop, device));
     const int blocks = prop.multiProcessorCount * 8, threads = 256;
     double *out = nullptr;
+    long long *clk = nullptr;
     TAL_CK(cudaMalloc((void **)&out, sizeof(double) * blocks));
+    TAL_CK(cudaMalloc((void **)&clk, sizeof(long long) * 2));
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    int iters = 64;
+    int iters = 16;
     float ms = 0.f;
-    k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);  // warm-up
-    for (int rep = 0; rep < 12; ++rep) {
+    k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7, clk);  // warm-up
+    for (int rep = 0; rep < 16; ++rep) {
         cudaEventRecord(a);
-        k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+        k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7, clk);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         cudaEventElapsedTime(&ms, a, b);
         if (ms >= ms_target)
             break;
-        iters = (int)std::min<double>(iters * std::max(2.0, 1.2 * ms_target / std::max(ms, 1e-3f)), 1 << 26);
+        iters = (int)std::min<double>(iters * std::max(1.25, ms_target / std::max(ms, 1e-3f)), 1 << 26);
     }
-    // best of 3 at the final size
-    float best = ms;
-    for (int rep = 0; rep < 3; ++rep) {
+    float best = 1e30f;
+    long long best_clk[2] = {0, 1};
+    for (int rep = 0; rep < 20; ++rep) {
         cudaEventRecord(a);
-        k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+        k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7, clk);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         cudaEventElapsedTime(&ms, a, b);
-        best = std::min(best, ms);
+        if (ms < best) {
+            best = ms;
+            cudaMemcpy(best_clk, clk, sizeof best_clk, cudaMemcpyDeviceToHost);
+        }
     }
     cudaError_t e = cudaGetLastError();
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(out);
+    cudaFree(clk);
     if (e != cudaSuccess)
         return fail(TAL_ECUDA, std::string("fp64 probe: ") + cudaGetErrorString(e));
     const double flops = 2.0 * 16.0 * 8.0 * (double)iters * blocks * threads;
     *tflops = flops / (best * 1e-3) / 1e12;
-    if (sm_clock_mhz) {
-        // 64 DFMA lanes/SM/clk on sm_100 -> implied clock
-        *sm_clock_mhz = (*tflops * 1e12) / (2.0 * 64.0 * prop.multiProcessorCount) / 1e6;
-    }
+    if (sm_clock_mhz)
+        *sm_clock_mhz = best_clk[1] > 0 ? (double)best_clk[0] / (double)best_clk[1] * 1e3 : 0.0;
     return TAL_OK;
 }
 

@@ -503,8 +503,14 @@ __global__ void k_halo_accumulate(const int32_t *__restrict__ list, int64_t n,
 }
 
 // FP64 pipe throughput probe: 8 independent DFMA chains per thread
-__global__ void __launch_bounds__(256) k_dfma_peak(double *out, int iters, double a, double b)
+__global__ void __launch_bounds__(256) k_dfma_peak(double *out, int iters, double a, double b,
+                                                   long long *clk)
 {
+    long long c0 = 0, t0 = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        c0 = clock64();
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    }
     double c[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -522,6 +528,12 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double *out, int iters, doubl
         s += c[i];
     if (s == 1.2345)  // never true; keeps the chains live
         out[blockIdx.x] = s;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // SM clock of this launch: cycles / ns
+        long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        clk[0] = clock64() - c0;
+        clk[1] = t1 - t0;
+    }
 }
 
 }  // namespace tal
