@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--permute", action="store_true", help="config 3: random node permutation")
+    ap.add_argument("--check", action="store_true",
+                    help="N>1: gather the owned RHS rows to rank 0 and check them against the oracle")
     return ap.parse_args()
 
 
@@ -215,12 +217,16 @@ def run_ours(a) -> None:
     from paper_2403_08777_b200 import _native as N
 
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = local
+    dev = local % max(torch.cuda.device_count(), 1)  # ranks may share a GPU in validation runs
+    torch.cuda.set_device(dev)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("TAL_DIST_BACKEND", "nccl")  # gloo: host-staged validation
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     P = tb.PhysParams()
     cfg = tb.RunConfig(scatter=a.scatter, renumber=a.renumber, element_order=a.element_order,
                        patches=a.patches, cta_patches=a.cta_patches, chunk_nodes=a.chunk_nodes,
@@ -361,6 +367,23 @@ def run_ours(a) -> None:
                "pipelined_results_consistent": ok}
         for p_ in pu + pr:
             p_.free()
+    if dom is not None and a.check:  # N>1 parity: owned rows of every rank vs the oracle
+        torch.cuda.synchronize()
+        rows = [None] * ws
+        dist.all_gather_object(rows, dom.owned_rhs())
+        if rank == 0:
+            from oracle import oracle as O
+            O.build()
+            g = O.box_mesh(c, c, c * ws)
+            ug = O.velocity(g.coords, a.init)
+            ref = O.assemble_rsp(g.coords, g.connectivity, ug, n_threads=O.default_threads())
+            full = np.full_like(ref, np.nan)
+            for lo, blk in rows:
+                full[lo:lo + blk.shape[0]] = blk
+            chk = O.compare(full, ref, g.coords, g.connectivity, ug)
+            parity = {"reference_rel_diff": chk.rel_diff, "rel_l2": chk.rel_l2,
+                      "entry_rel": chk.entry_rel, "passed": bool(chk.passed),
+                      "gathered": f"owned rows of {ws} ranks vs single-domain oracle"}
     clocks = sampler.stop()
     asm.profile(False)
 

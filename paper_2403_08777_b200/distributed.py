@@ -190,11 +190,30 @@ class SlabDomain:
         for nbr, lst in self._lists.items():
             asm.halo_pack(lst.data_ptr(), lst.numel(), self._send[nbr].data_ptr(), stream=stream)
             n += 1
-        exchange_interfaces(self.part, self._send, self._recv)
+        if self._host_staged():  # gloo (validation runs): stage the planes through host memory
+            send = {k: v.cpu() for k, v in self._send.items()}
+            recv = {k: v.cpu() for k, v in self._recv.items()}
+            exchange_interfaces(self.part, send, recv)
+            for k, v in recv.items():
+                self._recv[k].copy_(v)
+        else:
+            exchange_interfaces(self.part, self._send, self._recv)
         for nbr, lst in self._lists.items():
             asm.halo_accumulate(lst.data_ptr(), lst.numel(), self._recv[nbr].data_ptr(), stream=stream)
             n += 1
         return n
+
+    @staticmethod
+    def _host_staged() -> bool:
+        import torch.distributed as dist
+        return dist.is_initialized() and dist.get_backend() == "gloo"
+
+    def owned_rhs(self) -> tuple[int, np.ndarray]:
+        """(first global node id, rhs rows this rank reports) after a step."""
+        rhs = self.assembler.get_rhs_host(stream=0)
+        self.assembler.synchronize(stream=0)
+        lo, _ = self.part.node_range
+        return lo, rhs[self.part.owned_mask()]
 
     def close(self) -> None:
         self.assembler.close()
