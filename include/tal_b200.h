@@ -126,6 +126,13 @@ int tal_host_free(void *p);
 int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn,
                     int64_t n_nodes, int64_t n_elems, const int64_t *colors,
                     const tal_mesh_opts *opts);
+/* As tal_upload_mesh; 'external' (caller ids) are nodes whose sums other
+ * ranks complete (interface planes of a domain decomposition): they are never
+ * stored as chunk-interior, always accumulated, so a peer may add into them. */
+int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
+                       int64_t n_nodes, int64_t n_elems, const int64_t *colors,
+                       const tal_mesh_opts *opts, const int64_t *external,
+                       int64_t n_external);
 int tal_mesh_info_get(tal_handle *h, tal_mesh_info *out);
 int tal_default_mesh_opts(tal_mesh_opts *out);
 
@@ -176,6 +183,25 @@ int tal_halo_pack(tal_handle *h, const int32_t *d_list, int64_t n, double *d_out
 int tal_halo_accumulate(tal_handle *h, const int32_t *d_list, int64_t n, const double *d_in, void *stream);
 /* caller node id -> internal node id (host arrays) */
 int tal_map_nodes(tal_handle *h, const int64_t *caller_ids, int64_t n, int32_t *internal_ids);
+
+/* ---- fused interface sum over peer memory (domain decomposition) ---------- */
+/* With up to two neighbours attached, tal_run(scatter=private-atomic) REDs the
+ * partial sums of the attached interface nodes into the local RHS AND directly
+ * into the neighbour's RHS (NVLink peer memory), ordered across ranks by
+ * device-side flag words: zero -> signal/wait -> assemble -> signal/wait.
+ * The neighbour's RHS must be sized/renumbered as that neighbour's handle
+ * says: pass its INTERNAL ids (tal_map_nodes on the neighbour) for my caller
+ * ids my_ids[0..n).  In-process neighbours: tal_peer_local + tal_peer_attach;
+ * other processes: tal_peer_export (64-B cudaIpcMemHandle_t each) + tal_peer_open. */
+int tal_peer_local(tal_handle *h, double **rx, unsigned long long **flags, int64_t *n_nodes);
+int tal_peer_export(tal_handle *h, void *rhs_handle, int64_t *rhs_offset, void *flags_handle);
+int tal_peer_attach(tal_handle *h, int slot, double *peer_rx, int64_t peer_n_nodes,
+                    unsigned long long *peer_flags, const int64_t *my_ids,
+                    const int32_t *peer_ids, int64_t n);
+int tal_peer_open(tal_handle *h, int slot, const void *rhs_handle, int64_t rhs_offset,
+                  const void *flags_handle, int64_t peer_n_nodes, const int64_t *my_ids,
+                  const int32_t *peer_ids, int64_t n);
+int tal_peer_detach(tal_handle *h);
 
 /* ---- host-side mesh utilities (native; used by the Python Mesh type) ------- */
 /* Kuhn 6-tet split of a box (mesh.py:145-184). coords (N,3), conn (E,4). */

@@ -70,7 +70,13 @@ SIGNATURES = [
     ("tal_host_alloc", _I, [_I64, ctypes.POINTER(_P)]),
     ("tal_host_free", _I, [_P]),
     ("tal_upload_mesh", _I, [_P, _P, _P, _I64, _I64, _P, ctypes.POINTER(TalMeshOpts)]),
+    ("tal_upload_mesh_ex", _I, [_P, _P, _P, _I64, _I64, _P, ctypes.POINTER(TalMeshOpts), _P, _I64]),
     ("tal_mesh_info_get", _I, [_P, ctypes.POINTER(TalMeshInfo)]),
+    ("tal_peer_local", _I, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
+    ("tal_peer_export", _I, [_P, _P, ctypes.POINTER(_I64), _P]),
+    ("tal_peer_attach", _I, [_P, _I, _P, _I64, _P, _P, _P, _I64]),
+    ("tal_peer_open", _I, [_P, _I, _P, _I64, _P, _I64, _P, _P, _I64]),
+    ("tal_peer_detach", _I, [_P]),
     ("tal_default_mesh_opts", _I, [ctypes.POINTER(TalMeshOpts)]),
     ("tal_assemble", _I, [_P, _P, ctypes.POINTER(TalParams), _P, _I, ctypes.POINTER(TalTimings)]),
     ("tal_assemble_async", _I, [_P, _P, ctypes.POINTER(TalParams), _P, _I, ctypes.POINTER(_I64)]),

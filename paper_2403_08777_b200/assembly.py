@@ -214,7 +214,8 @@ class Assembler:
     internal (renumbered, SoA) buffers exposed by ``device_buffers()``.
     """
 
-    def __init__(self, mesh, cfg: Optional[RunConfig] = None, build_colors: Optional[bool] = None):
+    def __init__(self, mesh, cfg: Optional[RunConfig] = None, build_colors: Optional[bool] = None,
+                 external_nodes: Optional[np.ndarray] = None):
         cfg = cfg or RunConfig()
         self.cfg = cfg
         L = N.lib()
@@ -238,8 +239,10 @@ class Assembler:
             build_colors = cfg.scatter == "colored"
         opts.build_colors = 1 if build_colors else 0
         try:
-            N.check(L.tal_upload_mesh(h, N.ptr(coords), N.ptr(conn), self.n_nodes, self.n_elems,
-                                      N.ptr(colors), ctypes.byref(opts)))
+            ext = None if external_nodes is None else np.ascontiguousarray(external_nodes, np.int64)
+            N.check(L.tal_upload_mesh_ex(h, N.ptr(coords), N.ptr(conn), self.n_nodes, self.n_elems,
+                                         N.ptr(colors), ctypes.byref(opts), N.ptr(ext),
+                                         0 if ext is None else ext.shape[0]))
         except Exception:
             L.tal_destroy(h)
             self._h = None
@@ -358,6 +361,39 @@ class Assembler:
     def halo_accumulate(self, d_list: int, n: int, d_in: int, stream=None) -> None:
         N.check(N.lib().tal_halo_accumulate(self._h, ctypes.c_void_p(d_list), n,
                                             ctypes.c_void_p(d_in), _stream(stream)))
+
+    # -- fused interface sum with neighbouring ranks (include/tal_b200.h) ---
+    def peer_local(self) -> tuple[int, int, int]:
+        """(rhs x pointer, flag-word pointer, n_nodes) for an in-process neighbour."""
+        rx, fl, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+        N.check(N.lib().tal_peer_local(self._h, ctypes.byref(rx), ctypes.byref(fl), ctypes.byref(n)))
+        return rx.value, fl.value, n.value
+
+    def peer_export(self) -> tuple[bytes, int, bytes]:
+        """CUDA IPC handles of the RHS and flag words, for a neighbour process."""
+        rh = ctypes.create_string_buffer(64)
+        fh = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64()
+        N.check(N.lib().tal_peer_export(self._h, rh, ctypes.byref(off), fh))
+        return rh.raw, off.value, fh.raw
+
+    def peer_attach(self, slot: int, rx_ptr: int, peer_n: int, flags_ptr: int,
+                    my_ids: np.ndarray, peer_ids: np.ndarray) -> None:
+        my = np.ascontiguousarray(my_ids, dtype=np.int64)
+        pe = np.ascontiguousarray(peer_ids, dtype=np.int32)
+        N.check(N.lib().tal_peer_attach(self._h, slot, ctypes.c_void_p(rx_ptr), peer_n,
+                                        ctypes.c_void_p(flags_ptr), N.ptr(my), N.ptr(pe), my.shape[0]))
+
+    def peer_open(self, slot: int, rhs_handle: bytes, rhs_offset: int, flags_handle: bytes,
+                  peer_n: int, my_ids: np.ndarray, peer_ids: np.ndarray) -> None:
+        my = np.ascontiguousarray(my_ids, dtype=np.int64)
+        pe = np.ascontiguousarray(peer_ids, dtype=np.int32)
+        N.check(N.lib().tal_peer_open(self._h, slot, ctypes.c_char_p(rhs_handle), rhs_offset,
+                                      ctypes.c_char_p(flags_handle), peer_n, N.ptr(my), N.ptr(pe),
+                                      my.shape[0]))
+
+    def peer_detach(self) -> None:
+        N.check(N.lib().tal_peer_detach(self._h))
 
     def profile(self, enable: bool = True) -> None:
         """Record CUDA events around the dominant kernel of every run()."""

@@ -87,6 +87,18 @@ struct tal_handle {
     int32_t *d_bnd_nodes = nullptr, *d_bnd_off = nullptr, *d_bnd_pos = nullptr;
     double *d_partial = nullptr;  // 3 * n_chunk_nodes
     int priv_grid = 0, priv_cfg = 1;
+    // fused interface sum with up to two neighbours (domain decomposition)
+    struct Peer {
+        double *rx = nullptr;              // neighbour's RHS x (y, z follow at +n, +2n)
+        int64_t n = 0;                     // neighbour's node count
+        unsigned long long *flags = nullptr;  // neighbour's flag words
+        void *ipc_rhs = nullptr, *ipc_flags = nullptr;  // IPC mappings to close
+    } peers[2];
+    unsigned long long *d_flags = nullptr;  // own flag words (8): [0] zeroed, [1] done
+    int32_t *d_pidx = nullptr;              // per chunk-node entry: slot<<30 | remote id
+    std::vector<int32_t> h_pidx;
+    uint64_t peer_epoch = 0;
+    std::vector<uint8_t> external;  // internal-id mask of nodes completed by peers
     tal_mesh_info info = {};
     tal_timings last = {};
     // dominant-kernel event ring (tal_profile)
@@ -100,8 +112,29 @@ struct tal_handle {
     double *RY() const { return nodebuf + 7 * N; }
     double *RZ() const { return nodebuf + 8 * N; }
 
+    int n_peers() const { return (peers[0].rx ? 1 : 0) + (peers[1].rx ? 1 : 0); }
+
+    void free_peers()
+    {
+        for (auto &p : peers) {
+            if (p.ipc_rhs)
+                cudaIpcCloseMemHandle(p.ipc_rhs);
+            if (p.ipc_flags)
+                cudaIpcCloseMemHandle(p.ipc_flags);
+            p = Peer();
+        }
+        if (d_pidx)
+            cudaFree(d_pidx);
+        d_pidx = nullptr;
+        h_pidx.clear();
+        peer_epoch = 0;
+        if (d_flags)
+            cudaMemset(d_flags, 0, 8 * sizeof(unsigned long long));
+    }
+
     void free_mesh()
     {
+        free_peers();
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
                         d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial,
                         astage_u[0], astage_u[1], astage_r[0], astage_r[1]};
@@ -184,22 +217,24 @@ int check_params(const tal_params *p)
 
 template <int CFG>
 cudaError_t launch_private_cfg(bool ordered, unsigned grid, cudaStream_t s, PrivArgs pa, const double *nodes,
-                               RhsSoA rhs, ElemConsts kc)
+                               RhsSoA rhs, ElemConsts kc, PeerArgs peer)
 {
     constexpr size_t sm = PrivLayoutOf<CFG>::TOTAL;
     constexpr int T = PrivCfg<CFG>::THREADS;
-    void *args[] = {(void *)&pa, (void *)&nodes, (void *)&rhs, (void *)&kc};
-    const void *fn = ordered ? (const void *)k_assemble_private<CFG, true>
-                             : (const void *)k_assemble_private<CFG, false>;
-    // cooperative: all CTAs co-resident (the in-kernel zeroing barrier relies on it)
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(T), args, sm, s);
+    void *args[] = {(void *)&pa, (void *)&nodes, (void *)&rhs, (void *)&kc, (void *)&peer};
+    const void *fn = ordered   ? (const void *)k_assemble_private<CFG, true>
+                     : peer.pidx ? (const void *)k_assemble_private<CFG, false, true>
+                                    : (const void *)k_assemble_private<CFG, false>;
+    // plain launch of a persistent grid (occupancy x SMs); no grid-wide barrier
+    // is used, so CTAs that cannot be resident yet simply start later
+    return cudaLaunchKernel(fn, dim3(grid), dim3(T), args, sm, s);
 }
 
 cudaError_t launch_private(int cfg, bool ordered, unsigned grid, cudaStream_t s, const PrivArgs &pa,
-                           const double *nodes, RhsSoA rhs, const ElemConsts &kc)
+                           const double *nodes, RhsSoA rhs, const ElemConsts &kc, const PeerArgs &peer)
 {
-    return cfg == 0 ? launch_private_cfg<0>(ordered, grid, s, pa, nodes, rhs, kc)
-                    : launch_private_cfg<1>(ordered, grid, s, pa, nodes, rhs, kc);
+    return cfg == 0 ? launch_private_cfg<0>(ordered, grid, s, pa, nodes, rhs, kc, peer)
+                    : launch_private_cfg<1>(ordered, grid, s, pa, nodes, rhs, kc, peer);
 }
 
 struct ProfMark {
@@ -278,6 +313,19 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         const bool ordered = scatter == TAL_SCATTER_PRIVATE;
         const int64_t ncn = (int64_t)h->ch.cnodes.size();
         PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr, nullptr, nullptr};
+        PeerArgs peer{};
+        const int np = h->n_peers();
+        if (np && ordered)
+            return fail(TAL_EINVAL, "the fused interface sum needs scatter='private-atomic'");
+        if (np) {
+            peer.pidx = h->d_pidx;
+            for (int sl = 0; sl < 2; ++sl)
+                if (h->peers[sl].rx) {
+                    peer.rx[sl] = h->peers[sl].rx;
+                    peer.ry[sl] = h->peers[sl].rx + h->peers[sl].n;
+                    peer.rz[sl] = h->peers[sl].rx + 2 * h->peers[sl].n;
+                }
+        }
         if (ordered && h->d_partial) {
             pa.px = h->d_partial;
             pa.py = h->d_partial + ncn;
@@ -288,14 +336,27 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         // bulk stores, measured ~45 us slower -- DESIGN.md)
         if (!ordered && N)
             TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
+        if (np) {  // every neighbour has zeroed before anyone REDs into it
+            ++h->peer_epoch;
+            k_peer_signal<<<1, 1, 0, s>>>(h->peers[0].flags, h->peers[1].flags, 0);
+            k_peer_wait<<<1, 1, 0, s>>>(h->d_flags, 0, h->peer_epoch * np);
+            TAL_CK_LAUNCH();
+            nl += 2;
+        }
         if (h->info.n_chunks) {
             const unsigned grid = (unsigned)std::min<int64_t>(h->priv_grid, h->info.n_chunks);
             pm.begin();
-            const cudaError_t le = launch_private(h->priv_cfg, ordered, grid, s, pa, nodes, rhs, kc);
+            const cudaError_t le = launch_private(h->priv_cfg, ordered, grid, s, pa, nodes, rhs, kc, peer);
             pm.end();
             if (le != cudaSuccess)
                 return fail(TAL_ECUDA, std::string("private kernel launch: ") + cudaGetErrorString(le));
             ++nl;
+        }
+        if (np) {  // every neighbour's REDs into this RHS have landed
+            k_peer_signal<<<1, 1, 0, s>>>(h->peers[0].flags, h->peers[1].flags, 1);
+            k_peer_wait<<<1, 1, 0, s>>>(h->d_flags, 1, h->peer_epoch * np);
+            TAL_CK_LAUNCH();
+            nl += 2;
         }
         const int64_t nb = (int64_t)h->ch.bnd_nodes.size();
         if (ordered && nb) {
@@ -319,7 +380,8 @@ int set_attrs_cfg(int device, int *grid_out)
 {
     constexpr int sm = PrivLayoutOf<CFG>::TOTAL;
     const void *fns[] = {(const void *)k_assemble_private<CFG, true>,
-                         (const void *)k_assemble_private<CFG, false>};
+                         (const void *)k_assemble_private<CFG, false>,
+                         (const void *)k_assemble_private<CFG, false, true>};
     for (const void *f : fns)
         TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     int per_sm = 0, n_sm = 0;
@@ -385,6 +447,11 @@ int tal_create(int device, tal_handle **out)
     }
     for (auto &ev : h->ev)
         cudaEventCreate(&ev);
+    if (cudaMalloc((void **)&h->d_flags, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(h->d_flags, 0, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+        delete h;
+        return fail(TAL_ECUDA, "flag allocation failed");
+    }
     cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking);
     for (int s = 0; s < 2; ++s) {
@@ -414,6 +481,8 @@ int tal_destroy(tal_handle *h)
     }
     cudaStreamDestroy(h->s_h2d);
     cudaStreamDestroy(h->s_d2h);
+    if (h->d_flags)
+        cudaFree(h->d_flags);
     for (auto &ev : h->prof_ev)
         cudaEventDestroy(ev);
     cudaStreamDestroy(h->stream);
@@ -453,8 +522,20 @@ int tal_default_mesh_opts(tal_mesh_opts *o)
 int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, int64_t n_nodes,
                     int64_t n_elems, const int64_t *colors, const tal_mesh_opts *opts_in)
 {
+    return tal_upload_mesh_ex(h, coords, conn, n_nodes, n_elems, colors, opts_in, nullptr, 0);
+}
+
+int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn, int64_t n_nodes,
+                       int64_t n_elems, const int64_t *colors, const tal_mesh_opts *opts_in,
+                       const int64_t *external, int64_t n_external)
+{
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
+    if (n_external < 0 || (n_external && !external))
+        return fail(TAL_EINVAL, "bad external node list");
+    for (int64_t i = 0; i < n_external; ++i)
+        if (external[i] < 0 || external[i] >= n_nodes)
+            return fail(TAL_EINVAL, "external node id out of range [0, n_nodes)");
     if (n_nodes < 0 || n_elems < 0)
         return fail(TAL_EINVAL, "negative sizes");
     if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
@@ -532,7 +613,14 @@ int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, in
     h->priv_cfg = cfg;
     Patches patches;
     build_patches(cord.data(), n_nodes, n_elems, opts.patch_mode, patches);
-    if (!build_chunks(patches, n_nodes, opts.cta_patches, opts.chunk_nodes, cfg_max_contrib(cfg), h->ch, err))
+    std::vector<uint8_t> ext;
+    if (n_external) {
+        ext.assign((size_t)n_nodes, 0);
+        for (int64_t i = 0; i < n_external; ++i)
+            ext[renum ? iperm[external[i]] : external[i]] = 1;
+    }
+    if (!build_chunks(patches, n_nodes, opts.cta_patches, opts.chunk_nodes, cfg_max_contrib(cfg),
+                      ext.empty() ? nullptr : ext.data(), h->ch, err))
         return fail(TAL_EINVAL, err);
     h->info.n_patches = patches.n_patches();
     std::vector<uint8_t> blobs;
@@ -1077,6 +1165,111 @@ int tal_build_patches(const int64_t *conn, int64_t n_nodes, int64_t n_elems, int
         std::memcpy(nodes_out, p.nodes.data(), sizeof(int32_t) * p.nodes.size());
         std::memcpy(closed_out, p.closed.data(), p.closed.size());
     }
+    return TAL_OK;
+}
+
+int tal_peer_local(tal_handle *h, double **rx, unsigned long long **flags, int64_t *n_nodes)
+{
+    if (!h || !rx || !flags || !n_nodes)
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    *rx = h->RX();
+    *flags = h->d_flags;
+    *n_nodes = h->N;
+    return TAL_OK;
+}
+
+int tal_peer_export(tal_handle *h, void *rhs_handle, int64_t *rhs_offset, void *flags_handle)
+{
+    if (!h || !rhs_handle || !rhs_offset || !flags_handle)
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    DeviceGuard g(h->device);
+    TAL_CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)rhs_handle, h->nodebuf));
+    TAL_CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)flags_handle, h->d_flags));
+    *rhs_offset = (int64_t)((char *)h->RX() - (char *)h->nodebuf);
+    return TAL_OK;
+}
+
+int tal_peer_attach(tal_handle *h, int slot, double *peer_rx, int64_t peer_n_nodes,
+                    unsigned long long *peer_flags, const int64_t *my_ids, const int32_t *peer_ids,
+                    int64_t n)
+{
+    if (!h || slot < 0 || slot > 1 || !peer_rx || !peer_flags || peer_n_nodes <= 0 || n < 0 ||
+        (n && (!my_ids || !peer_ids)))
+        return fail(TAL_EINVAL, "bad arguments");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    DeviceGuard g(h->device);
+    // caller id -> internal id -> every chunk-node entry of that node
+    std::vector<int32_t> remote((size_t)h->N, -1);
+    for (int64_t i = 0; i < n; ++i) {
+        if (my_ids[i] < 0 || my_ids[i] >= h->N || peer_ids[i] < 0 || peer_ids[i] >= peer_n_nodes ||
+            peer_ids[i] >= (1 << 30))
+            return fail(TAL_EINVAL, "peer node id out of range");
+        const int64_t v = h->h_iperm.empty() ? my_ids[i] : h->h_iperm[my_ids[i]];
+        remote[v] = peer_ids[i];
+    }
+    const auto &cn = h->ch.cnodes;
+    if (h->h_pidx.size() != cn.size())
+        h->h_pidx.assign(cn.size(), -1);
+    for (size_t q = 0; q < cn.size(); ++q) {
+        const uint32_t raw = (uint32_t)cn[q];
+        const int32_t r = remote[raw & 0x7fffffffu];
+        if (r < 0)
+            continue;
+        if (raw & 0x80000000u)
+            return fail(TAL_EINVAL, "peer node was not declared external at upload");
+        h->h_pidx[q] = (int32_t)(((uint32_t)slot << 30) | (uint32_t)r);
+    }
+    if (!h->d_pidx && !cn.empty())
+        TAL_CK(cudaMalloc((void **)&h->d_pidx, sizeof(int32_t) * cn.size()));
+    if (!cn.empty())
+        TAL_CK(cudaMemcpy(h->d_pidx, h->h_pidx.data(), sizeof(int32_t) * cn.size(), cudaMemcpyHostToDevice));
+    h->peers[slot].rx = peer_rx;
+    h->peers[slot].n = peer_n_nodes;
+    h->peers[slot].flags = peer_flags;
+    return TAL_OK;
+}
+
+int tal_peer_open(tal_handle *h, int slot, const void *rhs_handle, int64_t rhs_offset,
+                  const void *flags_handle, int64_t peer_n_nodes, const int64_t *my_ids,
+                  const int32_t *peer_ids, int64_t n)
+{
+    if (!h || slot < 0 || slot > 1 || !rhs_handle || !flags_handle)
+        return fail(TAL_EINVAL, "bad arguments");
+    DeviceGuard g(h->device);
+    void *rb = nullptr, *fb = nullptr;
+    cudaIpcMemHandle_t hr, hf;
+    std::memcpy(&hr, rhs_handle, sizeof hr);
+    std::memcpy(&hf, flags_handle, sizeof hf);
+    TAL_CK(cudaIpcOpenMemHandle(&rb, hr, cudaIpcMemLazyEnablePeerAccess));
+    cudaError_t e = cudaIpcOpenMemHandle(&fb, hf, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaIpcCloseMemHandle(rb);
+        return fail(TAL_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    }
+    int rc = tal_peer_attach(h, slot, (double *)((char *)rb + rhs_offset), peer_n_nodes,
+                             (unsigned long long *)fb, my_ids, peer_ids, n);
+    if (rc) {
+        cudaIpcCloseMemHandle(rb);
+        cudaIpcCloseMemHandle(fb);
+        return rc;
+    }
+    h->peers[slot].ipc_rhs = rb;
+    h->peers[slot].ipc_flags = fb;
+    return TAL_OK;
+}
+
+int tal_peer_detach(tal_handle *h)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    DeviceGuard g(h->device);
+    cudaStreamSynchronize(h->stream);
+    h->free_peers();
     return TAL_OK;
 }
 

@@ -223,6 +223,15 @@ struct PrivLayout {
 template <int CFG>
 using PrivLayoutOf = PrivLayout<PrivCfg<CFG>::THREADS, PrivCfg<CFG>::NM, PrivCfg<CFG>::NC>;
 
+// Fused interface sum of a domain decomposition (scatter=private-atomic):
+// the partial sum of an interface-plane node is REDed into the local RHS and,
+// over NVLink peer memory, straight into the neighbouring rank's RHS -- the
+// assembly kernel itself performs the "collective".
+struct PeerArgs {
+    const int32_t *__restrict__ pidx;  // per chunk-node entry: slot<<30 | remote internal id, or -1
+    double *rx[2], *ry[2], *rz[2];     // neighbours' RHS (slot 0, 1)
+};
+
 struct PrivArgs {
     const uint8_t *__restrict__ blobs;
     const int32_t *__restrict__ blob_off;  // 16-B units, n_chunks+1
@@ -230,9 +239,10 @@ struct PrivArgs {
     double *px, *py, *pz;  // ordered-merge partials, indexed node_begin + j
 };
 
-template <int CFG, bool ORDERED>
+template <int CFG, bool ORDERED, bool PEER = false>
 __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
-    k_assemble_private(PrivArgs pa, const double *__restrict__ nrec_g, RhsSoA rhs, ElemConsts kc)
+    k_assemble_private(PrivArgs pa, const double *__restrict__ nrec_g, RhsSoA rhs, ElemConsts kc,
+                       PeerArgs peer)
 {
     constexpr int T = PrivCfg<CFG>::THREADS, NM = PrivCfg<CFG>::NM, NC = PrivCfg<CFG>::NC;
     using L = PrivLayoutOf<CFG>;
@@ -411,6 +421,16 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
                 atomicAdd(rhs.rx + v, ax);
                 atomicAdd(rhs.ry + v, ay);
                 atomicAdd(rhs.rz + v, az);
+                if constexpr (PEER) {
+                    const int pi = peer.pidx[hdr.z + q];
+                    if (pi >= 0) {  // interface node: the neighbour's copy gets our sum too
+                        const bool s1 = (pi >> 30) != 0;  // selects, not a local-memory index
+                        const int r = pi & 0x3fffffff;
+                        atomicAdd_system((s1 ? peer.rx[1] : peer.rx[0]) + r, ax);
+                        atomicAdd_system((s1 ? peer.ry[1] : peer.ry[0]) + r, ay);
+                        atomicAdd_system((s1 ? peer.rz[1] : peer.rz[0]) + r, az);
+                    }
+                }
             }
         }
         __syncthreads();  // blob b and res free again
@@ -475,6 +495,30 @@ __global__ void __launch_bounds__(256) k_unpack_aos(const double *__restrict__ r
     aos[3 * j + 0] = rx[s];
     aos[3 * j + 1] = ry[s];
     aos[3 * j + 2] = rz[s];
+}
+
+// cross-rank ordering of the fused interface sum: a rank signals each
+// neighbour (system-scope add on the neighbour's flag word) and waits until
+// its own flag word reached the epoch target
+__global__ void k_peer_signal(unsigned long long *f0, unsigned long long *f1, int which)
+{
+    __threadfence_system();
+    if (f0)
+        atomicAdd_system(f0 + which, 1ull);
+    if (f1)
+        atomicAdd_system(f1 + which, 1ull);
+}
+
+__global__ void k_peer_wait(const unsigned long long *flags, int which, unsigned long long target)
+{
+    for (;;) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + which) : "memory");
+        if (v >= target)
+            break;
+        __nanosleep(256);
+    }
+    __threadfence_system();
 }
 
 // interface-node exchange helpers (multi-GPU domain decomposition)

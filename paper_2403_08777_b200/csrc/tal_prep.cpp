@@ -442,7 +442,7 @@ void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int m
 }
 
 bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_nodes, int max_contrib,
-                  Chunking &out, std::string &err)
+                  const uint8_t *external, Chunking &out, std::string &err)
 {
     if (max_patches < 1 || max_nodes < PATCH_MAX_RING + 2 || max_contrib < PATCH_MAX_RING + 2 ||
         max_contrib > 65535 || max_nodes > 65535) {
@@ -552,13 +552,14 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
 
     // interior flag + shared/isolated node lists for the ordered merge
     const int64_t total = (int64_t)out.cnodes.size();
+    auto interior = [&](int64_t v) { return cnt_chunks[v] == 1 && !(external && external[v]); };
     for (int64_t q = 0; q < total; ++q) {
         const int32_t v = out.cnodes[q];
-        if (cnt_chunks[v] == 1)
+        if (interior(v))
             out.cnodes[q] = (int32_t)((uint32_t)v | 0x80000000u);
     }
     for (int64_t v = 0; v < n_nodes; ++v)
-        if (cnt_chunks[v] != 1) {
+        if (!interior(v)) {
             out.bnd_nodes.push_back((int32_t)v);
             if (cnt_chunks[v] > 1)
                 out.n_shared++;

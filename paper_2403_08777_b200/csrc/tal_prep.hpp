@@ -67,8 +67,11 @@ struct Chunking {
     std::vector<int32_t> bnd_nodes, bnd_off, bnd_pos;
     int64_t n_shared = 0;
 };
+// external[v] != 0 marks nodes whose sums other processes complete (e.g. the
+// interface planes of a domain decomposition): never "interior" to a chunk,
+// so they are always accumulated (REDs / ordered partials), never stored.
 bool build_chunks(const Patches &p, int64_t n_nodes, int max_patches, int max_nodes, int max_contrib,
-                  Chunking &out, std::string &err);
+                  const uint8_t *external, Chunking &out, std::string &err);
 // One contiguous 16-B aligned record per chunk (layout: tal_kernels.cuh,
 // patch tables transposed with stride 'cta_threads'); blob_off in 16-B units.
 void pack_blobs(const Chunking &ch, int cta_threads, std::vector<uint8_t> &blobs,

@@ -160,23 +160,54 @@ def exchange_interfaces(part: SlabPartition, send: dict, recv: dict, group=None)
 
 
 class SlabDomain:
-    """One rank's slab on its GPU: local assembly + NCCL interface sum."""
+    """One rank's slab on its GPU: local assembly + the interface sum.
 
-    def __init__(self, cells, rank: int, world: int, cfg=None):
+    ``fused`` (default for scatter='private-atomic'): the assembly kernel
+    itself REDs the interface-plane partial sums into the neighbours' RHS over
+    peer memory (CUDA IPC; include/tal_b200.h "fused interface sum") -- one
+    launch per step plus four tiny flag kernels, no separate exchange.
+    Otherwise: local assembly, then an NCCL send/recv of the interface planes
+    and a halo-add kernel (``exchange_interfaces``).
+    """
+
+    def __init__(self, cells, rank: int, world: int, cfg=None, fused: Optional[bool] = None):
         import torch
 
         from .assembly import Assembler, RunConfig
         self.part = SlabPartition(tuple(int(c) for c in cells), rank, world)
         self.cfg = cfg or RunConfig()
         self.mesh = self.part.local_mesh()
-        self.assembler = Assembler(self.mesh, self.cfg)
+        ifaces = self.part.interfaces()
+        if fused is None:
+            fused = self.cfg.scatter == "private-atomic" and world > 1
+        self.fused = bool(fused) and bool(ifaces)
+        ext = np.concatenate(list(ifaces.values())) if self.fused else None
+        self.assembler = Assembler(self.mesh, self.cfg, external_nodes=ext)
         dev = torch.device("cuda", self.cfg.device)
         self._lists, self._send, self._recv = {}, {}, {}
-        for nbr, ids in self.part.interfaces().items():
+        if self.fused:
+            self._connect_peers(ifaces)
+            return
+        for nbr, ids in ifaces.items():
             internal = self.assembler.map_nodes(ids)
             self._lists[nbr] = torch.as_tensor(internal, device=dev)
             self._send[nbr] = torch.empty((ids.size, 3), dtype=torch.float64, device=dev)
             self._recv[nbr] = torch.empty((ids.size, 3), dtype=torch.float64, device=dev)
+
+    def _connect_peers(self, ifaces) -> None:
+        """Exchange IPC handles and interface internal ids with the neighbours
+        (host objects over torch.distributed), then open the peer mappings."""
+        import torch.distributed as dist
+        asm = self.assembler
+        rh, off, fh = asm.peer_export()
+        mine = {nbr: asm.map_nodes(ids) for nbr, ids in ifaces.items()}
+        info = [None] * self.part.world
+        dist.all_gather_object(info, (rh, off, fh, asm.n_nodes, mine))
+        for nbr, ids in ifaces.items():
+            prh, poff, pfh, pn, pmap = info[nbr]
+            slot = 0 if nbr < self.part.rank else 1
+            asm.peer_open(slot, prh, poff, pfh, pn, ids, pmap[self.part.rank])
+        dist.barrier()
 
     def velocity(self, spec: str) -> np.ndarray:
         u = self.part.velocity(spec, self.mesh)
@@ -184,9 +215,11 @@ class SlabDomain:
         return u
 
     def step(self, params, stream=0) -> int:
-        """Local assembly, then the interface exchange; returns kernels launched."""
+        """One assembly including the interface sum; returns kernels launched."""
         asm = self.assembler
         n = asm.run(params, stream=stream)
+        if self.fused:
+            return n
         for nbr, lst in self._lists.items():
             asm.halo_pack(lst.data_ptr(), lst.numel(), self._send[nbr].data_ptr(), stream=stream)
             n += 1

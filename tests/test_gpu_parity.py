@@ -363,3 +363,62 @@ def test_slab_domains_loopback_on_one_gpu(oracle, world):
         asm.close()
     assert not np.isnan(full).any()
     assert_parity(oracle, full, ref, g, ug)
+
+
+def test_extreme_scales_all_modes(oracle):
+    """Tiny and huge mesh/velocity scales, non-default physics: every scatter
+    mode within tolerance, the deterministic ones bitwise reproducible."""
+    for ext, amp in [((1e-6, 1e-6, 1e-6), 1e3), ((1e3, 2e3, 5e2), 1e-4), ((1.0, 1.0, 1.0), 1e8)]:
+        m = tb.generate_box_mesh(7, 6, 5, extents=ext)
+        u = amp * np.random.default_rng(9).uniform(-1, 1, (m.n_nodes, 3))
+        p = tb.PhysParams(rho=2.0, mu=3e-3, c_vreman=0.1)
+        ref = oracle.assemble_rsp(m.coords, m.connectivity, u, p.rho, p.mu, p.c_vreman)
+        for mode in MODES:
+            a = run(m, u, p, scatter=mode).rhs
+            assert_parity(oracle, a, ref, m, u, p)
+            if mode in ("private", "colored"):
+                np.testing.assert_array_equal(a, run(m, u, p, scatter=mode).rhs)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_interface_sum_in_process(oracle, world):
+    """Fused interface sum: each slab's kernel REDs its interface partials into
+    the neighbour's RHS through peer pointers (here in-process, one device),
+    ordered by the device flag words; owned rows match the single-domain oracle,
+    and repeated steps (epochs) stay correct."""
+    from paper_2403_08777_b200.distributed import SlabPartition
+    cells = (8, 7, 10)
+    doms = []
+    for r in range(world):
+        p = SlabPartition(cells, r, world)
+        m = p.local_mesh()
+        ext = np.concatenate(list(p.interfaces().values()))
+        asm = tb.Assembler(m, tb.RunConfig(scatter="private-atomic"), external_nodes=ext)
+        asm.set_velocity_host(p.velocity("random:1", m))
+        doms.append((p, m, asm))
+    for p, m, asm in doms:
+        for nbr, ids in p.interfaces().items():
+            q, _, asq = doms[nbr]
+            rx, fl, n = asq.peer_local()
+            slot = 0 if nbr < p.rank else 1
+            asm.peer_attach(slot, rx, n, fl, ids, asq.map_nodes(q.interfaces()[p.rank]))
+    g = oracle.box_mesh(*cells)
+    ug = oracle.velocity(g.coords, "random:1")
+    ref = oracle.assemble_rsp(g.coords, g.connectivity, ug)
+    for step in range(3):
+        for p, m, asm in doms:
+            asm.run(P)  # internal streams: the ranks' flag waits overlap
+        full = np.full_like(ref, np.nan)
+        for p, m, asm in doms:
+            loc = asm.get_rhs_host()
+            asm.synchronize()
+            lo, hi = p.node_range
+            mask = p.owned_mask()
+            full[lo:hi][mask] = loc[mask]
+            for nbr, ids in p.interfaces().items():  # both copies of a plane agree
+                assert np.abs(loc[ids]).max() > 0
+        assert not np.isnan(full).any()
+        assert_parity(oracle, full, ref, g, ug)
+    for _, _, asm in doms:
+        asm.peer_detach()
+        asm.close()
