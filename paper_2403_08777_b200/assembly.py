@@ -54,8 +54,8 @@ class RunConfig:
     GPU knobs: ``device``, ``renumber`` (rcm | sfc | none), ``element_order``
     (sfc | node | keep), ``patches`` (star: edge-star patches, the rings of
     tets around an edge; tet: one tet per thread), ``cta_patches`` (patches =
-    threads per CTA chunk: <= 64 selects 64-thread CTAs, else 128) and
-    ``chunk_nodes`` (max distinct nodes per chunk: <= 144 | 256).
+    threads per CTA chunk: <= 64 | 128 | 256 select 64 | 128 | 256-thread CTAs)
+    and ``chunk_nodes`` (max distinct nodes per chunk: <= 144 | 256 | 512).
     """
 
     vector_dim: int = 16
@@ -89,11 +89,11 @@ class RunConfig:
             raise ValueError(f"element_order must be one of {tuple(N.EORDER)}")
         if self.patches not in N.PATCHES:
             raise ValueError(f"patches must be one of {tuple(N.PATCHES)}, got {self.patches!r}")
-        if not 1 <= self.cta_patches <= 128:
-            raise ValueError("cta_patches must be in [1, 128]")
-        # CTA shapes (tal_kernels.cuh PrivCfg): <= 64 patches -> 64 threads and
-        # room for 144 nodes; else 128 threads and 256 nodes
-        nmax = 144 if self.cta_patches <= 64 else 256
+        if not 1 <= self.cta_patches <= 256:
+            raise ValueError("cta_patches must be in [1, 256]")
+        # CTA shapes (tal_kernels.cuh PrivCfg): <= 64 | 128 | 256 patches run
+        # 64 | 128 | 256 threads with room for 144 | 256 | 512 nodes
+        nmax = 144 if self.cta_patches <= 64 else 256 if self.cta_patches <= 128 else 512
         if not 16 <= self.chunk_nodes <= nmax:
             raise ValueError(f"chunk_nodes must be in [16, {nmax}] for cta_patches={self.cta_patches}")
 

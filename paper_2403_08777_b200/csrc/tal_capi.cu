@@ -233,8 +233,9 @@ cudaError_t launch_private_cfg(bool ordered, unsigned grid, cudaStream_t s, Priv
 cudaError_t launch_private(int cfg, bool ordered, unsigned grid, cudaStream_t s, const PrivArgs &pa,
                            const double *nodes, RhsSoA rhs, const ElemConsts &kc, const PeerArgs &peer)
 {
-    return cfg == 0 ? launch_private_cfg<0>(ordered, grid, s, pa, nodes, rhs, kc, peer)
-                    : launch_private_cfg<1>(ordered, grid, s, pa, nodes, rhs, kc, peer);
+    return cfg == 0   ? launch_private_cfg<0>(ordered, grid, s, pa, nodes, rhs, kc, peer)
+           : cfg == 1 ? launch_private_cfg<1>(ordered, grid, s, pa, nodes, rhs, kc, peer)
+                      : launch_private_cfg<2>(ordered, grid, s, pa, nodes, rhs, kc, peer);
 }
 
 struct ProfMark {
@@ -393,14 +394,24 @@ int set_attrs_cfg(int device, int *grid_out)
 
 int set_kernel_attrs(int device, int cfg, int *grid_out)
 {
-    return cfg == 0 ? set_attrs_cfg<0>(device, grid_out) : set_attrs_cfg<1>(device, grid_out);
+    return cfg == 0   ? set_attrs_cfg<0>(device, grid_out)
+           : cfg == 1 ? set_attrs_cfg<1>(device, grid_out)
+                      : set_attrs_cfg<2>(device, grid_out);
 }
 
 // cta_patches -> CTA configuration (PrivCfg in tal_kernels.cuh)
-int cfg_for(int cta_patches) { return cta_patches <= PrivCfg<0>::THREADS ? 0 : 1; }
-int cfg_threads(int cfg) { return cfg == 0 ? PrivCfg<0>::THREADS : PrivCfg<1>::THREADS; }
-int cfg_max_nodes(int cfg) { return cfg == 0 ? PrivCfg<0>::NM : PrivCfg<1>::NM; }
-int cfg_max_contrib(int cfg) { return cfg == 0 ? PrivCfg<0>::NC : PrivCfg<1>::NC; }
+int cfg_for(int cta_patches)
+{
+    return cta_patches <= PrivCfg<0>::THREADS ? 0 : cta_patches <= PrivCfg<1>::THREADS ? 1 : 2;
+}
+template <class F>
+int by_cfg(int cfg, F f)
+{
+    return cfg == 0 ? f(PrivCfg<0>{}) : cfg == 1 ? f(PrivCfg<1>{}) : f(PrivCfg<2>{});
+}
+int cfg_threads(int cfg) { return by_cfg(cfg, [](auto c) { return decltype(c)::THREADS; }); }
+int cfg_max_nodes(int cfg) { return by_cfg(cfg, [](auto c) { return decltype(c)::NM; }); }
+int cfg_max_contrib(int cfg) { return by_cfg(cfg, [](auto c) { return decltype(c)::NC; }); }
 
 }  // namespace
 
@@ -605,9 +616,9 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
     // chunks
     std::string err;
     const int cfg = cfg_for(opts.cta_patches);
-    if (opts.cta_patches < 1 || opts.cta_patches > cfg_threads(1) || opts.chunk_nodes < 16 ||
+    if (opts.cta_patches < 1 || opts.cta_patches > cfg_threads(2) || opts.chunk_nodes < 16 ||
         opts.chunk_nodes > cfg_max_nodes(cfg) || (opts.patch_mode != 0 && opts.patch_mode != 1))
-        return fail(TAL_EINVAL, "cta_patches must be in [1," + std::to_string(cfg_threads(1)) +
+        return fail(TAL_EINVAL, "cta_patches must be in [1," + std::to_string(cfg_threads(2)) +
                                     "], chunk_nodes in [16," + std::to_string(cfg_max_nodes(cfg)) +
                                     "], patch_mode 0|1");
     h->priv_cfg = cfg;

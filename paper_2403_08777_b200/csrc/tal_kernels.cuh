@@ -206,6 +206,10 @@ template <>
 struct PrivCfg<1> {  // 128 patches / chunk
     static constexpr int THREADS = 128, NM = 256, NC = 1088, MINB = TAL_CFG1_MINB;
 };
+template <>
+struct PrivCfg<2> {  // 256 patches / chunk
+    static constexpr int THREADS = 256, NM = 512, NC = 2176, MINB = 2;
+};
 
 constexpr int BLOB_LEVELS = 32;  // = CHUNK_LEVELS (tal_prep.hpp)
 constexpr int SLOTS = 12;        // = PATCH_SLOTS (tal_prep.hpp)

@@ -107,7 +107,7 @@ def test_mesh_validation_errors():
 def test_runconfig_validation():
     for kw in [dict(vector_dim=0), dict(n_threads=0), dict(reps=0), dict(scatter="bogus"),
                dict(renumber="x"), dict(element_order="x"), dict(cta_patches=0),
-               dict(cta_patches=129), dict(chunk_nodes=8), dict(chunk_nodes=257),
+               dict(cta_patches=257), dict(chunk_nodes=8), dict(chunk_nodes=257),
                dict(cta_patches=64, chunk_nodes=145), dict(patches="x"), dict(device=-1),
                dict(cache_capacity_bytes=-1)]:
         with pytest.raises(ValueError):
