@@ -327,12 +327,13 @@ def run_ours(a) -> None:
     # end-to-end through the public host API (pinned host buffers): every step
     # copies that step's u host->device and reads its rhs back device->host.
     #  sync     : Assembler.assemble_into (one field at a time, blocking)
-    #  pipelined: Assembler.assemble_async, two fields in flight (H2D of the next
-    #             field and D2H of the previous result overlap the assembly)
+    #  pipelined: Assembler.assemble_async, three fields in flight (H2D of the
+    #             next field and D2H of the previous result overlap the assembly)
     e2e = None
     if not a.no_e2e and dom is None:
-        pu = [N.PinnedArray((Nn, 3)) for _ in range(2)]
-        pr = [N.PinnedArray((Nn, 3)) for _ in range(2)]
+        NSLOT = 3  # = tal_handle::ASYNC_SLOTS
+        pu = [N.PinnedArray((Nn, 3)) for _ in range(NSLOT)]
+        pr = [N.PinnedArray((Nn, 3)) for _ in range(NSLOT)]
         for p_ in pu:
             p_.array[:] = u
         ksteps = max(min(a.steps, 50), 3)
@@ -347,20 +348,20 @@ def run_ours(a) -> None:
             asm.assemble_into(pu[0].array, P, pr[0].array, a.scatter)
             tot += time.perf_counter() - t1
         sync_val = E * ksteps / tot
-        for i in range(4):  # warm the async slots
-            asm.wait(asm.assemble_async(pu[i & 1].array, P, pr[i & 1].array, a.scatter))
+        for i in range(2 * NSLOT):  # warm the async slots
+            asm.wait(asm.assemble_async(pu[i % NSLOT].array, P, pr[i % NSLOT].array, a.scatter))
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        tickets = [asm.assemble_async(pu[i & 1].array, P, pr[i & 1].array, a.scatter)
+        tickets = [asm.assemble_async(pu[i % NSLOT].array, P, pr[i % NSLOT].array, a.scatter)
                    for i in range(ksteps)]
-        for tk in tickets[-2:]:
+        for tk in tickets[-NSLOT:]:
             asm.wait(tk)
         pipe_tot = time.perf_counter() - t1
         ok = bool(np.array_equal(pr[0].array, pr[1].array)) if a.scatter in ("private", "colored") \
             else bool(np.allclose(pr[0].array, pr[1].array, rtol=0, atol=1e-12 * np.abs(pr[0].array).max()))
         e2e = {"value": E * ksteps / pipe_tot, "unit": "elem/s", "h2d_bytes_per_step": 24 * Nn,
                "d2h_bytes_per_step": 24 * Nn, "steps": ksteps,
-               "api": "Assembler.assemble_async (tal_assemble_async): 2 fields in flight, "
+               "api": "Assembler.assemble_async (tal_assemble_async): 3 fields in flight, "
                       "H2D/D2H overlapped with the assembly; wall clock over all steps",
                "sync_value": sync_val,
                "sync_api": "Assembler.assemble_into (tal_assemble), one field at a time, wall clock",

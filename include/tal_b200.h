@@ -145,9 +145,9 @@ int tal_assemble(tal_handle *h, const double *u, const tal_params *p,
 
 /* Pipelined host round trip for streams of fields (time loops with host-side
  * I/O, ensembles): enqueues H2D(u) -> assembly -> D2H(rhs) on internal
- * streams and returns; at most two calls are in flight (a third call first
+ * streams and returns; at most three calls are in flight (a fourth call first
  * waits for the oldest), so the H2D of field n+1 and the D2H of result n-1
- * overlap the assembly of field n.  u and rhs must stay untouched until
+ * overlap the assembly of field n and each other.  u and rhs must stay untouched until
  * tal_wait(ticket) (pinned host memory, tal_host_alloc, gives full overlap). */
 int tal_assemble_async(tal_handle *h, const double *u, const tal_params *p,
                        double *rhs, int scatter, int64_t *ticket);

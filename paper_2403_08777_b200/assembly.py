@@ -275,7 +275,7 @@ class Assembler:
                        scatter: Optional[str] = None) -> int:
         """Pipelined host round trip (tal_assemble_async): enqueue and return a
         ticket; ``u`` and ``rhs`` (C-contiguous float64 (n_nodes,3), ideally
-        pinned) must stay untouched until ``wait(ticket)``.  Two calls overlap:
+        pinned) must stay untouched until ``wait(ticket)``.  Three calls stay in flight:
         H2D of the next field and D2H of the previous result run beside the
         assembly of the current one."""
         scatter = scatter or self.cfg.scatter

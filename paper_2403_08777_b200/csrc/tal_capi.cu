@@ -64,10 +64,14 @@ struct tal_handle {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
-    // pipelined host round trip (tal_assemble_async): two slots, copy streams
+    // pipelined host round trip (tal_assemble_async): ASYNC_SLOTS fields in
+    // flight on two copy streams.  Three slots let the H2D of field n+1, the
+    // assembly of n and the D2H of n-1 run concurrently: the period is then
+    // max(h2d, d2h) instead of (h2d + compute + d2h) / 2 with two slots.
+    static constexpr int ASYNC_SLOTS = 3;
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
-    double *astage_u[2] = {}, *astage_r[2] = {};
+    cudaEvent_t ev_h2d[ASYNC_SLOTS] = {}, ev_comp[ASYNC_SLOTS] = {}, ev_d2h[ASYNC_SLOTS] = {};
+    double *astage_u[ASYNC_SLOTS] = {}, *astage_r[ASYNC_SLOTS] = {};
     int64_t async_next = 0;  // next ticket
     int64_t N = 0, E = 0;
     bool has_mesh = false;
@@ -136,13 +140,18 @@ struct tal_handle {
     {
         free_peers();
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
-                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial,
-                        astage_u[0], astage_u[1], astage_r[0], astage_r[1]};
+                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial};
         for (void *p : ptrs)
             if (p)
                 cudaFree(p);
         nodebuf = staging = d_partial = nullptr;
-        astage_u[0] = astage_u[1] = astage_r[0] = astage_r[1] = nullptr;
+        for (int s = 0; s < ASYNC_SLOTS; ++s) {
+            if (astage_u[s])
+                cudaFree(astage_u[s]);
+            if (astage_r[s])
+                cudaFree(astage_r[s]);
+            astage_u[s] = astage_r[s] = nullptr;
+        }
         async_next = 0;
         perm = iperm = d_blob_off = d_bnd_nodes = d_bnd_off = d_bnd_pos = nullptr;
         conn = conn_col = nullptr;
@@ -465,7 +474,7 @@ int tal_create(int device, tal_handle **out)
     }
     cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < tal_handle::ASYNC_SLOTS; ++s) {
         cudaEventCreateWithFlags(&h->ev_h2d[s], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&h->ev_comp[s], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&h->ev_d2h[s], cudaEventDisableTiming);
@@ -485,7 +494,7 @@ int tal_destroy(tal_handle *h)
     h->free_mesh();
     for (auto &ev : h->ev)
         cudaEventDestroy(ev);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < tal_handle::ASYNC_SLOTS; ++s) {
         cudaEventDestroy(h->ev_h2d[s]);
         cudaEventDestroy(h->ev_comp[s]);
         cudaEventDestroy(h->ev_d2h[s]);
@@ -856,17 +865,18 @@ int tal_assemble_async(tal_handle *h, const double *u, const tal_params *p, doub
     if (rc)
         return rc;
     DeviceGuard g(h->device);
+    constexpr int NS = tal_handle::ASYNC_SLOTS;
     const int64_t n = h->async_next;
-    const int s = (int)(n & 1);
+    const int s = (int)(n % NS);
     const size_t nb = sizeof(double) * 3 * (size_t)h->N;
     if (nb && !h->astage_u[s]) {
         TAL_CK(cudaMalloc((void **)&h->astage_u[s], nb));
         TAL_CK(cudaMalloc((void **)&h->astage_r[s], nb));
     }
-    // slot s was last used by ticket n-2: its host buffers must be free
-    if (n >= 2)
+    // slot s was last used by ticket n-NS: its device staging must be free
+    if (n >= NS)
         TAL_CK(cudaEventSynchronize(h->ev_d2h[s]));
-    if (n >= 2)
+    if (n >= NS)
         TAL_CK(cudaStreamWaitEvent(h->s_h2d, h->ev_comp[s], 0));  // staging_u[s] consumed
     if (nb)
         TAL_CK(cudaMemcpyAsync(h->astage_u[s], u, nb, cudaMemcpyHostToDevice, h->s_h2d));
@@ -876,7 +886,7 @@ int tal_assemble_async(tal_handle *h, const double *u, const tal_params *p, doub
         return rc;
     if ((rc = launch_run(h, p, scatter, h->stream, nullptr)))
         return rc;
-    if (n >= 2)
+    if (n >= NS)
         TAL_CK(cudaStreamWaitEvent(h->stream, h->ev_d2h[s], 0));  // staging_r[s] drained
     if ((rc = tal_get_rhs_device(h, h->astage_r[s], h->stream)))
         return rc;
@@ -896,10 +906,10 @@ int tal_wait(tal_handle *h, int64_t ticket)
         return fail(TAL_EINVAL, "handle is NULL");
     if (ticket < 0 || ticket >= h->async_next)
         return fail(TAL_EINVAL, "unknown ticket");
-    if (ticket < h->async_next - 2)
+    if (ticket < h->async_next - tal_handle::ASYNC_SLOTS)
         return TAL_OK;  // its slot was reused, so it completed already
     DeviceGuard g(h->device);
-    TAL_CK(cudaEventSynchronize(h->ev_d2h[ticket & 1]));
+    TAL_CK(cudaEventSynchronize(h->ev_d2h[ticket % tal_handle::ASYNC_SLOTS]));
     return TAL_OK;
 }
 

@@ -23,6 +23,14 @@ for r in rows[2:]:
             return float(g(k).replace(",", ""))
         except ValueError:
             return None
+    def tot(op):
+        r = f(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum")
+        if r is not None:
+            return r
+        r = f(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed")
+        c = f("smsp__cycles_elapsed.avg")
+        return None if r is None or c is None else round(r * c)
+
     stalls = {}
     for k in hdr:
         m = re.match(r"smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio$", k)
@@ -41,9 +49,14 @@ for r in rows[2:]:
         "registers": f("launch__registers_per_thread"),
         "smem_per_block": f("launch__shared_mem_per_block_dynamic"),
         "inst_executed": f("smsp__inst_executed.sum"),
-        "dfma_thread_inst": f("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum"),
-        "dmul_thread_inst": f("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"),
-        "dadd_thread_inst": f("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"),
+        # the full set reports these as rates: x elapsed SM cycles = totals
+        "dfma_thread_inst": tot("dfma"),
+        "dmul_thread_inst": tot("dmul"),
+        "dadd_thread_inst": tot("dadd"),
+        "local_ld_inst": f("sass__inst_executed_local_loads"),
+        "local_st_inst": f("sass__inst_executed_local_stores"),
+        "lsu_pipe_pct": f("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+        "shared_wavefronts": f("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
         "shared_bank_conflicts": f("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
         "l2_hit_pct": f("lts__t_sector_hit_rate.pct"),
         "red_sectors": f("l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum"),
