@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cells", type=int, default=128, help="cells per side (per rank slab)")
     ap.add_argument("--init", default="random:1")
     ap.add_argument("--scatter", default="private-atomic")
+    ap.add_argument("--variant", choices=["rsp", "rs", "b"], default="rsp",
+                    help="code shape (rs/b: the paper's study shapes, one thread per element)")
     ap.add_argument("--renumber", default="rcm")
     ap.add_argument("--element-order", default="sfc")
     ap.add_argument("--patches", default="star")
@@ -244,7 +246,9 @@ def run_ours(a) -> None:
         if a.permute:
             mesh = tb.permute_nodes(mesh, np.random.default_rng(0).permutation(mesh.n_nodes))
         u = tb.make_velocity(mesh, a.init)
-        asm = tb.Assembler(mesh, cfg)
+        variant = tb.VariantId(a.variant)
+        asm = tb.Assembler(mesh, cfg, build_colors=(a.scatter == "colored" or (
+            variant is not tb.VariantId.RSP and a.scatter == "private")))
     prep_s = time.perf_counter() - t0
     info = asm.info()
     E, Nn = mesh.n_elems, mesh.n_nodes
@@ -253,7 +257,7 @@ def run_ours(a) -> None:
 
     def one_step():
         if dom is None:
-            return asm.run(P, stream=stream)
+            return asm.run(P, stream=stream, variant=tb.VariantId(a.variant))
         return dom.step(P, stream=stream)
 
     # parity + CPU baseline (rank 0, N=1): the oracle as checker / baseline only
@@ -263,7 +267,7 @@ def run_ours(a) -> None:
         from oracle import oracle as O
         O.build()
         T = O.default_threads()
-        rhs_gpu, _ = asm.assemble(u, P)
+        rhs_gpu, _ = asm.assemble(u, P, variant=tb.VariantId(a.variant))
         O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)  # warm-up
         ts = []
         ref = None
@@ -330,7 +334,7 @@ def run_ours(a) -> None:
     #  pipelined: Assembler.assemble_async, three fields in flight (H2D of the
     #             next field and D2H of the previous result overlap the assembly)
     e2e = None
-    if not a.no_e2e and dom is None:
+    if not a.no_e2e and dom is None and a.variant == "rsp":
         NSLOT = 3  # = tal_handle::ASYNC_SLOTS
         pu = [N.PinnedArray((Nn, 3)) for _ in range(NSLOT)]
         pr = [N.PinnedArray((Nn, 3)) for _ in range(NSLOT)]
@@ -424,6 +428,10 @@ def run_ours(a) -> None:
     kname = {"private": "k_assemble_private<cfg,ordered=true>",
              "private-atomic": "k_assemble_private<cfg,ordered=false>",
              "atomic": "k_assemble_atomic<true>", "colored": "k_assemble_colored<true> (all colours)"}[a.scatter]
+    if a.variant != "rsp":
+        colored = a.scatter in ("private", "colored")
+        kname = ("k_assemble_baseline" if a.variant == "b" else "k_assemble_rs") + \
+            ("<colored> (all colours)" if colored else "<atomic>")
     traffic = ncu_traffic(kname, workload)
     line = {
         "metric": "assembled elements/s", "value": value, "unit": "elem/s", "n_gpus": ws,
@@ -433,7 +441,7 @@ def run_ours(a) -> None:
         "config": {"workload": workload, "n_elems": E, "n_nodes": Nn, "scatter": a.scatter,
                    "renumber": a.renumber, "element_order": a.element_order,
                    "patches": a.patches, "cta_patches": a.cta_patches, "chunk_nodes": a.chunk_nodes,
-                   "permuted": bool(a.permute),
+                   "permuted": bool(a.permute), "variant": a.variant,
                    "l2": "flushed (256 MiB write) before every step, outside the timed events"
                          if flush_buf is not None else "not flushed",
                    "parallelism": f"dp{ws} z-slabs" if ws > 1 else "single GPU"},

@@ -52,6 +52,15 @@ extern "C" {
 #define TAL_SCATTER_ATOMIC 2         /* 12 FP64 REDs per element */
 #define TAL_SCATTER_PRIVATE_ATOMIC 3 /* CTA-private smem sums, FP64 RED per shared node */
 
+/* code shapes of the paper's study (variants.py:28-60 VariantId).
+ * RSP is the production path (all scatter modes above); B and RS are the
+ * baseline and restructured+specialised shapes, one thread per element:
+ * scatter 'atomic'/'private-atomic' -> FP64 REDs, 'private'/'colored' ->
+ * colour-by-colour plain stores (bitwise reproducible, needs a colouring). */
+#define TAL_VARIANT_B 0
+#define TAL_VARIANT_RS 1
+#define TAL_VARIANT_RSP 2
+
 /* node renumbering applied at upload (inverted on every host read-back) */
 #define TAL_RENUMBER_NONE 0
 #define TAL_RENUMBER_RCM 1 /* reverse Cuthill-McKee on the node graph */
@@ -143,6 +152,11 @@ int tal_default_mesh_opts(tal_mesh_opts *out);
 int tal_assemble(tal_handle *h, const double *u, const tal_params *p,
                  double *rhs, int scatter, tal_timings *t);
 
+/* tal_assemble for any code shape (TAL_VARIANT_*): the assemble_baseline /
+ * assemble_rs / assemble_rsp entry points (variants.py:522-616). */
+int tal_assemble_variant(tal_handle *h, const double *u, const tal_params *p,
+                         double *rhs, int variant, int scatter, tal_timings *t);
+
 /* Pipelined host round trip for streams of fields (time loops with host-side
  * I/O, ensembles): enqueues H2D(u) -> assembly -> D2H(rhs) on internal
  * streams and returns; at most three calls are in flight (a fourth call first
@@ -162,6 +176,9 @@ int tal_set_velocity_host(tal_handle *h, const double *u, void *stream);
 int tal_set_velocity_device(tal_handle *h, const double *d_u, void *stream);
 int tal_run(tal_handle *h, const tal_params *p, int scatter, void *stream,
             int64_t *kernel_launches);
+/* tal_run for any code shape (TAL_VARIANT_*) */
+int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter,
+                    void *stream, int64_t *kernel_launches);
 int tal_get_rhs_host(tal_handle *h, double *rhs, void *stream);
 int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream);
 int tal_synchronize(tal_handle *h, void *stream);

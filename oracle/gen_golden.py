@@ -19,6 +19,9 @@ GPU path, against outputs of tet-assembly-lab 0.1.0 computed here:
                        random:1) -- harness.py:124-125 convention
 * ``vreman.npz``      vreman_viscosity known answers on random tensors
 * ``pmat.npz``        quadrature_tet4 points and pmat = P^T P
+* ``rhs_shapes.npz``  assemble_baseline / assemble_rs (variants.py:522-550)
+                       on the test_variants.py matrix + the 4^3 TG box
+                       (``--shapes`` writes only this file)
 This script is the only file in the repo that imports /root/reference; it is
 never run on the GPU box.
 """
@@ -51,7 +54,30 @@ def versions() -> dict:
     }
 
 
+def shapes() -> None:
+    """The B and RS code shapes of the reference (variants.py:522-550)."""
+    params = tal.PhysParams()
+    store = {}
+    for dims in [(2, 2, 2), (3, 2, 1)]:
+        m = tal.generate_box_mesh(*dims)
+        key = "x".join(map(str, dims))
+        for init in INITS:
+            u = tal.make_velocity(m, init)
+            ik = init.split(":")[0]
+            store[f"b_{key}_{ik}"] = tal.assemble_baseline(m, u, params, RunConfig(vector_dim=8)).rhs
+            store[f"rs_{key}_{ik}"] = tal.assemble_rs(m, u, params, RunConfig(vector_dim=8)).rhs
+    m = tal.generate_box_mesh(4, 4, 4)
+    u = tal.make_velocity(m, "taylor-green")
+    store["b_4x4x4_taylor-green"] = tal.assemble_baseline(m, u, params, RunConfig()).rhs
+    store["rs_4x4x4_taylor-green"] = tal.assemble_rs(m, u, params, RunConfig()).rhs
+    np.savez_compressed(OUT / "rhs_shapes.npz", **store, **{f"meta_{k}": v for k, v in versions().items()})
+    print("wrote rhs_shapes.npz", len(store))
+
+
 def main() -> None:
+    if "--shapes" in sys.argv:
+        shapes()
+        return
     OUT.mkdir(parents=True, exist_ok=True)
     params = tal.PhysParams()
     one = RunConfig(n_threads=1)
@@ -164,6 +190,7 @@ def main() -> None:
     rule = tal.quadrature_tet4()
     np.savez_compressed(OUT / "pmat.npz", points=rule.points, weights=rule.weights,
                         pmat=rule.points.T @ rule.points)
+    shapes()
     print("wrote", sorted(p.name for p in OUT.glob("*.npz")), meta)
 
 

@@ -8,6 +8,8 @@ numba seam ``assemble_elements`` run as hand-written sm_100a CUDA kernels in
 
 from .assembly import (
     ASSEMBLERS,
+    NULL_SCALE_FRACTION,
+    REL_TOL,
     SCATTER_MODES,
     Assembler,
     AssemblyResult,
@@ -16,12 +18,19 @@ from .assembly import (
     Timings,
     VARIANT_INFO,
     VariantId,
+    VariantCheck,
     VariantInfo,
+    VerifyReport,
     assemble,
+    assemble_baseline,
     assemble_elements,
+    assemble_rs,
     assemble_rsp,
     clear_cache,
+    contribution_scale,
     make_ledger,
+    oracle_compare,
+    verify_variants,
 )
 from .fields import (
     DENOM_EPSILON,

@@ -18,6 +18,7 @@ LIB_PATH = Path(os.environ.get("TAL_LIB_PATH") or Path(__file__).resolve().paren
 TAL_OK, TAL_EINVAL, TAL_ECUDA, TAL_ENOMEM, TAL_ESTATE = 0, 1, 2, 3, 4
 
 SCATTER = {"private": 0, "colored": 1, "atomic": 2, "private-atomic": 3}
+VARIANT = {"b": 0, "rs": 1, "rsp": 2}  # TAL_VARIANT_*
 RENUMBER = {"none": 0, "rcm": 1, "sfc": 2}
 EORDER = {"keep": 0, "node": 1, "sfc": 2}
 PATCHES = {"tet": 0, "star": 1}
@@ -79,6 +80,9 @@ SIGNATURES = [
     ("tal_peer_detach", _I, [_P]),
     ("tal_default_mesh_opts", _I, [ctypes.POINTER(TalMeshOpts)]),
     ("tal_assemble", _I, [_P, _P, ctypes.POINTER(TalParams), _P, _I, ctypes.POINTER(TalTimings)]),
+    ("tal_assemble_variant", _I, [_P, _P, ctypes.POINTER(TalParams), _P, _I, _I,
+                                  ctypes.POINTER(TalTimings)]),
+    ("tal_run_variant", _I, [_P, ctypes.POINTER(TalParams), _I, _I, _P, ctypes.POINTER(_I64)]),
     ("tal_assemble_async", _I, [_P, _P, ctypes.POINTER(TalParams), _P, _I, ctypes.POINTER(_I64)]),
     ("tal_wait", _I, [_P, _I64]),
     ("tal_buffers_get", _I, [_P, ctypes.POINTER(TalBuffers)]),

@@ -7,6 +7,11 @@ Reference interface mirrored (tet-assembly-lab 0.1.0, variants.py):
 * ``CounterLedger`` / ``VariantInfo`` / ``AssemblyResult`` (variants.py:104-135).
 * ``assemble_rsp(mesh, u, params, cfg) -> AssemblyResult`` (variants.py:553-616),
   registered in ``ASSEMBLERS`` and dispatched by ``assemble`` (:619-627).
+* ``assemble_baseline`` / ``assemble_rs`` (variants.py:522-550): the paper's
+  B and RS code shapes as sm_100a kernels (csrc/tal_shapes.cuh), for the
+  code-shape study on B200.
+* ``verify_variants`` / ``oracle_compare`` / ``contribution_scale``
+  (variants.py:634-755): the reference comparison arithmetic.
 * ``assemble_elements(coords, conn, u, rho, mu, cvre, pmat, ids, rhs)`` --
   the numba seam (_rsp_kernels.py:20-21), accumulating into ``rhs``.
 
@@ -18,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import math
 from collections import OrderedDict
 from dataclasses import dataclass
 from typing import Callable, Optional
@@ -29,7 +35,15 @@ from .fields import PhysParams, interpolation_table, validate_velocity
 
 
 class VariantId(enum.Enum):
+    B = "b"
+    RS = "rs"
     RSP = "rsp"
+
+
+# relative tolerance of the oracle comparison and the floor of its
+# denominator for cancellation-null fields (variants.py:62-65)
+REL_TOL = 1e-12
+NULL_SCALE_FRACTION = 0.01
 
 
 SCATTER_MODES = tuple(N.SCATTER)
@@ -121,9 +135,36 @@ class VariantInfo:
     flop_formula: str
 
 
-# The operator and its algorithmic cost are the reference RSP ledger's
-# (variants.py:207-217); the kernel executes fewer FP64 instructions.
+# Static per-element ledgers of the three code shapes: the reference's
+# statement-structure counts (variants.py:182-218), which the B200 kernels
+# follow shape for shape; the executed FP64 instructions measured by ncu are
+# in DESIGN.md (the RSP kernel executes fewer than its ledger).
 VARIANT_INFO: dict[VariantId, VariantInfo] = {
+    VariantId.B: VariantInfo(
+        variant=VariantId.B,
+        name="baseline (B200)",
+        summary="one thread per element, generic runtime trip counts, per-Gauss-point "
+        "geometry, dense 12x12 elemental matrix in local memory, separate scatter",
+        flops_per_elem=3108,
+        loadstore_per_elem=4908,
+        intermediate_doubles_per_elem=316,
+        intermediate_arrays=30,
+        flop_formula="4 gauss x 363 (geometry, fields, eddy viscosity) "
+        "+ 64 pairs x 21 (elemental matrix) + 300 (matvec) + 12 (scatter)",
+    ),
+    VariantId.RS: VariantInfo(
+        variant=VariantId.RS,
+        name="restructured+specialized (B200)",
+        summary="one thread per element, tet4 trip counts and constants fixed, one "
+        "gradient/viscosity per element, direct RHS entries, registers only",
+        flops_per_elem=544,
+        loadstore_per_elem=691,
+        intermediate_doubles_per_elem=113,
+        intermediate_arrays=27,
+        flop_formula="62 (geometry) + 63 (velocity gradient) + 67 (eddy viscosity) "
+        "+ 4 (factors) + 144 (point velocities and convection) + 192 (rhs entries) "
+        "+ 12 (scatter)",
+    ),
     VariantId.RSP: VariantInfo(
         variant=VariantId.RSP,
         name="privatized (B200)",
@@ -140,13 +181,20 @@ VARIANT_INFO: dict[VariantId, VariantInfo] = {
 
 
 def make_ledger(variant: VariantId, cfg: RunConfig) -> CounterLedger:
+    """The reference's modeled ledger (variants.py:221-243): 384 B/elem of
+    gathers + scatter RMW for every shape, plus a write+read-back of the
+    baseline's chunk intermediates once a chunk exceeds the modeled cache."""
     info = VARIANT_INFO[variant]
+    spill = 0.0
+    if variant is VariantId.B and \
+            info.intermediate_doubles_per_elem * 8 * cfg.vector_dim > cfg.cache_capacity_bytes:
+        spill = info.intermediate_doubles_per_elem * 8 * 2
     return CounterLedger(
         flops_per_elem=info.flops_per_elem,
         loadstore_per_elem=info.loadstore_per_elem,
         intermediate_doubles_per_elem=info.intermediate_doubles_per_elem,
         intermediate_arrays=info.intermediate_arrays,
-        bytes_dram_est=float(4 * 3 * 8 * 2 + 4 * 3 * 8 * 2),
+        bytes_dram_est=float(4 * 3 * 8 * 2 + 4 * 3 * 8 * 2) + spill,
     )
 
 
@@ -256,18 +304,21 @@ class Assembler:
 
     # -- host round trip -----------------------------------------------------
     def assemble_into(self, u: np.ndarray, params: PhysParams, rhs: np.ndarray,
-                      scatter: Optional[str] = None, pmat=None) -> Timings:
+                      scatter: Optional[str] = None, pmat=None,
+                      variant: VariantId = VariantId.RSP) -> Timings:
         scatter = scatter or self.cfg.scatter
         if scatter not in N.SCATTER:
             raise ValueError(f"unknown scatter mode {scatter!r}")
+        variant = VariantId(variant)
         if u.shape != (self.n_nodes, 3) or rhs.shape != (self.n_nodes, 3):
             raise ValueError("u and rhs must have shape (n_nodes, 3)")
         if not (u.flags.c_contiguous and rhs.flags.c_contiguous and u.dtype == np.float64
                 and rhs.dtype == np.float64):
             raise ValueError("u and rhs must be C-contiguous float64")
         t = N.TalTimings()
-        N.check(N.lib().tal_assemble(self._h, N.ptr(u), ctypes.byref(_params(params, pmat)),
-                                     N.ptr(rhs), N.SCATTER[scatter], ctypes.byref(t)))
+        N.check(N.lib().tal_assemble_variant(self._h, N.ptr(u), ctypes.byref(_params(params, pmat)),
+                                             N.ptr(rhs), N.VARIANT[variant.value],
+                                             N.SCATTER[scatter], ctypes.byref(t)))
         return Timings(t.h2d_ms, t.pack_ms, t.kernel_ms, t.unpack_ms, t.d2h_ms, t.total_ms,
                        int(t.kernel_launches))
 
@@ -292,9 +343,11 @@ class Assembler:
     def wait(self, ticket: int) -> None:
         N.check(N.lib().tal_wait(self._h, int(ticket)))
 
-    def assemble(self, u: np.ndarray, params: PhysParams, scatter: Optional[str] = None):
+    def assemble(self, u: np.ndarray, params: PhysParams, scatter: Optional[str] = None,
+                 variant: VariantId = VariantId.RSP):
         rhs = np.empty((self.n_nodes, 3))
-        t = self.assemble_into(np.ascontiguousarray(u, dtype=np.float64), params, rhs, scatter)
+        t = self.assemble_into(np.ascontiguousarray(u, dtype=np.float64), params, rhs, scatter,
+                               variant=variant)
         return rhs, t
 
     # -- device-resident path ----------------------------------------------
@@ -326,14 +379,15 @@ class Assembler:
                                                 _stream(stream)))
 
     def run(self, params: PhysParams, scatter: Optional[str] = None, stream=None,
-            pmat=None) -> int:
+            pmat=None, variant: VariantId = VariantId.RSP) -> int:
         """Enqueue one assembly on internal buffers; returns kernels launched."""
         scatter = scatter or self.cfg.scatter
         if scatter not in N.SCATTER:
             raise ValueError(f"unknown scatter mode {scatter!r}")
         nl = ctypes.c_int64(0)
-        N.check(N.lib().tal_run(self._h, ctypes.byref(_params(params, pmat)), N.SCATTER[scatter],
-                                _stream(stream), ctypes.byref(nl)))
+        N.check(N.lib().tal_run_variant(self._h, ctypes.byref(_params(params, pmat)),
+                                        N.VARIANT[VariantId(variant).value], N.SCATTER[scatter],
+                                        _stream(stream), ctypes.byref(nl)))
         return int(nl.value)
 
     def get_rhs_host(self, out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
@@ -424,16 +478,23 @@ _CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
 _CACHE_SIZE = 4
 
 
-def _cached_assembler(mesh, cfg: RunConfig) -> Assembler:
+def _needs_colors(variant: VariantId, scatter: str) -> bool:
+    """Colour-by-colour launches: scatter='colored', and the B / RS shapes
+    under the reproducible default scatter='private' (tal_b200.h)."""
+    return scatter == "colored" or (variant is not VariantId.RSP and scatter == "private")
+
+
+def _cached_assembler(mesh, cfg: RunConfig, variant: VariantId = VariantId.RSP) -> Assembler:
     colors = getattr(mesh, "colors", None)
+    need_colors = _needs_colors(variant, cfg.scatter)
     key = (id(mesh.coords), id(mesh.connectivity), id(colors), mesh.coords.shape,
            mesh.connectivity.shape, cfg.device, cfg.renumber, cfg.element_order,
-           cfg.patches, cfg.cta_patches, cfg.chunk_nodes, cfg.scatter == "colored")
+           cfg.patches, cfg.cta_patches, cfg.chunk_nodes, need_colors)
     hit = _CACHE.get(key)
     if hit is not None:
         _CACHE.move_to_end(key)
         return hit[0]
-    asm = Assembler(mesh, cfg)
+    asm = Assembler(mesh, cfg, build_colors=need_colors)
     # hold the arrays so their ids cannot be recycled while cached
     _CACHE[key] = (asm, mesh.coords, mesh.connectivity, colors)
     while len(_CACHE) > _CACHE_SIZE:
@@ -448,6 +509,19 @@ def clear_cache() -> None:
         asm.close()
 
 
+def _assemble_variant(variant: VariantId, mesh, u, params: PhysParams,
+                      cfg: Optional[RunConfig]) -> AssemblyResult:
+    cfg = cfg or RunConfig()
+    u = validate_velocity(mesh, u)
+    asm = _cached_assembler(mesh, cfg, variant)
+    rhs = np.empty((asm.n_nodes, 3))
+    t = asm.assemble_into(u, params, rhs, cfg.scatter, variant=variant)
+    wall = t.total_ms * 1e-3
+    rate = asm.n_elems / wall if wall > 0.0 else 0.0
+    return AssemblyResult(rhs=rhs, ledger=make_ledger(variant, cfg), wall_time=wall,
+                          elements_per_second=rate, variant=variant, timings=t)
+
+
 def assemble_rsp(mesh, u: np.ndarray, params: PhysParams,
                  cfg: Optional[RunConfig] = None) -> AssemblyResult:
     """Drop-in for ``tet_assembly_lab.assemble_rsp`` (variants.py:553-616).
@@ -456,18 +530,30 @@ def assemble_rsp(mesh, u: np.ndarray, params: PhysParams,
     (velocity H2D + layout pack + assembly kernels + unpack + RHS D2H); the
     one-time mesh upload is excluded like the reference's colouring.
     """
-    cfg = cfg or RunConfig()
-    u = validate_velocity(mesh, u)
-    asm = _cached_assembler(mesh, cfg)
-    rhs = np.empty((asm.n_nodes, 3))
-    t = asm.assemble_into(u, params, rhs, cfg.scatter)
-    wall = t.total_ms * 1e-3
-    rate = asm.n_elems / wall if wall > 0.0 else 0.0
-    return AssemblyResult(rhs=rhs, ledger=make_ledger(VariantId.RSP, cfg), wall_time=wall,
-                          elements_per_second=rate, variant=VariantId.RSP, timings=t)
+    return _assemble_variant(VariantId.RSP, mesh, u, params, cfg)
 
 
-ASSEMBLERS: dict[VariantId, Callable] = {VariantId.RSP: assemble_rsp}
+def assemble_baseline(mesh, u: np.ndarray, params: PhysParams,
+                      cfg: Optional[RunConfig] = None) -> AssemblyResult:
+    """The baseline code shape (variants.py:522-538) as a B200 kernel:
+    scatter 'private'/'colored' run colour by colour (bitwise reproducible),
+    'atomic'/'private-atomic' with FP64 REDs.  ``vector_dim`` only enters the
+    modeled ledger, as in the reference."""
+    return _assemble_variant(VariantId.B, mesh, u, params, cfg)
+
+
+def assemble_rs(mesh, u: np.ndarray, params: PhysParams,
+                cfg: Optional[RunConfig] = None) -> AssemblyResult:
+    """The restructured+specialised code shape (variants.py:541-550) as a
+    B200 kernel; scatter handling as ``assemble_baseline``."""
+    return _assemble_variant(VariantId.RS, mesh, u, params, cfg)
+
+
+ASSEMBLERS: dict[VariantId, Callable] = {
+    VariantId.B: assemble_baseline,
+    VariantId.RS: assemble_rs,
+    VariantId.RSP: assemble_rsp,
+}
 
 
 def assemble(variant: VariantId, mesh, u, params, cfg=None) -> AssemblyResult:
@@ -491,3 +577,99 @@ def assemble_elements(coords, conn, u, rho, mu, cvre, pmat, ids, rhs, device: in
                                           conn.shape[0], N.ptr(u), float(rho), float(mu),
                                           float(cvre), N.ptr(pm), N.ptr(ids), ids.shape[0],
                                           N.ptr(rhs)))
+
+
+# ---------------------------------------------------------------------------
+# verification arithmetic (variants.py:634-755)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class VariantCheck:
+    variant: VariantId
+    max_abs_diff: float
+    rel_diff: float
+    denominator: float
+    worst_node: int
+    passed: bool
+    note: str = ""
+
+
+@dataclass(frozen=True)
+class VerifyReport:
+    tolerance: float
+    denominator: float
+    checks: tuple
+    passed: bool
+
+
+def contribution_scale(mesh, u: np.ndarray, params: PhysParams) -> float:
+    """Bound on one element's raw RHS contribution (variants.py:653-676): the
+    denominator floor for fields whose assembled RHS is pure cancellation."""
+    conn = np.asarray(mesh.connectivity)
+    if conn.shape[0] == 0 or np.asarray(u).size == 0:
+        return 0.0
+    x = np.asarray(mesh.coords)[conn]
+    e = x[:, 1:] - x[:, :1]                                   # (E, 3 edges, 3)
+    cof = np.stack([np.cross(e[:, 1], e[:, 2]), np.cross(e[:, 2], e[:, 0]),
+                    np.cross(e[:, 0], e[:, 1])], axis=1)
+    det = np.einsum("ek,ek->e", e[:, 0], cof[:, 0])
+    vol = np.abs(det) / 6.0
+    grad_bound = 4.0 * np.abs(cof).max(axis=(1, 2)) / np.abs(det)
+    u_max = np.abs(np.asarray(u)[conn]).max(axis=(1, 2))
+    nut_cap = 24.0 * params.c_vreman * np.cbrt(6.0 * vol) ** 2 * grad_bound * u_max
+    scale = vol * u_max * grad_bound * (params.rho * u_max + params.mu + params.rho * nut_cap)
+    return float(scale.max())
+
+
+def _denominator(mesh, u, params, oracle: np.ndarray) -> float:
+    top = float(np.abs(oracle).max()) if oracle.size else 0.0
+    return max(top, NULL_SCALE_FRACTION * contribution_scale(mesh, u, params))
+
+
+def _compare(variant: VariantId, rhs: np.ndarray, oracle: np.ndarray, denom: float) -> VariantCheck:
+    bad = ~np.isfinite(rhs)
+    if bad.any():
+        node = int(np.argwhere(bad)[0][0])
+        return VariantCheck(variant, math.inf, math.inf, denom, node, False,
+                            f"non-finite output at node {node}")
+    diff = np.abs(rhs - oracle)
+    max_abs = float(diff.max()) if diff.size else 0.0
+    worst = int(np.argmax(diff) // 3) if diff.size else 0
+    rel = max_abs / denom if denom > 0.0 else (0.0 if max_abs == 0.0 else math.inf)
+    return VariantCheck(variant, max_abs, rel, denom, worst, rel <= REL_TOL)
+
+
+def oracle_compare(mesh, u: np.ndarray, params: PhysParams, rhs: np.ndarray,
+                   variant: VariantId, oracle: Optional[np.ndarray] = None) -> VariantCheck:
+    """Compare one assembled vector with an oracle vector (variants.py:714-720).
+    The CPU oracle is test infrastructure (repo ``oracle/``), never called
+    from this package: pass its vector as ``oracle``; without one the B
+    shape on the GPU -- the most literal restatement of the operator --
+    stands in."""
+    u = validate_velocity(mesh, u)
+    if oracle is None:
+        oracle = assemble_baseline(mesh, u, params, RunConfig(scatter="colored")).rhs
+    return _compare(VariantId(variant), rhs, oracle, _denominator(mesh, u, params, oracle))
+
+
+def verify_variants(mesh, u: np.ndarray, params: PhysParams, cfg: Optional[RunConfig] = None,
+                    fault_inject: Optional[str] = None,
+                    oracle: Optional[np.ndarray] = None) -> VerifyReport:
+    """Run every code shape and compare each with the oracle vector at
+    ``REL_TOL`` (variants.py:723-755); ``fault_inject`` (a variant value)
+    perturbs that shape's output to prove the check can fail.  ``oracle`` as
+    in :func:`oracle_compare`."""
+    cfg = cfg or RunConfig()
+    u = validate_velocity(mesh, u)
+    if oracle is None:
+        oracle = assemble_baseline(mesh, u, params, RunConfig(scatter="colored",
+                                                              device=cfg.device)).rhs
+    denom = _denominator(mesh, u, params, oracle)
+    checks = []
+    for variant, fn in ASSEMBLERS.items():
+        rhs = fn(mesh, u, params, cfg).rhs
+        if fault_inject is not None and variant.value == fault_inject:
+            rhs = rhs.copy()
+            rhs[0, 0] += 1e-6 * (denom if denom > 0.0 else 1.0)
+        checks.append(_compare(variant, rhs, oracle, denom))
+    return VerifyReport(REL_TOL, denom, tuple(checks), all(c.passed for c in checks))

@@ -16,6 +16,7 @@
 #include "../../include/tal_b200.h"
 #include "tal_kernels.cuh"
 #include "tal_prep.hpp"
+#include "tal_shapes.cuh"
 
 using namespace tal;
 
@@ -383,6 +384,95 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
     if (launches)
         *launches = nl;
     return TAL_OK;
+}
+
+// B / RS code shapes (tal_shapes.cuh): one thread per element over the
+// chunk-ordered connectivity (REDs) or colour by colour (plain stores)
+ShapeConsts shape_consts(const tal_params *p)
+{
+    ShapeConsts sc{};
+    sc.rho = p->rho;
+    sc.mu = p->mu;
+    sc.cvre = p->c_vreman;
+    sc.nn = 4;
+    sc.nd = 3;
+    sc.ng = 4;
+    // quadrature_tet4 (kernel.py:71-86): same IEEE operations as the reference
+    const double qa = (5.0 + 3.0 * std::sqrt(5.0)) / 20.0, qb = (5.0 - std::sqrt(5.0)) / 20.0;
+    static const double ref_grads[4][3] = {{-1.0, -1.0, -1.0}, {1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
+    for (int g = 0; g < 4; ++g) {
+        sc.wts[g] = 0.25;
+        for (int a = 0; a < 4; ++a) {
+            sc.npts[g][a] = (a == g) ? qa : qb;
+            for (int k = 0; k < 3; ++k)
+                sc.dshape[g][a][k] = ref_grads[a][k];
+        }
+    }
+    return sc;
+}
+
+int launch_shape(tal_handle *h, const tal_params *p, int variant, int scatter, cudaStream_t s,
+                 int64_t *launches)
+{
+    ProfMark pm{h, s};
+    ElemConsts kc;
+    bool sym;
+    if (!make_consts(p, kc, sym))
+        return fail(TAL_EINVAL, "non-finite physical parameters");
+    const ShapeConsts sc = shape_consts(p);
+    const double *nodes = h->REC();
+    RhsSoA rhs{h->RX(), h->RY(), h->RZ()};
+    const int64_t N = h->N, E = h->E;
+    const bool colored = scatter == TAL_SCATTER_PRIVATE || scatter == TAL_SCATTER_COLORED;
+    if (!colored && scatter != TAL_SCATTER_ATOMIC && scatter != TAL_SCATTER_PRIVATE_ATOMIC)
+        return fail(TAL_EINVAL, "unknown scatter mode " + std::to_string(scatter));
+    if (colored && !h->conn_col && E)
+        return fail(TAL_ESTATE, "colour-by-colour scatter needs a colouring (build_colors=1 or colors)");
+    int64_t nl = 0;
+    if (N)
+        TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
+    auto one = [&](const int4 *conn, int64_t b, int64_t e) -> int {
+        const unsigned grid = grid_for(e - b, 256);
+        if (variant == TAL_VARIANT_B) {
+            if (colored)
+                k_assemble_baseline<true><<<grid, 256, 0, s>>>(conn, b, e, nodes, rhs, sc);
+            else
+                k_assemble_baseline<false><<<grid, 256, 0, s>>>(conn, b, e, nodes, rhs, sc);
+        } else {
+            if (colored)
+                k_assemble_rs<true><<<grid, 256, 0, s>>>(conn, b, e, nodes, rhs, sc);
+            else
+                k_assemble_rs<false><<<grid, 256, 0, s>>>(conn, b, e, nodes, rhs, sc);
+        }
+        TAL_CK_LAUNCH();
+        ++nl;
+        return TAL_OK;
+    };
+    pm.begin();
+    if (colored) {
+        for (size_t c = 0; c + 1 < h->col_off.size(); ++c) {
+            const int64_t b = h->col_off[c], e = h->col_off[c + 1];
+            if (e > b)
+                if (int rc = one(h->conn_col, b, e))
+                    return rc;
+        }
+    } else if (E) {
+        if (int rc = one(h->conn, 0, E))
+            return rc;
+    }
+    pm.end();
+    if (launches)
+        *launches = nl;
+    return TAL_OK;
+}
+
+int launch_any(tal_handle *h, const tal_params *p, int variant, int scatter, cudaStream_t s, int64_t *launches)
+{
+    if (variant == TAL_VARIANT_RSP)
+        return launch_run(h, p, scatter, s, launches);
+    if (variant == TAL_VARIANT_B || variant == TAL_VARIANT_RS)
+        return launch_shape(h, p, variant, scatter, s, launches);
+    return fail(TAL_EINVAL, "unknown variant " + std::to_string(variant));
 }
 
 template <int CFG>
@@ -812,6 +902,20 @@ int tal_run(tal_handle *h, const tal_params *p, int scatter, void *stream, int64
     return launch_run(h, p, scatter, stream ? (cudaStream_t)stream : h->stream, kernel_launches);
 }
 
+int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter, void *stream,
+                    int64_t *kernel_launches)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    int rc = check_params(p);
+    if (rc)
+        return rc;
+    DeviceGuard g(h->device);
+    return launch_any(h, p, variant, scatter, stream ? (cudaStream_t)stream : h->stream, kernel_launches);
+}
+
 int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream)
 {
     if (!h || (!d_rhs && h->N))
@@ -916,6 +1020,12 @@ int tal_wait(tal_handle *h, int64_t ticket)
 int tal_assemble(tal_handle *h, const double *u, const tal_params *p, double *rhs, int scatter,
                  tal_timings *t)
 {
+    return tal_assemble_variant(h, u, p, rhs, TAL_VARIANT_RSP, scatter, t);
+}
+
+int tal_assemble_variant(tal_handle *h, const double *u, const tal_params *p, double *rhs, int variant,
+                         int scatter, tal_timings *t)
+{
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (!h->has_mesh)
@@ -938,7 +1048,7 @@ int tal_assemble(tal_handle *h, const double *u, const tal_params *p, double *rh
     nl += h->N ? 1 : 0;
     TAL_CK(cudaEventRecord(h->ev[2], s));
     int64_t nrun = 0;
-    if ((rc = launch_run(h, p, scatter, s, &nrun)))
+    if ((rc = launch_any(h, p, variant, scatter, s, &nrun)))
         return rc;
     nl += nrun;
     TAL_CK(cudaEventRecord(h->ev[3], s));

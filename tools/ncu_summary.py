@@ -23,6 +23,11 @@ for r in rows[2:]:
             return float(g(k).replace(",", ""))
         except ValueError:
             return None
+    def mb(k):  # byte-valued metric in MB whatever unit ncu chose
+        v = f(k)
+        scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}
+        return None if v is None else v * scale.get(units[hdr.index(k)], 1.0)
+
     def tot(op):
         r = f(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum")
         if r is not None:
@@ -41,8 +46,8 @@ for r in rows[2:]:
         "duration": [f("gpu__time_duration.sum"), units[hdr.index("gpu__time_duration.sum")]],
         "sm_clock": [f("smsp__cycles_elapsed.avg.per_second"),
                      units[hdr.index("smsp__cycles_elapsed.avg.per_second")]],
-        "dram_read_mbytes": f("dram__bytes_read.sum"),
-        "dram_write_mbytes": f("dram__bytes_write.sum"),
+        "dram_read_mbytes": mb("dram__bytes_read.sum"),
+        "dram_write_mbytes": mb("dram__bytes_write.sum"),
         "fp64_pipe_pct": f("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
         "issue_active_pct": f("sm__inst_issued.avg.pct_of_peak_sustained_active"),
         "warps_active_per_sm": f("sm__warps_active.avg.per_cycle_active"),
