@@ -335,7 +335,7 @@ def run_ours(a) -> None:
     #             next field and D2H of the previous result overlap the assembly)
     e2e = None
     if not a.no_e2e and dom is None and a.variant == "rsp":
-        NSLOT = 3  # = tal_handle::ASYNC_SLOTS
+        NSLOT = 4  # >= tal_handle::ASYNC_SLOTS: a host buffer is never reused while in flight
         pu = [N.PinnedArray((Nn, 3)) for _ in range(NSLOT)]
         pr = [N.PinnedArray((Nn, 3)) for _ in range(NSLOT)]
         for p_ in pu:

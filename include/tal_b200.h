@@ -143,6 +143,12 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
                        const tal_mesh_opts *opts, const int64_t *external,
                        int64_t n_external);
 int tal_mesh_info_get(tal_handle *h, tal_mesh_info *out);
+/* Host-only dry run of an upload: renumbering, element order, patches and CTA
+ * chunks as tal_upload_mesh would build them; fills n_nodes, n_elems,
+ * n_patches, n_chunks, n_chunk_nodes, n_shared_nodes, prep_seconds (no
+ * device needed -- layout quality checks and planning). */
+int tal_plan_layout(const double *coords, const int64_t *conn, int64_t n_nodes,
+                    int64_t n_elems, const tal_mesh_opts *opts, tal_mesh_info *out);
 int tal_default_mesh_opts(tal_mesh_opts *out);
 
 /* ---- assembly ------------------------------------------------------------- */

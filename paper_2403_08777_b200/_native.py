@@ -73,6 +73,8 @@ SIGNATURES = [
     ("tal_upload_mesh", _I, [_P, _P, _P, _I64, _I64, _P, ctypes.POINTER(TalMeshOpts)]),
     ("tal_upload_mesh_ex", _I, [_P, _P, _P, _I64, _I64, _P, ctypes.POINTER(TalMeshOpts), _P, _I64]),
     ("tal_mesh_info_get", _I, [_P, ctypes.POINTER(TalMeshInfo)]),
+    ("tal_plan_layout", _I, [_P, _P, _I64, _I64, ctypes.POINTER(TalMeshOpts),
+                             ctypes.POINTER(TalMeshInfo)]),
     ("tal_peer_local", _I, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
     ("tal_peer_export", _I, [_P, _P, ctypes.POINTER(_I64), _P]),
     ("tal_peer_attach", _I, [_P, _I, _P, _I64, _P, _P, _P, _I64]),

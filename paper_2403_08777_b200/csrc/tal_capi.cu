@@ -69,7 +69,10 @@ struct tal_handle {
     // flight on two copy streams.  Three slots let the H2D of field n+1, the
     // assembly of n and the D2H of n-1 run concurrently: the period is then
     // max(h2d, d2h) instead of (h2d + compute + d2h) / 2 with two slots.
-    static constexpr int ASYNC_SLOTS = 3;
+#ifndef TAL_ASYNC_SLOTS
+#define TAL_ASYNC_SLOTS 3
+#endif
+    static constexpr int ASYNC_SLOTS = TAL_ASYNC_SLOTS;
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d[ASYNC_SLOTS] = {}, ev_comp[ASYNC_SLOTS] = {}, ev_d2h[ASYNC_SLOTS] = {};
     double *astage_u[ASYNC_SLOTS] = {}, *astage_r[ASYNC_SLOTS] = {};
@@ -512,6 +515,69 @@ int cfg_threads(int cfg) { return by_cfg(cfg, [](auto c) { return decltype(c)::T
 int cfg_max_nodes(int cfg) { return by_cfg(cfg, [](auto c) { return decltype(c)::NM; }); }
 int cfg_max_contrib(int cfg) { return by_cfg(cfg, [](auto c) { return decltype(c)::NC; }); }
 
+// Host half of a mesh upload: renumbering, element order, patches, CTA
+// chunks (tal_prep.hpp).  Shared by tal_upload_mesh_ex and tal_plan_layout.
+struct HostLayout {
+    std::vector<int32_t> perm, iperm, eperm, cord;
+    std::vector<double> xin;
+    Patches patches;
+    Chunking ch;
+    int cfg = 1;
+};
+
+int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
+                const tal_mesh_opts &opts, const int64_t *external, int64_t n_external, HostLayout &L)
+{
+    // node renumbering: perm[new] = old
+    if (opts.renumber == TAL_RENUMBER_RCM)
+        renumber_rcm(conn, n_nodes, n_elems, L.perm);
+    else if (opts.renumber == TAL_RENUMBER_SFC)
+        renumber_sfc(coords, n_nodes, L.perm);
+    else if (opts.renumber != TAL_RENUMBER_NONE)
+        return fail(TAL_EINVAL, "unknown renumber method");
+    const bool renum = !L.perm.empty();
+    if (renum) {
+        L.iperm.resize((size_t)n_nodes);
+        for (int64_t i = 0; i < n_nodes; ++i)
+            L.iperm[L.perm[i]] = (int32_t)i;
+    }
+    L.xin.resize((size_t)(3 * n_nodes));  // internal AoS coords
+    for (int64_t i = 0; i < n_nodes; ++i) {
+        const int64_t s = renum ? L.perm[i] : i;
+        for (int c = 0; c < 3; ++c)
+            L.xin[3 * i + c] = coords[3 * s + c];
+    }
+    std::vector<int32_t> cin((size_t)(4 * n_elems));
+    for (int64_t i = 0; i < 4 * n_elems; ++i)
+        cin[i] = renum ? L.iperm[conn[i]] : (int32_t)conn[i];
+    // element order
+    element_order(opts.element_order, cin.data(), L.xin.data(), n_nodes, n_elems, L.eperm);
+    L.cord.resize((size_t)(4 * n_elems));
+    for (int64_t e = 0; e < n_elems; ++e)
+        for (int a = 0; a < 4; ++a)
+            L.cord[4 * e + a] = cin[4 * (int64_t)L.eperm[e] + a];
+    // chunks
+    std::string err;
+    const int cfg = cfg_for(opts.cta_patches);
+    if (opts.cta_patches < 1 || opts.cta_patches > cfg_threads(2) || opts.chunk_nodes < 16 ||
+        opts.chunk_nodes > cfg_max_nodes(cfg) || (opts.patch_mode != 0 && opts.patch_mode != 1))
+        return fail(TAL_EINVAL, "cta_patches must be in [1," + std::to_string(cfg_threads(2)) +
+                                    "], chunk_nodes in [16," + std::to_string(cfg_max_nodes(cfg)) +
+                                    "], patch_mode 0|1");
+    L.cfg = cfg;
+    build_patches(L.cord.data(), n_nodes, n_elems, opts.patch_mode, L.patches);
+    std::vector<uint8_t> ext;
+    if (n_external) {
+        ext.assign((size_t)n_nodes, 0);
+        for (int64_t i = 0; i < n_external; ++i)
+            ext[renum ? L.iperm[external[i]] : external[i]] = 1;
+    }
+    if (!build_chunks(L.patches, n_nodes, opts.cta_patches, opts.chunk_nodes, cfg_max_contrib(cfg),
+                      ext.empty() ? nullptr : ext.data(), L.ch, err))
+        return fail(TAL_EINVAL, err);
+    return TAL_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -681,57 +747,16 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
     h->N = n_nodes;
     h->E = n_elems;
 
-    // node renumbering: perm[new] = old
-    std::vector<int32_t> perm;
-    if (opts.renumber == TAL_RENUMBER_RCM)
-        renumber_rcm(conn, n_nodes, n_elems, perm);
-    else if (opts.renumber == TAL_RENUMBER_SFC)
-        renumber_sfc(coords, n_nodes, perm);
-    else if (opts.renumber != TAL_RENUMBER_NONE)
-        return fail(TAL_EINVAL, "unknown renumber method");
-    const bool renum = !perm.empty();
-    std::vector<int32_t> iperm;
-    if (renum) {
-        iperm.resize((size_t)n_nodes);
-        for (int64_t i = 0; i < n_nodes; ++i)
-            iperm[perm[i]] = (int32_t)i;
-    }
-    std::vector<double> xin((size_t)(3 * n_nodes));  // internal AoS coords
-    for (int64_t i = 0; i < n_nodes; ++i) {
-        const int64_t s = renum ? perm[i] : i;
-        for (int c = 0; c < 3; ++c)
-            xin[3 * i + c] = coords[3 * s + c];
-    }
-    std::vector<int32_t> cin((size_t)(4 * n_elems));
-    for (int64_t i = 0; i < 4 * n_elems; ++i)
-        cin[i] = renum ? iperm[conn[i]] : (int32_t)conn[i];
-    // element order
-    std::vector<int32_t> eperm;
-    element_order(opts.element_order, cin.data(), xin.data(), n_nodes, n_elems, eperm);
-    std::vector<int32_t> cord((size_t)(4 * n_elems));
-    for (int64_t e = 0; e < n_elems; ++e)
-        for (int a = 0; a < 4; ++a)
-            cord[4 * e + a] = cin[4 * (int64_t)eperm[e] + a];
-    // chunks
-    std::string err;
-    const int cfg = cfg_for(opts.cta_patches);
-    if (opts.cta_patches < 1 || opts.cta_patches > cfg_threads(2) || opts.chunk_nodes < 16 ||
-        opts.chunk_nodes > cfg_max_nodes(cfg) || (opts.patch_mode != 0 && opts.patch_mode != 1))
-        return fail(TAL_EINVAL, "cta_patches must be in [1," + std::to_string(cfg_threads(2)) +
-                                    "], chunk_nodes in [16," + std::to_string(cfg_max_nodes(cfg)) +
-                                    "], patch_mode 0|1");
+    HostLayout L;
+    if (int rc = host_layout(coords, conn, n_nodes, n_elems, opts, external, n_external, L))
+        return rc;
+    const int cfg = L.cfg;
     h->priv_cfg = cfg;
-    Patches patches;
-    build_patches(cord.data(), n_nodes, n_elems, opts.patch_mode, patches);
-    std::vector<uint8_t> ext;
-    if (n_external) {
-        ext.assign((size_t)n_nodes, 0);
-        for (int64_t i = 0; i < n_external; ++i)
-            ext[renum ? iperm[external[i]] : external[i]] = 1;
-    }
-    if (!build_chunks(patches, n_nodes, opts.cta_patches, opts.chunk_nodes, cfg_max_contrib(cfg),
-                      ext.empty() ? nullptr : ext.data(), h->ch, err))
-        return fail(TAL_EINVAL, err);
+    h->ch = std::move(L.ch);
+    std::vector<int32_t> &perm = L.perm, &iperm = L.iperm, &eperm = L.eperm, &cord = L.cord;
+    std::vector<double> &xin = L.xin;
+    const bool renum = !perm.empty();
+    Patches &patches = L.patches;
     h->info.n_patches = patches.n_patches();
     std::vector<uint8_t> blobs;
     std::vector<int32_t> blob_off;
@@ -830,6 +855,35 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
     h->info.n_shared_nodes = C.n_shared;
     h->info.device_bytes = (int64_t)bytes;
     h->info.prep_seconds = std::chrono::duration<double>(t1 - t0).count();
+    return TAL_OK;
+}
+
+int tal_plan_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
+                    const tal_mesh_opts *opts_in, tal_mesh_info *out)
+{
+    if (!out || n_nodes < 0 || n_elems < 0 || (n_nodes && !coords) || (n_elems && !conn))
+        return fail(TAL_EINVAL, "bad arguments");
+    if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
+        return fail(TAL_EINVAL, "meshes are limited to 2^31-1 nodes/elements per device");
+    for (int64_t i = 0; i < 4 * n_elems; ++i)
+        if (conn[i] < 0 || conn[i] >= n_nodes)
+            return fail(TAL_EINVAL, "connectivity index out of range [0, n_nodes)");
+    tal_mesh_opts opts;
+    tal_default_mesh_opts(&opts);
+    if (opts_in)
+        opts = *opts_in;
+    const auto t0 = std::chrono::steady_clock::now();
+    HostLayout L;
+    if (int rc = host_layout(coords, conn, n_nodes, n_elems, opts, nullptr, 0, L))
+        return rc;
+    *out = tal_mesh_info{};
+    out->n_nodes = n_nodes;
+    out->n_elems = n_elems;
+    out->n_patches = L.patches.n_patches();
+    out->n_chunks = (int64_t)L.ch.chunks.size() / 5;
+    out->n_chunk_nodes = (int64_t)L.ch.cnodes.size();
+    out->n_shared_nodes = L.ch.n_shared;
+    out->prep_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return TAL_OK;
 }
 

@@ -173,8 +173,16 @@ uint64_t spread3(uint64_t v)
     return v;
 }
 
+// Morton order of points.  With a grid (pitch cell[3] > 0 per axis, anchored
+// at origin[3]) the primary key is the Morton code of the point's grid cell --
+// on an element-size grid, points of one cell stay together and aligned code
+// blocks are compact blocks of cells whatever the extents -- and the
+// bounding-box code breaks ties; without one, the bounding-box code only.
+inline bool p_ok(double lo, double origin) { return lo >= origin; }
+
 template <class GetPoint>
-void morton_order(int64_t n, GetPoint pt, std::vector<int32_t> &perm)
+void morton_order(int64_t n, GetPoint pt, std::vector<int32_t> &perm, const double *cell = nullptr,
+                  const double *origin = nullptr)
 {
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int64_t i = 0; i < n; ++i) {
@@ -189,19 +197,33 @@ void morton_order(int64_t n, GetPoint pt, std::vector<int32_t> &perm)
     for (int c = 0; c < 3; ++c)
         span = std::max(span, hi[c] - lo[c]);
     const double scale = span > 0.0 ? (double)((1u << 21) - 1) / span : 0.0;
-    std::vector<std::pair<uint64_t, int32_t>> key((size_t)n);
+    bool grid = cell && origin;
+    for (int c = 0; grid && c < 3; ++c)
+        grid = cell[c] > 0.0 && (hi[c] - origin[c]) / cell[c] < (double)(1u << 21) && p_ok(lo[c], origin[c]);
+    struct Key {
+        uint64_t coarse, fine;
+        int32_t i;
+        bool operator<(const Key &o) const
+        {
+            return coarse != o.coarse ? coarse < o.coarse : fine != o.fine ? fine < o.fine : i < o.i;
+        }
+    };
+    std::vector<Key> key((size_t)n);
     for (int64_t i = 0; i < n; ++i) {
         double p[3];
         pt(i, p);
-        uint64_t code = 0;
-        for (int c = 0; c < 3; ++c)
-            code |= spread3((uint64_t)((p[c] - lo[c]) * scale)) << c;
-        key[i] = {code, (int32_t)i};
+        uint64_t fine = 0, coarse = 0;
+        for (int c = 0; c < 3; ++c) {
+            fine |= spread3((uint64_t)((p[c] - lo[c]) * scale)) << c;
+            if (grid)
+                coarse |= spread3((uint64_t)((p[c] - origin[c]) / cell[c])) << c;
+        }
+        key[i] = {coarse, fine, (int32_t)i};
     }
     std::sort(key.begin(), key.end());
     perm.resize((size_t)n);
     for (int64_t i = 0; i < n; ++i)
-        perm[i] = key[i].second;
+        perm[i] = key[i].i;
 }
 
 }  // namespace
@@ -259,7 +281,6 @@ void renumber_sfc(const double *coords, int64_t n_nodes, std::vector<int32_t> &p
 void element_order(int method, const int32_t *conn4, const double *coords_int, int64_t n_nodes,
                    int64_t n_elems, std::vector<int32_t> &eperm)
 {
-    (void)n_nodes;
     eperm.resize((size_t)n_elems);
     std::iota(eperm.begin(), eperm.end(), 0);
     if (method == 1) {  // by smallest node id
@@ -271,7 +292,27 @@ void element_order(int method, const int32_t *conn4, const double *coords_int, i
         std::sort(key.begin(), key.end());
         for (int64_t e = 0; e < n_elems; ++e)
             eperm[e] = key[e].second;
-    } else if (method == 2) {  // Morton order of centroids
+    } else if (method == 2) {  // Morton order of centroids on an element-size grid
+        // grid pitch per axis: the mean extent of an element's bounding box
+        // (a Kuhn tet spans exactly its cell, so the key is the cell index),
+        // anchored at the nodes' bounding-box corner
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, cell[3] = {0.0, 0.0, 0.0};
+        for (int64_t v = 0; v < n_nodes; ++v)
+            for (int c = 0; c < 3; ++c)
+                lo[c] = std::min(lo[c], coords_int[3 * v + c]);
+        for (int64_t e = 0; e < n_elems; ++e) {
+            const int32_t *q = conn4 + 4 * e;
+            for (int c = 0; c < 3; ++c) {
+                double a = coords_int[3 * q[0] + c], b = a;
+                for (int k = 1; k < 4; ++k) {
+                    a = std::min(a, coords_int[3 * q[k] + c]);
+                    b = std::max(b, coords_int[3 * q[k] + c]);
+                }
+                cell[c] += b - a;
+            }
+        }
+        for (int c = 0; c < 3; ++c)
+            cell[c] = n_elems ? cell[c] / (double)n_elems : 0.0;
         morton_order(
             n_elems,
             [&](int64_t e, double p[3]) {
@@ -280,7 +321,7 @@ void element_order(int method, const int32_t *conn4, const double *coords_int, i
                     p[c] = 0.25 * (coords_int[3 * q[0] + c] + coords_int[3 * q[1] + c] +
                                    coords_int[3 * q[2] + c] + coords_int[3 * q[3] + c]);
             },
-            eperm);
+            eperm, cell, lo);
     }
 }
 

@@ -167,3 +167,23 @@ def edge_star_patches(mesh, mode: str = "star"):
         seg = nodes[off[g]:off[g + 1]]
         out.append((int(seg[0]), int(seg[1]), [int(x) for x in seg[2:]], bool(closed[g])))
     return out
+
+
+def plan_layout(mesh, cfg=None) -> dict:
+    """Host-only dry run of the device upload (tal_plan_layout): renumbering,
+    element order, edge-star patches and CTA chunks for ``cfg`` (a RunConfig);
+    returns the chunking statistics without touching a GPU."""
+    from . import _native as N
+    from .assembly import RunConfig
+    cfg = cfg or RunConfig()
+    coords = np.ascontiguousarray(mesh.coords, dtype=np.float64)
+    conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int64)
+    o = N.TalMeshOpts()
+    check(lib().tal_default_mesh_opts(ctypes.byref(o)))
+    o.renumber, o.element_order = N.RENUMBER[cfg.renumber], N.EORDER[cfg.element_order]
+    o.cta_patches, o.chunk_nodes, o.patch_mode = cfg.cta_patches, cfg.chunk_nodes, N.PATCHES[cfg.patches]
+    inf = N.TalMeshInfo()
+    check(lib().tal_plan_layout(ptr(coords), ptr(conn), coords.shape[0], conn.shape[0],
+                                ctypes.byref(o), ctypes.byref(inf)))
+    return {k: getattr(inf, k) for k, _ in N.TalMeshInfo._fields_
+            if k not in ("n_colors", "device_bytes")}

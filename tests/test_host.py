@@ -224,3 +224,32 @@ def test_patches_on_permuted_and_perturbed_mesh():
     for mesh in (pm, sub):
         pt = _patch_tets(edge_star_patches(mesh, "star"))
         assert sorted(pt) == sorted(tuple(sorted(t)) for t in mesh.connectivity.tolist())
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 16), (24, 24, 24), (40, 20, 12)])
+def test_chunks_are_compact_cell_blocks(dims):
+    """Element Morton order on an element-size grid: every CTA chunk of a
+    Kuhn box is a full 8x4x4 block of cells (128 rings, 5*5*9 = 225 nodes),
+    also when the extents are not powers of two (160^3 measured 255 nodes per
+    chunk with a bounding-box-scaled Morton key)."""
+    from paper_2403_08777_b200.mesh import plan_layout
+    m = tb.generate_box_mesh(*dims)
+    info = plan_layout(m)
+    assert info["n_patches"] == m.n_elems // 6
+    assert info["n_chunks"] == info["n_patches"] // 128
+    assert info["n_chunk_nodes"] == 225 * info["n_chunks"]
+
+
+def test_plan_layout_general_mesh_and_errors():
+    from paper_2403_08777_b200.mesh import plan_layout
+    base = tb.generate_box_mesh(6, 5, 4)
+    pm = tb.permute_nodes(base, np.random.default_rng(3).permutation(base.n_nodes))
+    for cfg in (tb.RunConfig(), tb.RunConfig(renumber="sfc", element_order="node"),
+                tb.RunConfig(patches="tet", cta_patches=64, chunk_nodes=144)):
+        info = plan_layout(pm, cfg)
+        assert info["n_chunks"] >= 1 and info["n_chunk_nodes"] >= base.n_nodes
+    bad = tb.Mesh.__new__(tb.Mesh)
+    object.__setattr__(bad, "coords", base.coords)
+    object.__setattr__(bad, "connectivity", base.connectivity + base.n_nodes)
+    with pytest.raises(ValueError):
+        plan_layout(bad)
