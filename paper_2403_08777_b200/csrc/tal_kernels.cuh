@@ -205,6 +205,9 @@ constexpr int kRingUnroll = TAL_RING_UNROLL;
 #ifndef TAL_PREFETCH
 #define TAL_PREFETCH 0
 #endif
+#ifndef TAL_DIAG_NO_C
+#define TAL_DIAG_NO_C 0
+#endif
 template <>
 struct PrivCfg<1> {  // 128 patches / chunk
     static constexpr int THREADS = 128, NM = 256, NC = 1088, MINB = TAL_CFG1_MINB;
@@ -419,7 +422,11 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
         // phase C: one node per thread, nodes in rank order (contribution count
         // descending); its s-th contribution sits at lev[s] + q, so a warp
         // reads lane-contiguous addresses at every level
+#if TAL_DIAG_NO_C  // diagnostic build only (results wrong): cost of phase C
+        for (int q = tid; q < 0; q += T) {
+#else
         for (int q = tid; q < hdr.y; q += T) {
+#endif
             const int nr_ = run[q];
             double ax = 0.0, ay = 0.0, az = 0.0;
             for (int s = 0; s < nr_; ++s) {
