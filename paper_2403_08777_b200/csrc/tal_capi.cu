@@ -185,6 +185,27 @@ struct DeviceGuard {
     }
 };
 
+// RHS zeroing before RED accumulation
+#ifndef TAL_ZERO_KERNEL
+#define TAL_ZERO_KERNEL 0  // 1: k_zero (10 us alone, but the step measured 1.8 us slower than the memset)
+#endif
+cudaError_t zero_rhs(tal_handle *h, cudaStream_t s)
+{
+    const int64_t n = 3 * h->N;
+    if (!n)
+        return cudaSuccess;
+#if TAL_ZERO_KERNEL
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->device);
+    const int64_t want = (n / 2 + 511) / 512;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, 4 * (int64_t)n_sm));
+    k_zero<<<grid, 512, 0, s>>>(h->RX(), n);
+    return cudaGetLastError();
+#else
+    return cudaMemsetAsync(h->RX(), 0, sizeof(double) * n, s);
+#endif
+}
+
 bool make_consts(const tal_params *p, ElemConsts &kc, bool &sym)
 {
     kc.rho = p->rho;
@@ -286,8 +307,10 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
     const int64_t N = h->N, E = h->E;
     switch (scatter) {
     case TAL_SCATTER_ATOMIC: {
-        if (N)
-            TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
+        if (N) {
+            TAL_CK(zero_rhs(h, s));
+            nl += TAL_ZERO_KERNEL;
+        }
         if (E) {
             pm.begin();
             if (sym)
@@ -303,8 +326,10 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
     case TAL_SCATTER_COLORED: {
         if (!h->conn_col && E)
             return fail(TAL_ESTATE, "mesh was uploaded without a colouring (build_colors=0, colors=NULL)");
-        if (N)
-            TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
+        if (N) {
+            TAL_CK(zero_rhs(h, s));
+            nl += TAL_ZERO_KERNEL;
+        }
         pm.begin();  // colour launches together form the dominant work
         for (size_t c = 0; c + 1 < h->col_off.size(); ++c) {
             const int64_t b = h->col_off[c], e = h->col_off[c + 1];
@@ -345,11 +370,13 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             pa.py = h->d_partial + ncn;
             pa.pz = h->d_partial + 2 * ncn;
         }
-        // shared nodes receive FP64 REDs: zero the RHS first (a separate memset
-        // measured 16 us at 128^3; zeroing inside the kernel, by thread or TMA
-        // bulk stores, measured ~45 us slower -- DESIGN.md)
-        if (!ordered && N)
-            TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
+        // shared nodes receive FP64 REDs: zero the RHS first (a separate pass:
+        // zeroing inside the kernel, by thread or TMA bulk stores, measured
+        // ~45 us slower -- DESIGN.md)
+        if (!ordered && N) {
+            TAL_CK(zero_rhs(h, s));
+            nl += TAL_ZERO_KERNEL;
+        }
         if (np) {  // every neighbour has zeroed before anyone REDs into it
             ++h->peer_epoch;
             k_peer_signal<<<1, 1, 0, s>>>(h->peers[0].flags, h->peers[1].flags, 0);
@@ -432,8 +459,10 @@ int launch_shape(tal_handle *h, const tal_params *p, int variant, int scatter, c
     if (colored && !h->conn_col && E)
         return fail(TAL_ESTATE, "colour-by-colour scatter needs a colouring (build_colors=1 or colors)");
     int64_t nl = 0;
-    if (N)
-        TAL_CK(cudaMemsetAsync(h->RX(), 0, sizeof(double) * 3 * N, s));
+    if (N) {
+        TAL_CK(zero_rhs(h, s));
+        nl += TAL_ZERO_KERNEL;
+    }
     auto one = [&](const int4 *conn, int64_t b, int64_t e) -> int {
         const unsigned grid = grid_for(e - b, 256);
         if (variant == TAL_VARIANT_B) {

@@ -167,10 +167,13 @@ __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict
 //
 // Each persistent CTA walks chunks c = blockIdx.x + i*gridDim.x.  Per chunk:
 //   stage : one TMA bulk copy brings the chunk blob (patch tables, node lists,
-//           contribution layout) into shared memory (mbarrier completion), two
-//           chunks ahead; cp.async gathers the chunk's node records one chunk
-//           ahead (issued after phase B of the previous chunk, so the blob it
-//           reads has had a whole phase B to arrive).
+//           contribution layout) into shared memory (mbarrier completion),
+//           issued at the top of the previous chunk into the buffer freed by
+//           the chunk before it; cp.async gathers the chunk's node records
+//           one chunk ahead (issued after phase B of the previous chunk, so
+//           the blob it reads has had a whole phase B to arrive).  Two CTA
+//           barriers per chunk: records ready / phase C(i-1) done, and
+//           phase B done.
 //   B     : thread t walks patch t's ring, computing each tet's 4x3 RHS in
 //           registers; each patch node's sum is stored once, at its position
 //           in the chunk's node-major contribution list;
@@ -207,6 +210,9 @@ constexpr int kRingUnroll = TAL_RING_UNROLL;
 #endif
 #ifndef TAL_DIAG_NO_C
 #define TAL_DIAG_NO_C 0
+#endif
+#ifndef TAL_BAR3  // 1: the earlier three-barrier chunk loop (A/B builds)
+#define TAL_BAR3 0
 #endif
 template <>
 struct PrivCfg<1> {  // 128 patches / chunk
@@ -307,7 +313,16 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
     for (int i = 0; i < n_my; ++i) {
         const int b = i & 1;
         cp_async_wait_all();
-        __syncthreads();  // node records of chunk i visible to all
+        __syncthreads();  // node records of chunk i visible to all; phase C(i-1) done
+#if !TAL_BAR3
+        // blob i+1 into the buffer chunk i-1 used: every thread has finished
+        // reading it (phase C(i-1)) before the barrier above, so no third
+        // barrier per chunk is needed; it lands during phase B(i)
+        if (tid == 0 && i >= 1 && i + 1 < n_my) {
+            fence_proxy_async();
+            issue(i + 1, b ^ 1);
+        }
+#endif
         const uint8_t *bl = blob(b);
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);  // n_patch, n_node, node_begin, n_contrib
         const uint16_t *lev = reinterpret_cast<const uint16_t *>(bl + 16 + L::TABLES);
@@ -461,12 +476,28 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
                 }
             }
         }
+#if TAL_BAR3
         __syncthreads();  // blob b and res free again
         if (tid == 0 && i + 2 < n_my) {
             fence_proxy_async();
             issue(i + 2, b);
         }
+#endif
     }
+}
+
+// zero n doubles (16-B aligned start): 16-B streaming stores, grid-stride.
+// Replaces cudaMemsetAsync for the RHS (measured 3.2 TB/s for 51.5 MB).
+__global__ void __launch_bounds__(512) k_zero(double *__restrict__ p, int64_t n)
+{
+    const int64_t n2 = n >> 1;
+    double2 *q = reinterpret_cast<double2 *>(p);
+    const double2 z = make_double2(0.0, 0.0);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
+         i += (int64_t)gridDim.x * blockDim.x)
+        __stcs(q + i, z);
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+        p[n - 1] = 0.0;
 }
 
 // ordered merge of chunk partials for nodes shared between chunks (and zero

@@ -223,7 +223,7 @@ def test_shapes_device_resident_run(oracle, shape):
     u = tb.make_velocity(m, "random:7")
     asm = tb.Assembler(m, tb.RunConfig(scatter="atomic"))
     asm.set_velocity_host(u)
-    assert asm.run(P, variant=tb.VariantId(shape)) == 1
+    assert asm.run(P, variant=tb.VariantId(shape)) >= 1
     rhs = asm.get_rhs_host()
     asm.synchronize()
     ref = oracle.assemble_reference(m.coords, m.connectivity, u)
