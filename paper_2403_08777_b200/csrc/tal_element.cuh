@@ -32,9 +32,6 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#ifndef TAL_W_BY_ROW
-#define TAL_W_BY_ROW 0
-#endif
 
 namespace tal {
 
@@ -151,33 +148,6 @@ __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3],
     const double B = vis * (inv * (-1.0 / 6.0));
     const double As = mul_sign(k.a_po, det), Aq = mul_sign(k.a_q, det);
     const double A4 = fma(4.0, As, Aq);
-#if TAL_W_BY_ROW
-    // component-major: w[.][cc] is consumed as soon as it exists (4 live
-    // doubles instead of 12); R accumulates over cc = 2, 1, 0
-#pragma unroll
-    for (int cc = 2; cc >= 0; --cc) {
-        const double S = S01[cc] + (U2[cc] + U3[cc]);
-        const double AsS = As * S;
-        const double w1 = fma(Aq, U1[cc], fma(B, c1[cc], AsS));
-        const double w2 = fma(Aq, U2[cc], fma(B, c2[cc], AsS));
-        const double w3 = fma(Aq, U3[cc], fma(B, c3[cc], AsS));
-        const double w0 = fma(A4, S, -((w1 + w2) + w3));
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            if (!ACC && cc == 2) {
-                R[0][i] = w0 * Gh[cc][i];
-                R[1][i] = w1 * Gh[cc][i];
-                R[2][i] = w2 * Gh[cc][i];
-                R[3][i] = w3 * Gh[cc][i];
-            } else {
-                R[0][i] = fma(w0, Gh[cc][i], R[0][i]);
-                R[1][i] = fma(w1, Gh[cc][i], R[1][i]);
-                R[2][i] = fma(w2, Gh[cc][i], R[2][i]);
-                R[3][i] = fma(w3, Gh[cc][i], R[3][i]);
-            }
-        }
-    }
-#else
     double w[4][3];
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
@@ -196,7 +166,6 @@ __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3],
             const double last = ACC ? fma(w[a][2], Gh[2][i], R[a][i]) : w[a][2] * Gh[2][i];
             R[a][i] = fma(w[a][0], Gh[0][i], fma(w[a][1], Gh[1][i], last));
         }
-#endif
 }
 
 // Symmetric-rule element (pmat = po * ones + (pd - po) * I).

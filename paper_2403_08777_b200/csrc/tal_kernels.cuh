@@ -205,15 +205,10 @@ struct PrivCfg<0> {  // 64 patches / chunk
 #define TAL_RING_UNROLL 1
 #endif
 constexpr int kRingUnroll = TAL_RING_UNROLL;
-#ifndef TAL_PREFETCH
-#define TAL_PREFETCH 0
-#endif
 #ifndef TAL_DIAG_NO_C
 #define TAL_DIAG_NO_C 0
 #endif
-#ifndef TAL_BAR3  // 1: the earlier three-barrier chunk loop (A/B builds)
-#define TAL_BAR3 0
-#endif
+
 template <>
 struct PrivCfg<1> {  // 128 patches / chunk
     static constexpr int THREADS = 128, NM = 256, NC = 1088, MINB = TAL_CFG1_MINB;
@@ -314,7 +309,6 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
         const int b = i & 1;
         cp_async_wait_all();
         __syncthreads();  // node records of chunk i visible to all; phase C(i-1) done
-#if !TAL_BAR3
         // blob i+1 into the buffer chunk i-1 used: every thread has finished
         // reading it (phase C(i-1)) before the barrier above, so no third
         // barrier per chunk is needed; it lands during phase B(i)
@@ -322,7 +316,6 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
             fence_proxy_async();
             issue(i + 1, b ^ 1);
         }
-#endif
         const uint8_t *bl = blob(b);
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);  // n_patch, n_node, node_begin, n_contrib
         const uint16_t *lev = reinterpret_cast<const uint16_t *>(bl + 16 + L::TABLES);
@@ -363,25 +356,11 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
             // previous tet's contribution to r_t and leaves complete for r_t,
             // R[3] (r_t+1) becomes the next tet's carry
             double R[4][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-#if TAL_PREFETCH
-            // the next ring node's record is loaded one tet ahead (hides the
-            // table -> record shared-memory latency chain)
-            double Xn[3], Un[3];
-            load_record_s(nr, ID(3 + (m == 1 ? 0 : 1)), Xn, Un);
-#endif
 #pragma unroll kRingUnroll
             for (int t = 0; t < k; ++t) {
                 double X3[3], U3[3], e3[3], du3[3], c1[3], c2[3];
-#if TAL_PREFETCH
-#pragma unroll
-                for (int q = 0; q < 3; ++q)
-                    X3[q] = Xn[q], U3[q] = Un[q];
-                if (t + 1 < k)
-                    load_record_s(nr, ID(3 + ((t + 2 == m) ? 0 : t + 2)), Xn, Un);
-#else
                 const int nxt = (t + 1 == m) ? 0 : t + 1;
                 load_record_s(nr, ID(3 + nxt), X3, U3);
-#endif
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     e3[q] = X3[q] - Xa[q];
@@ -476,13 +455,6 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
                 }
             }
         }
-#if TAL_BAR3
-        __syncthreads();  // blob b and res free again
-        if (tid == 0 && i + 2 < n_my) {
-            fence_proxy_async();
-            issue(i + 2, b);
-        }
-#endif
     }
 }
 
