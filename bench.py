@@ -444,7 +444,11 @@ def run_ours(a) -> None:
                    "permuted": bool(a.permute), "variant": a.variant,
                    "l2": "flushed (256 MiB write) before every step, outside the timed events"
                          if flush_buf is not None else "not flushed",
-                   "parallelism": f"dp{ws} z-slabs" if ws > 1 else "single GPU"},
+                   "parallelism": f"dp{ws} z-slabs" if ws > 1 else "single GPU",
+                   "interface_sum": None if dom is None else (
+                       "fused: assembly kernel REDs into the neighbours' RHS (CUDA IPC peer memory)"
+                       if dom.fused else "exchange: NCCL send/recv of the interface planes + halo add"
+                       + (f" (fused unavailable: {dom.fused_error})" if dom.fused_error else ""))},
         "roofline": {"bound": "fp64", "kernel": kname, "achieved": tf, "peak": fp64_tf,
                      "unit": "TFLOP/s", "frac": tf / fp64_tf,
                      "peak_source": "live DFMA probe in this run (tal_fp64_peak: ~0.5 ms "

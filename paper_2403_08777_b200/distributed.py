@@ -185,29 +185,46 @@ class SlabDomain:
         self.assembler = Assembler(self.mesh, self.cfg, external_nodes=ext)
         dev = torch.device("cuda", self.cfg.device)
         self._lists, self._send, self._recv = {}, {}, {}
+        self.fused_error = None
         if self.fused:
-            self._connect_peers(ifaces)
-            return
+            if self._connect_peers(ifaces):
+                return
+            # a rank could not map its neighbours' memory (no P2P / IPC on
+            # this system): every rank switches to the NCCL exchange path;
+            # the external (interface) nodes are REDed either way
+            self.fused = False
         for nbr, ids in ifaces.items():
             internal = self.assembler.map_nodes(ids)
             self._lists[nbr] = torch.as_tensor(internal, device=dev)
             self._send[nbr] = torch.empty((ids.size, 3), dtype=torch.float64, device=dev)
             self._recv[nbr] = torch.empty((ids.size, 3), dtype=torch.float64, device=dev)
 
-    def _connect_peers(self, ifaces) -> None:
+    def _connect_peers(self, ifaces) -> bool:
         """Exchange IPC handles and interface internal ids with the neighbours
-        (host objects over torch.distributed), then open the peer mappings."""
+        (host objects over torch.distributed), then open the peer mappings.
+        Returns whether EVERY rank succeeded (a collective decision)."""
         import torch.distributed as dist
         asm = self.assembler
         rh, off, fh = asm.peer_export()
         mine = {nbr: asm.map_nodes(ids) for nbr, ids in ifaces.items()}
         info = [None] * self.part.world
         dist.all_gather_object(info, (rh, off, fh, asm.n_nodes, mine))
-        for nbr, ids in ifaces.items():
-            prh, poff, pfh, pn, pmap = info[nbr]
-            slot = 0 if nbr < self.part.rank else 1
-            asm.peer_open(slot, prh, poff, pfh, pn, ids, pmap[self.part.rank])
+        ok = True
+        try:
+            for nbr, ids in ifaces.items():
+                prh, poff, pfh, pn, pmap = info[nbr]
+                slot = 0 if nbr < self.part.rank else 1
+                asm.peer_open(slot, prh, poff, pfh, pn, ids, pmap[self.part.rank])
+        except RuntimeError as err:
+            ok, self.fused_error = False, str(err)
+        votes = [None] * self.part.world
+        dist.all_gather_object(votes, ok)
+        if not all(votes):
+            if ok:
+                asm.peer_detach()
+            return False
         dist.barrier()
+        return True
 
     def velocity(self, spec: str) -> np.ndarray:
         u = self.part.velocity(spec, self.mesh)
