@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--permute", action="store_true", help="config 3: random node permutation")
+    ap.add_argument("--pressure", action="store_true",
+                    help="add the P1 pressure-gradient term (extension; uniform [-1,1) nodal p, seed 2)")
     ap.add_argument("--check", action="store_true",
                     help="N>1: gather the owned RHS rows to rank 0 and check them against the oracle")
     return ap.parse_args()
@@ -251,6 +253,10 @@ def run_ours(a) -> None:
             variant is not tb.VariantId.RSP and a.scatter == "private")))
     prep_s = time.perf_counter() - t0
     info = asm.info()
+    press = None
+    if a.pressure:
+        press = np.random.default_rng(2).uniform(-1.0, 1.0, mesh.n_nodes)
+        asm.set_pressure(press)
     E, Nn = mesh.n_elems, mesh.n_nodes
 
     stream = torch.cuda.current_stream().cuda_stream
@@ -279,6 +285,8 @@ def run_ours(a) -> None:
         cpu_baseline = {"value": E / med, "unit": "elem/s", "cores": T, "kind": "port",
                         "sample": f"full {c}^3 mesh ({E} tets), {a.init}; C port of the reference "
                                   f"numba kernel + private driver, 1 warm-up + median of 3"}
+        if press is not None:
+            ref = ref + O.pressure_gradient(mesh.coords, mesh.connectivity, press)
         chk = O.compare(rhs_gpu, ref, mesh.coords, mesh.connectivity, u)
         parity = {"reference_rel_diff": chk.rel_diff, "rel_l2": chk.rel_l2,
                   "entry_rel": chk.entry_rel, "passed": bool(chk.passed)}
@@ -442,6 +450,7 @@ def run_ours(a) -> None:
                    "renumber": a.renumber, "element_order": a.element_order,
                    "patches": a.patches, "cta_patches": a.cta_patches, "chunk_nodes": a.chunk_nodes,
                    "permuted": bool(a.permute), "variant": a.variant,
+                   "pressure_term": bool(a.pressure),
                    "l2": "flushed (256 MiB write) before every step, outside the timed events"
                          if flush_buf is not None else "not flushed",
                    "parallelism": f"dp{ws} z-slabs" if ws > 1 else "single GPU",

@@ -182,6 +182,14 @@ int tal_set_velocity_host(tal_handle *h, const double *u, void *stream);
 int tal_set_velocity_device(tal_handle *h, const double *d_u, void *stream);
 int tal_run(tal_handle *h, const tal_params *p, int scatter, void *stream,
             int64_t *kernel_launches);
+/* Optional P1 pressure-gradient term r_a += int p dN_a/dx_i (SURVEY.md section
+ * 8 f4; NOT part of the reference operator, kernel.py:7-10 -- its parity is
+ * pinned by this repo's own oracle only).  p: (n_nodes,) f64 in caller
+ * numbering, host or device; NULL switches the term off again.  Applies to
+ * every later assembly of the RSP shape on this handle (B/RS: TAL_EINVAL). */
+int tal_set_pressure_host(tal_handle *h, const double *p, void *stream);
+int tal_set_pressure_device(tal_handle *h, const double *d_p, void *stream);
+
 /* tal_run for any code shape (TAL_VARIANT_*) */
 int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter,
                     void *stream, int64_t *kernel_launches);

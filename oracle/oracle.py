@@ -20,6 +20,11 @@ Contents (each a restatement of the reference package tet-assembly-lab
 
 Parity of the restatement is pinned against ``tests/golden/*.npz``, which
 ``oracle/gen_golden.py`` produced by importing the reference itself.
+
+Exception -- parity UNPINNED: ``pressure_gradient``
+has no counterpart in the reference (its operator has no pressure term,
+kernel.py:7-10); it is restated here from the weak form and
+checked only against closed-form answers (tests/test_pressure.py).
 """
 
 from __future__ import annotations
@@ -198,6 +203,29 @@ def assemble_reference(coords, conn, u, rho=1.0, mu=1e-3, cvre=0.07) -> np.ndarr
     rhs = np.empty((coords.shape[0], 3))
     lib().orc_assemble_reference(_p(coords), _p(conn), _p(u), rho, mu, cvre,
                                  coords.shape[0], conn.shape[0], _p(rhs))
+    return rhs
+
+
+def pressure_gradient(coords, conn, p) -> np.ndarray:
+    """r_a[i] = sum over tets of int_T p dN_a/dx_i dV for P1 p (parity
+    unpinned, see the module header): per tet vol * mean(p) * dN_a/dx_i, with
+    dN_a/dx_i = c_a[i] / det from the cofactor rows (mesh.py:187-218 form)."""
+    coords = np.asarray(coords, dtype=np.float64)
+    conn = np.asarray(conn, dtype=np.int64)
+    p = np.asarray(p, dtype=np.float64)
+    rhs = np.zeros((coords.shape[0], 3))
+    if conn.shape[0] == 0:
+        return rhs
+    x = coords[conn]
+    e1, e2, e3 = x[:, 1] - x[:, 0], x[:, 2] - x[:, 0], x[:, 3] - x[:, 0]
+    c = np.stack([np.cross(e2, e3), np.cross(e3, e1), np.cross(e1, e2)], axis=1)  # (E,3,3)
+    det = np.einsum("ek,ek->e", e1, c[:, 0])
+    grad = np.concatenate([-c.sum(axis=1, keepdims=True), c], axis=1) / det[:, None, None]
+    vol = np.abs(det) / 6.0
+    pbar = p[conn].mean(axis=1)
+    contrib = (vol * pbar)[:, None, None] * grad  # (E, 4, 3)
+    for a in range(4):
+        np.add.at(rhs, conn[:, a], contrib[:, a])
     return rhs
 
 

@@ -89,6 +89,8 @@ SIGNATURES = [
     ("tal_wait", _I, [_P, _I64]),
     ("tal_buffers_get", _I, [_P, ctypes.POINTER(TalBuffers)]),
     ("tal_set_velocity_host", _I, [_P, _P, _P]),
+    ("tal_set_pressure_host", _I, [_P, _P, _P]),
+    ("tal_set_pressure_device", _I, [_P, _P, _P]),
     ("tal_set_velocity_device", _I, [_P, _P, _P]),
     ("tal_run", _I, [_P, ctypes.POINTER(TalParams), _I, _P, ctypes.POINTER(_I64)]),
     ("tal_get_rhs_host", _I, [_P, _P, _P]),

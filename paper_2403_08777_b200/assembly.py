@@ -368,6 +368,25 @@ class Assembler:
         out.update({k: torch.as_tensor(_CudaView(b[k], (n,)), device=dev) for k in ("rx", "ry", "rz")})
         return out
 
+    def set_pressure(self, p: Optional[np.ndarray], stream=None) -> None:
+        """Nodal pressure (n_nodes,) for the optional pressure-gradient term
+        (tal_set_pressure_host, not part of the
+        reference operator); None switches the term off.  Applies to every
+        later RSP-shape assembly on this handle."""
+        if p is None:
+            N.check(N.lib().tal_set_pressure_host(self._h, None, _stream(stream)))
+            return
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        if p.shape != (self.n_nodes,):
+            raise ValueError(f"pressure must have shape ({self.n_nodes},), got {p.shape}")
+        if not np.isfinite(p).all():
+            raise ValueError("pressure contains non-finite entries")
+        N.check(N.lib().tal_set_pressure_host(self._h, N.ptr(p), _stream(stream)))
+
+    def set_pressure_device(self, d_p_ptr: Optional[int], stream=None) -> None:
+        N.check(N.lib().tal_set_pressure_device(
+            self._h, None if d_p_ptr is None else ctypes.c_void_p(d_p_ptr), _stream(stream)))
+
     def set_velocity_host(self, u: np.ndarray, stream=None) -> None:
         u = np.ascontiguousarray(u, dtype=np.float64)
         if u.shape != (self.n_nodes, 3):
@@ -510,12 +529,19 @@ def clear_cache() -> None:
 
 
 def _assemble_variant(variant: VariantId, mesh, u, params: PhysParams,
-                      cfg: Optional[RunConfig]) -> AssemblyResult:
+                      cfg: Optional[RunConfig], pressure: Optional[np.ndarray] = None) -> AssemblyResult:
     cfg = cfg or RunConfig()
     u = validate_velocity(mesh, u)
     asm = _cached_assembler(mesh, cfg, variant)
     rhs = np.empty((asm.n_nodes, 3))
-    t = asm.assemble_into(u, params, rhs, cfg.scatter, variant=variant)
+    if pressure is None:
+        t = asm.assemble_into(u, params, rhs, cfg.scatter, variant=variant)
+    else:
+        asm.set_pressure(pressure)
+        try:
+            t = asm.assemble_into(u, params, rhs, cfg.scatter, variant=variant)
+        finally:
+            asm.set_pressure(None)
     wall = t.total_ms * 1e-3
     rate = asm.n_elems / wall if wall > 0.0 else 0.0
     return AssemblyResult(rhs=rhs, ledger=make_ledger(variant, cfg), wall_time=wall,
@@ -523,14 +549,17 @@ def _assemble_variant(variant: VariantId, mesh, u, params: PhysParams,
 
 
 def assemble_rsp(mesh, u: np.ndarray, params: PhysParams,
-                 cfg: Optional[RunConfig] = None) -> AssemblyResult:
+                 cfg: Optional[RunConfig] = None, pressure: Optional[np.ndarray] = None) -> AssemblyResult:
     """Drop-in for ``tet_assembly_lab.assemble_rsp`` (variants.py:553-616).
 
     ``wall_time`` is the CUDA-event time of the call's device timeline
     (velocity H2D + layout pack + assembly kernels + unpack + RHS D2H); the
     one-time mesh upload is excluded like the reference's colouring.
+    ``pressure`` (n_nodes,) adds the P1 pressure-gradient term
+    ``int p dN_a/dx_i`` -- an extension with no reference counterpart
+    (parity pinned only by this repo's oracle).
     """
-    return _assemble_variant(VariantId.RSP, mesh, u, params, cfg)
+    return _assemble_variant(VariantId.RSP, mesh, u, params, cfg, pressure)
 
 
 def assemble_baseline(mesh, u: np.ndarray, params: PhysParams,

@@ -94,7 +94,10 @@ struct tal_handle {
     int32_t *d_blob_off = nullptr;
     int32_t *d_bnd_nodes = nullptr, *d_bnd_off = nullptr, *d_bnd_pos = nullptr;
     double *d_partial = nullptr;  // 3 * n_chunk_nodes
-    int priv_grid = 0, priv_cfg = 1;
+    int priv_grid = 0, priv_grid_pr = 0, priv_cfg = 1;
+    // optional nodal pressure (internal order) for the pressure-gradient term
+    double *d_press = nullptr;
+    bool has_press = false;
     // fused interface sum with up to two neighbours (domain decomposition)
     struct Peer {
         double *rx = nullptr;              // neighbour's RHS x (y, z follow at +n, +2n)
@@ -144,11 +147,12 @@ struct tal_handle {
     {
         free_peers();
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
-                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial};
+                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press};
         for (void *p : ptrs)
             if (p)
                 cudaFree(p);
-        nodebuf = staging = d_partial = nullptr;
+        nodebuf = staging = d_partial = d_press = nullptr;
+        has_press = false;
         for (int s = 0; s < ASYNC_SLOTS; ++s) {
             if (astage_u[s])
                 cudaFree(astage_u[s]);
@@ -253,12 +257,16 @@ template <int CFG>
 cudaError_t launch_private_cfg(bool ordered, unsigned grid, cudaStream_t s, PrivArgs pa, const double *nodes,
                                RhsSoA rhs, ElemConsts kc, PeerArgs peer)
 {
-    constexpr size_t sm = PrivLayoutOf<CFG>::TOTAL;
+    const bool pr = pa.press != nullptr;
+    const size_t sm = pr ? PrivLayoutOf<CFG, true>::TOTAL : PrivLayoutOf<CFG>::TOTAL;
     constexpr int T = PrivCfg<CFG>::THREADS;
     void *args[] = {(void *)&pa, (void *)&nodes, (void *)&rhs, (void *)&kc, (void *)&peer};
-    const void *fn = ordered   ? (const void *)k_assemble_private<CFG, true>
-                     : peer.pidx ? (const void *)k_assemble_private<CFG, false, true>
-                                    : (const void *)k_assemble_private<CFG, false>;
+    const void *fn = ordered   ? (pr ? (const void *)k_assemble_private<CFG, true, false, true>
+                                     : (const void *)k_assemble_private<CFG, true>)
+                     : peer.pidx ? (pr ? (const void *)k_assemble_private<CFG, false, true, true>
+                                       : (const void *)k_assemble_private<CFG, false, true>)
+                                 : (pr ? (const void *)k_assemble_private<CFG, false, false, true>
+                                       : (const void *)k_assemble_private<CFG, false>);
     // plain launch of a persistent grid (occupancy x SMs); no grid-wide barrier
     // is used, so CTAs that cannot be resident yet simply start later
     return cudaLaunchKernel(fn, dim3(grid), dim3(T), args, sm, s);
@@ -313,10 +321,14 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         }
         if (E) {
             pm.begin();
+            const double *pr = h->has_press ? h->d_press : nullptr;
+            const unsigned g = grid_for(E, 256);
             if (sym)
-                k_assemble_atomic<true><<<grid_for(E, 256), 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc);
+                pr ? k_assemble_atomic<true, true><<<g, 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc, pr)
+                   : k_assemble_atomic<true><<<g, 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc, nullptr);
             else
-                k_assemble_atomic<false><<<grid_for(E, 256), 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc);
+                pr ? k_assemble_atomic<false, true><<<g, 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc, pr)
+                   : k_assemble_atomic<false><<<g, 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc, nullptr);
             pm.end();
             TAL_CK_LAUNCH();
             ++nl;
@@ -335,10 +347,14 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             const int64_t b = h->col_off[c], e = h->col_off[c + 1];
             if (e <= b)
                 continue;
+            const double *pr = h->has_press ? h->d_press : nullptr;
+            const unsigned g = grid_for(e - b, 256);
             if (sym)
-                k_assemble_colored<true><<<grid_for(e - b, 256), 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc);
+                pr ? k_assemble_colored<true, true><<<g, 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc, pr)
+                   : k_assemble_colored<true><<<g, 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc, nullptr);
             else
-                k_assemble_colored<false><<<grid_for(e - b, 256), 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc);
+                pr ? k_assemble_colored<false, true><<<g, 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc, pr)
+                   : k_assemble_colored<false><<<g, 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc, nullptr);
             TAL_CK_LAUNCH();
             ++nl;
         }
@@ -351,7 +367,8 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             return launch_run(h, p, TAL_SCATTER_ATOMIC, s, launches);
         const bool ordered = scatter == TAL_SCATTER_PRIVATE;
         const int64_t ncn = (int64_t)h->ch.cnodes.size();
-        PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr, nullptr, nullptr};
+        PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr, nullptr, nullptr,
+                    h->has_press ? h->d_press : nullptr};
         PeerArgs peer{};
         const int np = h->n_peers();
         if (np && ordered)
@@ -385,7 +402,8 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             nl += 2;
         }
         if (h->info.n_chunks) {
-            const unsigned grid = (unsigned)std::min<int64_t>(h->priv_grid, h->info.n_chunks);
+            const unsigned grid =
+                (unsigned)std::min<int64_t>(pa.press ? h->priv_grid_pr : h->priv_grid, h->info.n_chunks);
             pm.begin();
             const cudaError_t le = launch_private(h->priv_cfg, ordered, grid, s, pa, nodes, rhs, kc, peer);
             pm.end();
@@ -502,32 +520,41 @@ int launch_any(tal_handle *h, const tal_params *p, int variant, int scatter, cud
 {
     if (variant == TAL_VARIANT_RSP)
         return launch_run(h, p, scatter, s, launches);
+    if (h->has_press && (variant == TAL_VARIANT_B || variant == TAL_VARIANT_RS))
+        return fail(TAL_EINVAL, "the pressure-gradient term is implemented for the RSP shape only");
     if (variant == TAL_VARIANT_B || variant == TAL_VARIANT_RS)
         return launch_shape(h, p, variant, scatter, s, launches);
     return fail(TAL_EINVAL, "unknown variant " + std::to_string(variant));
 }
 
 template <int CFG>
-int set_attrs_cfg(int device, int *grid_out)
+int set_attrs_cfg(int device, int *grid_out, int *grid_pr_out)
 {
-    constexpr int sm = PrivLayoutOf<CFG>::TOTAL;
+    constexpr int sm = PrivLayoutOf<CFG>::TOTAL, sm_pr = PrivLayoutOf<CFG, true>::TOTAL;
     const void *fns[] = {(const void *)k_assemble_private<CFG, true>,
                          (const void *)k_assemble_private<CFG, false>,
                          (const void *)k_assemble_private<CFG, false, true>};
+    const void *fns_pr[] = {(const void *)k_assemble_private<CFG, true, false, true>,
+                            (const void *)k_assemble_private<CFG, false, false, true>,
+                            (const void *)k_assemble_private<CFG, false, true, true>};
     for (const void *f : fns)
         TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    int per_sm = 0, n_sm = 0;
+    for (const void *f : fns_pr)
+        TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_pr));
+    int per_sm = 0, per_sm_pr = 0, n_sm = 0;
     TAL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[1], PrivCfg<CFG>::THREADS, sm));
+    TAL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_pr, fns_pr[1], PrivCfg<CFG>::THREADS, sm_pr));
     TAL_CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
     *grid_out = std::max(1, per_sm) * n_sm;
+    *grid_pr_out = std::max(1, per_sm_pr) * n_sm;
     return TAL_OK;
 }
 
-int set_kernel_attrs(int device, int cfg, int *grid_out)
+int set_kernel_attrs(int device, int cfg, int *grid_out, int *grid_pr_out)
 {
-    return cfg == 0   ? set_attrs_cfg<0>(device, grid_out)
-           : cfg == 1 ? set_attrs_cfg<1>(device, grid_out)
-                      : set_attrs_cfg<2>(device, grid_out);
+    return cfg == 0   ? set_attrs_cfg<0>(device, grid_out, grid_pr_out)
+           : cfg == 1 ? set_attrs_cfg<1>(device, grid_out, grid_pr_out)
+                      : set_attrs_cfg<2>(device, grid_out, grid_pr_out);
 }
 
 // cta_patches -> CTA configuration (PrivCfg in tal_kernels.cuh)
@@ -871,7 +898,7 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
         TAL_CK(cudaMalloc((void **)&h->d_partial, sizeof(double) * 3 * C.cnodes.size()));
     bytes += blobs.size() + blob_off.size() * 4 + C.cnodes.size() * 24 +
              (C.bnd_nodes.size() + C.bnd_off.size() + C.bnd_pos.size()) * 4;
-    if ((rc = set_kernel_attrs(h->device, h->priv_cfg, &h->priv_grid)))
+    if ((rc = set_kernel_attrs(h->device, h->priv_cfg, &h->priv_grid, &h->priv_grid_pr)))
         return rc;
     TAL_CK(cudaDeviceSynchronize());
 
@@ -957,6 +984,47 @@ int tal_set_velocity_device(tal_handle *h, const double *d_u, void *stream)
         TAL_CK_LAUNCH();
     }
     return TAL_OK;
+}
+
+int tal_set_pressure_device(tal_handle *h, const double *d_p, void *stream)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    DeviceGuard g(h->device);
+    if (!d_p) {
+        h->has_press = false;
+        return TAL_OK;
+    }
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    if (!h->d_press)
+        TAL_CK(cudaMalloc((void **)&h->d_press, sizeof(double) * std::max<int64_t>(h->N, 1)));
+    if (h->N) {
+        k_pack_scalar<<<grid_for(h->N, 256), 256, 0, s>>>(d_p, h->perm, h->N, h->d_press);
+        TAL_CK_LAUNCH();
+    }
+    h->has_press = true;
+    return TAL_OK;
+}
+
+int tal_set_pressure_host(tal_handle *h, const double *p, void *stream)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    if (!p)
+        return tal_set_pressure_device(h, nullptr, stream);
+    DeviceGuard g(h->device);
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    // the staging buffer (3N doubles) is free between calls on this stream
+    if (h->N)
+        TAL_CK(cudaMemcpyAsync(h->staging, p, sizeof(double) * h->N, cudaMemcpyHostToDevice, s));
+    int rc = tal_set_pressure_device(h, h->staging, s);
+    if (rc == TAL_OK)
+        TAL_CK(cudaStreamSynchronize(s));  // staging is reused by the next host call
+    return rc;
 }
 
 int tal_set_velocity_host(tal_handle *h, const double *u, void *stream)
@@ -1225,9 +1293,9 @@ int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
         const double *nodes = buf;
         RhsSoA r{buf + 6 * n_nodes, buf + 7 * n_nodes, buf + 8 * n_nodes};
         if (sym)
-            k_assemble_atomic<true><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc);
+            k_assemble_atomic<true><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc, nullptr);
         else
-            k_assemble_atomic<false><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc);
+            k_assemble_atomic<false><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc, nullptr);
         if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
             rc = fail(TAL_ECUDA, std::string("assemble_elements kernel: ") + cudaGetErrorString(e));
             break;

@@ -98,6 +98,24 @@ __device__ __forceinline__ double mul_sign(double x, double s)
                                 (__double_as_longlong(s) & (long long)0x8000000000000000ULL));
 }
 
+// Optional P1 pressure-gradient term (absent from the
+// reference operator, so its parity is pinned only by this repo's own oracle):
+//   r_a[i] += int p dN_a/dx_i dV = vol * pbar * c_a[i] / D = sgn(D) pbar / 6 c_a[i]
+// (weak form of -grad p without the boundary term; pbar = mean nodal pressure,
+// exact for P1 p).  c_0 = -(c_1 + c_2 + c_3).  15 FP64 instructions.
+__device__ __forceinline__ void pressure_add(double pbar, double det, const double c1[3],
+                                             const double c2[3], const double c3[3], double R[4][3])
+{
+    const double P = mul_sign(pbar * (1.0 / 6.0), det);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        R[1][i] = fma(P, c1[i], R[1][i]);
+        R[2][i] = fma(P, c2[i], R[2][i]);
+        R[3][i] = fma(P, c3[i], R[3][i]);
+        R[0][i] = fma(-P, (c1[i] + c2[i]) + c3[i], R[0][i]);
+    }
+}
+
 // Everything after the cofactor rows: velocity gradient, Vreman, the two
 // weighted terms.  c[1..3] = cofactor rows, D = det, du[b] = u_b - u_0
 // (b = 1..3), U = the four corner velocities.  R = 4x3 element RHS; with
@@ -168,9 +186,10 @@ __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3],
         }
 }
 
-// Symmetric-rule element (pmat = po * ones + (pd - po) * I).
+// Symmetric-rule element (pmat = po * ones + (pd - po) * I); p4 = nodal
+// pressures or nullptr.
 __device__ __forceinline__ void element_rhs_sym(const double X[4][3], const double U[4][3],
-                                                const ElemConsts &k, double R[4][3])
+                                                const double *p4, const ElemConsts &k, double R[4][3])
 {
     double e[3][3], du[3][3], c1[3], c2[3], c3[3];
 #pragma unroll
@@ -186,13 +205,15 @@ __device__ __forceinline__ void element_rhs_sym(const double X[4][3], const doub
     const double det = fma(e[0][0], c1[0], fma(e[0][1], c1[1], e[0][2] * c1[2]));
     const double S01[3] = {U[0][0] + U[1][0], U[0][1] + U[1][1], U[0][2] + U[1][2]};
     tet_tail<false>(c1, c2, c3, det, du[0], du[1], du[2], U[0], U[1], S01, U[2], U[3], k, R);
+    if (p4)
+        pressure_add(0.25 * ((p4[0] + p4[1]) + (p4[2] + p4[3])), det, c1, c2, c3, R);
 }
 
 // Geometry + gradient + Vreman for the general-pmat element: cofactor rows
 // cf[1..3], the unscaled gradient Gh, sgn(D) and B = -vis / (6 |D|).
 __device__ __forceinline__ void element_core(const double X[4][3], const double U[4][3],
                                              const ElemConsts &k, double cf[4][3],
-                                             double Gh[3][3], double &sg, double &B)
+                                             double Gh[3][3], double &sg, double &B, double &det_out)
 {
     double e[3][3], du[3][3];
 #pragma unroll
@@ -206,6 +227,7 @@ __device__ __forceinline__ void element_core(const double X[4][3], const double 
     cross3(e[2], e[0], cf[2]);
     cross3(e[0], e[1], cf[3]);
     const double det = fma(e[0][0], cf[1][0], fma(e[0][1], cf[1][1], e[0][2] * cf[1][2]));
+    det_out = det;
     const double ad = fabs(det);
     sg = (det < 0.0) ? -1.0 : 1.0;
     const double r3 = rcbrt(ad);
@@ -247,10 +269,10 @@ __device__ __forceinline__ void rhs_rows(const double w[4][3], const double Gh[3
 
 // General pmat (any 4x4 interpolation table): m_a = sum_b pmat[a][b] u_b.
 __device__ __forceinline__ void element_rhs_gen(const double X[4][3], const double U[4][3],
-                                                const ElemConsts &k, double R[4][3])
+                                                const double *p4, const ElemConsts &k, double R[4][3])
 {
-    double cf[4][3], Gh[3][3], sg, B;
-    element_core(X, U, k, cf, Gh, sg, B);
+    double cf[4][3], Gh[3][3], sg, B, det;
+    element_core(X, U, k, cf, Gh, sg, B, det);
 #pragma unroll
     for (int c = 0; c < 3; ++c)
         cf[0][c] = -(cf[1][c] + cf[2][c] + cf[3][c]);
@@ -266,16 +288,18 @@ __device__ __forceinline__ void element_rhs_gen(const double X[4][3], const doub
             w[a][c] = fma(A, m, B * cf[a][c]);
         }
     rhs_rows(w, Gh, R);
+    if (p4)
+        pressure_add(0.25 * ((p4[0] + p4[1]) + (p4[2] + p4[3])), det, cf[1], cf[2], cf[3], R);
 }
 
 template <bool SYM>
 __device__ __forceinline__ void element_rhs(const double X[4][3], const double U[4][3],
-                                            const ElemConsts &k, double R[4][3])
+                                            const double *p4, const ElemConsts &k, double R[4][3])
 {
     if constexpr (SYM)
-        element_rhs_sym(X, U, k, R);
+        element_rhs_sym(X, U, p4, k, R);
     else
-        element_rhs_gen(X, U, k, R);
+        element_rhs_gen(X, U, p4, k, R);
 }
 
 }  // namespace tal

@@ -71,6 +71,10 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src)
 {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -103,22 +107,25 @@ __device__ __forceinline__ void load_record_s(const double *rec, int v, double X
 // ---------------------------------------------------------------------------
 // (1) one thread per element, 12 FP64 REDs (scatter = atomic)
 // ---------------------------------------------------------------------------
-template <bool SYM>
+template <bool SYM, bool PR = false>
 __global__ void __launch_bounds__(256) k_assemble_atomic(const int4 *__restrict__ conn,
                                                          int64_t e_begin, int64_t e_end,
                                                          const double *__restrict__ nrec, RhsSoA rhs,
-                                                         ElemConsts kc)
+                                                         ElemConsts kc, const double *__restrict__ press)
 {
     const int64_t e = e_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e_end)
         return;
     const int4 q = ldg_stream(conn + e);
     const int ids[4] = {q.x, q.y, q.z, q.w};
-    double X[4][3], U[4][3], R[4][3];
+    double X[4][3], U[4][3], R[4][3], p4[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a) {
         load_record_g(nrec, ids[a], X[a], U[a]);
-    element_rhs<SYM>(X, U, kc, R);
+        if (PR)
+            p4[a] = __ldg(press + ids[a]);
+    }
+    element_rhs<SYM>(X, U, PR ? p4 : nullptr, kc, R);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         atomicAdd(rhs.rx + ids[a], R[a][0]);
@@ -130,22 +137,25 @@ __global__ void __launch_bounds__(256) k_assemble_atomic(const int4 *__restrict_
 // ---------------------------------------------------------------------------
 // (2) one colour class per launch, plain read-modify-write (scatter = colored)
 // ---------------------------------------------------------------------------
-template <bool SYM>
+template <bool SYM, bool PR = false>
 __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict__ conn,
                                                           int64_t e_begin, int64_t e_end,
                                                           const double *__restrict__ nrec, RhsSoA rhs,
-                                                          ElemConsts kc)
+                                                          ElemConsts kc, const double *__restrict__ press)
 {
     const int64_t e = e_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e_end)
         return;
     const int4 q = ldg_stream(conn + e);
     const int ids[4] = {q.x, q.y, q.z, q.w};
-    double X[4][3], U[4][3], R[4][3];
+    double X[4][3], U[4][3], R[4][3], p4[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a) {
         load_record_g(nrec, ids[a], X[a], U[a]);
-    element_rhs<SYM>(X, U, kc, R);
+        if (PR)
+            p4[a] = __ldg(press + ids[a]);
+    }
+    element_rhs<SYM>(X, U, PR ? p4 : nullptr, kc, R);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         rhs.rx[ids[a]] += R[a][0];
@@ -220,7 +230,7 @@ struct PrivCfg<2> {  // 256 patches / chunk
 
 constexpr int BLOB_LEVELS = 32;  // = CHUNK_LEVELS (tal_prep.hpp)
 constexpr int SLOTS = 12;        // = PATCH_SLOTS (tal_prep.hpp)
-template <int T, int NM, int NC>
+template <int T, int NM, int NC, bool PR = false>
 struct PrivLayout {
     static constexpr int TABLES = 4 * SLOTS * T;  // u16 ids[SLOTS][T], pos[SLOTS][T]
     static constexpr int BLOB = 16 + TABLES + 2 * BLOB_LEVELS + 2 * pad16(4 * NM) + pad16(NM);
@@ -229,10 +239,11 @@ struct PrivLayout {
     static constexpr int BLOBS = 128;
     static constexpr int NREC = BLOBS + 2 * BLOB_AL;  // one buffer: gathered after phase B
     static constexpr int RES = NREC + NM * 48;
-    static constexpr int TOTAL = RES + 3 * NC * 8;
+    static constexpr int PRS = RES + 3 * NC * 8;     // nodal pressures (PR only)
+    static constexpr int TOTAL = PRS + (PR ? NM * 8 : 0);
 };
-template <int CFG>
-using PrivLayoutOf = PrivLayout<PrivCfg<CFG>::THREADS, PrivCfg<CFG>::NM, PrivCfg<CFG>::NC>;
+template <int CFG, bool PR = false>
+using PrivLayoutOf = PrivLayout<PrivCfg<CFG>::THREADS, PrivCfg<CFG>::NM, PrivCfg<CFG>::NC, PR>;
 
 // Fused interface sum of a domain decomposition (scatter=private-atomic):
 // the partial sum of an interface-plane node is REDed into the local RHS and,
@@ -248,15 +259,19 @@ struct PrivArgs {
     const int32_t *__restrict__ blob_off;  // 16-B units, n_chunks+1
     int n_chunks;
     double *px, *py, *pz;  // ordered-merge partials, indexed node_begin + j
+    const double *press;   // nodal pressures, internal order (PR instances)
 };
 
-template <int CFG, bool ORDERED, bool PEER = false>
-__global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
+// PR: with the optional pressure-gradient term (tal_element.cuh pressure_add);
+// the nodal pressures are gathered next to the records (2 KB more shared
+// memory per CTA: 3 CTAs/SM instead of 4).
+template <int CFG, bool ORDERED, bool PEER = false, bool PR = false>
+__global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MINB * 3 + 3) / 4 : PrivCfg<CFG>::MINB)
     k_assemble_private(PrivArgs pa, const double *__restrict__ nrec_g, RhsSoA rhs, ElemConsts kc,
                        PeerArgs peer)
 {
     constexpr int T = PrivCfg<CFG>::THREADS, NM = PrivCfg<CFG>::NM, NC = PrivCfg<CFG>::NC;
-    using L = PrivLayoutOf<CFG>;
+    using L = PrivLayoutOf<CFG, PR>;
     extern __shared__ __align__(128) uint8_t sm[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + L::MBAR);
     // node-major contribution lists: res*[coff[j] .. coff[j+1]) belong to node j
@@ -269,6 +284,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
         return;
     auto blob = [&](int b) { return sm + L::BLOBS + b * L::BLOB_AL; };
     double *const nrec_s = reinterpret_cast<double *>(sm + L::NREC);
+    double *const pres_s = reinterpret_cast<double *>(sm + L::PRS);
 
     auto issue = [&](int i, int b) {  // one thread: bulk-copy chunk i's blob into buffer b
         const int c = first + i * stride;
@@ -287,6 +303,8 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
             cp_async16(dst + 6 * j, src);
             cp_async16(dst + 6 * j + 2, src + 2);
             cp_async16(dst + 6 * j + 4, src + 4);
+            if (PR)
+                cp_async8(pres_s + j, pa.press + gl[j]);
         }
         cp_async_commit();
     };
@@ -356,6 +374,11 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
             // previous tet's contribution to r_t and leaves complete for r_t,
             // R[3] (r_t+1) becomes the next tet's carry
             double R[4][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+            double pab = 0.0, p2 = 0.0;  // pressure: p_a + p_b, p_{r_t}
+            if (PR) {
+                pab = pres_s[ID(1)] + pres_s[ID(2)];
+                p2 = pres_s[ID(3)];
+            }
 #pragma unroll kRingUnroll
             for (int t = 0; t < k; ++t) {
                 double X3[3], U3[3], e3[3], du3[3], c1[3], c2[3];
@@ -370,6 +393,11 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PrivCfg<CFG>::MINB)
                 cross3(e3, e1, c2);
                 const double det = fma(e1[0], c1[0], fma(e1[1], c1[1], e1[2] * c1[2]));
                 tet_tail<true>(c1, c2, c3, det, du1, du2, du3, Ua, Ub, S01, U2, U3, kc, R);
+                if (PR) {
+                    const double p3 = pres_s[ID(3 + nxt)];
+                    pressure_add(0.25 * (pab + (p2 + p3)), det, c1, c2, c3, R);
+                    p2 = p3;
+                }
                 const int p = POS(3 + t);
                 resx[p] = R[2][0];
                 resy[p] = R[2][1];
@@ -511,6 +539,15 @@ __global__ void __launch_bounds__(256) k_pack_velocity(const double *__restrict_
     nrec[6 * i + 3] = aos[3 * s + 0];
     nrec[6 * i + 4] = aos[3 * s + 1];
     nrec[6 * i + 5] = aos[3 * s + 2];
+}
+
+__global__ void __launch_bounds__(256) k_pack_scalar(const double *__restrict__ src,
+                                                     const int32_t *__restrict__ perm, int64_t n,
+                                                     double *dst)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n)
+        dst[i] = src[perm ? (int64_t)perm[i] : i];
 }
 
 __global__ void __launch_bounds__(256) k_unpack_aos(const double *__restrict__ rx,
