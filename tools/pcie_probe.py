@@ -48,7 +48,28 @@ def both():
     cur.wait_stream(s2)
 
 
+def both_split(k):
+    ss = [torch.cuda.Stream() for _ in range(2 * k)]
+    step = (n + k - 1) // k
+
+    def f():
+        cur = torch.cuda.current_stream()
+        for st in ss:
+            st.wait_stream(cur)
+        for i in range(k):
+            lo, hi = i * step, min(n, (i + 1) * step)
+            with torch.cuda.stream(ss[i]):
+                d_in[lo:hi].copy_(h_in[lo:hi], non_blocking=True)
+            with torch.cuda.stream(ss[k + i]):
+                h_out[lo:hi].copy_(d_out[lo:hi], non_blocking=True)
+        for st in ss:
+            cur.wait_stream(st)
+    return f
+
+
 t_h2d, t_d2h, t_both = timed(h2d), timed(d2h), timed(both)
+split = {k: timed(both_split(k)) for k in (2, 4, 8)}
 print(json.dumps({"bytes": nb, "h2d_ms": t_h2d, "d2h_ms": t_d2h, "both_ms": t_both,
                   "h2d_gbs": nb / t_h2d / 1e6, "d2h_gbs": nb / t_d2h / 1e6,
-                  "both_gbs_per_dir": nb / t_both / 1e6}))
+                  "both_gbs_per_dir": nb / t_both / 1e6,
+                  "both_split_gbs_per_dir": {k: nb / v / 1e6 for k, v in split.items()}}))
