@@ -366,8 +366,7 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         if (!sym)  // patches permute tet corners: only valid for the symmetric rule
             return launch_run(h, p, TAL_SCATTER_ATOMIC, s, launches);
         const bool ordered = scatter == TAL_SCATTER_PRIVATE;
-        const int64_t ncn = (int64_t)h->ch.cnodes.size();
-        PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr, nullptr, nullptr,
+        PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr,
                     h->has_press ? h->d_press : nullptr};
         PeerArgs peer{};
         const int np = h->n_peers();
@@ -383,9 +382,7 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
                 }
         }
         if (ordered && h->d_partial) {
-            pa.px = h->d_partial;
-            pa.py = h->d_partial + ncn;
-            pa.pz = h->d_partial + 2 * ncn;
+            pa.part = h->d_partial;
         }
         // shared nodes receive FP64 REDs: zero the RHS first (a separate pass:
         // zeroing inside the kernel, by thread or TMA bulk stores, measured
@@ -420,7 +417,7 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         const int64_t nb = (int64_t)h->ch.bnd_nodes.size();
         if (ordered && nb) {
             k_merge_partials<<<grid_for(nb, 256), 256, 0, s>>>(h->d_bnd_nodes, h->d_bnd_off, h->d_bnd_pos,
-                                                              nb, pa.px, pa.py, pa.pz, rhs);
+                                                              nb, pa.part, rhs);
             TAL_CK_LAUNCH();
             ++nl;
         }

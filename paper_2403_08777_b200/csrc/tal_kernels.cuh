@@ -258,7 +258,7 @@ struct PrivArgs {
     const uint8_t *__restrict__ blobs;
     const int32_t *__restrict__ blob_off;  // 16-B units, n_chunks+1
     int n_chunks;
-    double *px, *py, *pz;  // ordered-merge partials, indexed node_begin + j
+    double *part;          // ordered-merge partials, AoS (x,y,z) per chunk-node entry node_begin + j
     const double *press;   // nodal pressures, internal order (PR instances)
 };
 
@@ -464,9 +464,10 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
                 rhs.ry[v] = ay;
                 rhs.rz[v] = az;
             } else if (ORDERED) {
-                pa.px[hdr.z + q] = ax;
-                pa.py[hdr.z + q] = ay;
-                pa.pz[hdr.z + q] = az;
+                double *d = pa.part + 3 * (int64_t)(hdr.z + q);
+                d[0] = ax;
+                d[1] = ay;
+                d[2] = az;
             } else {
                 atomicAdd(rhs.rx + v, ax);
                 atomicAdd(rhs.ry + v, ay);
@@ -505,19 +506,18 @@ __global__ void __launch_bounds__(512) k_zero(double *__restrict__ p, int64_t n)
 __global__ void __launch_bounds__(256) k_merge_partials(const int32_t *__restrict__ bnd_nodes,
                                                         const int32_t *__restrict__ bnd_off,
                                                         const int32_t *__restrict__ bnd_pos,
-                                                        int64_t n_bnd, const double *__restrict__ px,
-                                                        const double *__restrict__ py,
-                                                        const double *__restrict__ pz, RhsSoA rhs)
+                                                        int64_t n_bnd, const double *__restrict__ part,
+                                                        RhsSoA rhs)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_bnd)
         return;
     double ax = 0.0, ay = 0.0, az = 0.0;
     for (int p = bnd_off[i]; p < bnd_off[i + 1]; ++p) {
-        const int q = bnd_pos[p];
-        ax += px[q];
-        ay += py[q];
-        az += pz[q];
+        const double *e = part + 3 * (int64_t)bnd_pos[p];  // one 24-B entry
+        ax += e[0];
+        ay += e[1];
+        az += e[2];
     }
     const int v = bnd_nodes[i];
     rhs.rx[v] = ax;
