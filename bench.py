@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--cells", type=int, default=128, help="cells per side (per rank slab)")
     ap.add_argument("--init", default="random:1")
     ap.add_argument("--scatter", default="private-atomic")
-    ap.add_argument("--variant", choices=["rsp", "rs", "b"], default="rsp",
+    ap.add_argument("--variant", choices=["rsp", "rs", "b", "p"], default="rsp",
                     help="code shape (rs/b: the paper's study shapes, one thread per element)")
     ap.add_argument("--renumber", default="rcm")
     ap.add_argument("--element-order", default="sfc")
@@ -248,9 +248,8 @@ def run_ours(a) -> None:
         if a.permute:
             mesh = tb.permute_nodes(mesh, np.random.default_rng(0).permutation(mesh.n_nodes))
         u = tb.make_velocity(mesh, a.init)
-        variant = tb.VariantId(a.variant)
         asm = tb.Assembler(mesh, cfg, build_colors=(a.scatter == "colored" or (
-            variant is not tb.VariantId.RSP and a.scatter == "private")))
+            a.variant != "rsp" and a.scatter == "private")))
     prep_s = time.perf_counter() - t0
     info = asm.info()
     press = None
@@ -263,7 +262,7 @@ def run_ours(a) -> None:
 
     def one_step():
         if dom is None:
-            return asm.run(P, stream=stream, variant=tb.VariantId(a.variant))
+            return asm.run(P, stream=stream, variant=a.variant)
         return dom.step(P, stream=stream)
 
     # parity + CPU baseline (rank 0, N=1): the oracle as checker / baseline only
@@ -273,7 +272,7 @@ def run_ours(a) -> None:
         from oracle import oracle as O
         O.build()
         T = O.default_threads()
-        rhs_gpu, _ = asm.assemble(u, P, variant=tb.VariantId(a.variant))
+        rhs_gpu, _ = asm.assemble(u, P, variant=a.variant)
         O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)  # warm-up
         ts = []
         ref = None
@@ -438,7 +437,8 @@ def run_ours(a) -> None:
              "atomic": "k_assemble_atomic<true>", "colored": "k_assemble_colored<true> (all colours)"}[a.scatter]
     if a.variant != "rsp":
         colored = a.scatter in ("private", "colored")
-        kname = ("k_assemble_baseline" if a.variant == "b" else "k_assemble_rs") + \
+        kname = {"b": "k_assemble_baseline", "p": "k_assemble_baseline<fixed>",
+                 "rs": "k_assemble_rs"}[a.variant] + \
             ("<colored> (all colours)" if colored else "<atomic>")
     traffic = ncu_traffic(kname, workload)
     line = {

@@ -60,6 +60,7 @@ extern "C" {
 #define TAL_VARIANT_B 0
 #define TAL_VARIANT_RS 1
 #define TAL_VARIANT_RSP 2
+#define TAL_VARIANT_P 3 /* study only: B with literal trip counts, privatised arrays (PAPER.md "P") */
 
 /* node renumbering applied at upload (inverted on every host read-back) */
 #define TAL_RENUMBER_NONE 0

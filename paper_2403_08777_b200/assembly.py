@@ -219,6 +219,14 @@ class AssemblyResult:
     timings: Optional[Timings] = None
 
 
+def _variant_key(variant) -> str:
+    """A VariantId, or "p": the study-only privatised-baseline shape (B with
+    literal trip counts, csrc/tal_shapes.cuh), not one of the reference's."""
+    if isinstance(variant, str) and variant == "p":
+        return "p"
+    return VariantId(variant).value
+
+
 def _params(params: PhysParams, pmat: Optional[np.ndarray] = None) -> N.TalParams:
     p = N.TalParams()
     p.rho = float(params.rho)
@@ -309,7 +317,7 @@ class Assembler:
         scatter = scatter or self.cfg.scatter
         if scatter not in N.SCATTER:
             raise ValueError(f"unknown scatter mode {scatter!r}")
-        variant = VariantId(variant)
+        vkey = _variant_key(variant)
         if u.shape != (self.n_nodes, 3) or rhs.shape != (self.n_nodes, 3):
             raise ValueError("u and rhs must have shape (n_nodes, 3)")
         if not (u.flags.c_contiguous and rhs.flags.c_contiguous and u.dtype == np.float64
@@ -317,7 +325,7 @@ class Assembler:
             raise ValueError("u and rhs must be C-contiguous float64")
         t = N.TalTimings()
         N.check(N.lib().tal_assemble_variant(self._h, N.ptr(u), ctypes.byref(_params(params, pmat)),
-                                             N.ptr(rhs), N.VARIANT[variant.value],
+                                             N.ptr(rhs), N.VARIANT[vkey],
                                              N.SCATTER[scatter], ctypes.byref(t)))
         return Timings(t.h2d_ms, t.pack_ms, t.kernel_ms, t.unpack_ms, t.d2h_ms, t.total_ms,
                        int(t.kernel_launches))
@@ -405,7 +413,7 @@ class Assembler:
             raise ValueError(f"unknown scatter mode {scatter!r}")
         nl = ctypes.c_int64(0)
         N.check(N.lib().tal_run_variant(self._h, ctypes.byref(_params(params, pmat)),
-                                        N.VARIANT[VariantId(variant).value], N.SCATTER[scatter],
+                                        N.VARIANT[_variant_key(variant)], N.SCATTER[scatter],
                                         _stream(stream), ctypes.byref(nl)))
         return int(nl.value)
 

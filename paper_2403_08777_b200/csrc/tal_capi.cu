@@ -485,6 +485,11 @@ int launch_shape(tal_handle *h, const tal_params *p, int variant, int scatter, c
                 k_assemble_baseline<true><<<grid, 256, 0, s>>>(conn, b, e, nodes, rhs, sc);
             else
                 k_assemble_baseline<false><<<grid, 256, 0, s>>>(conn, b, e, nodes, rhs, sc);
+        } else if (variant == TAL_VARIANT_P) {
+            if (colored)
+                k_assemble_baseline<true, true><<<grid, 256, 0, s>>>(conn, b, e, nodes, rhs, sc);
+            else
+                k_assemble_baseline<false, true><<<grid, 256, 0, s>>>(conn, b, e, nodes, rhs, sc);
         } else {
             if (colored)
                 k_assemble_rs<true><<<grid, 256, 0, s>>>(conn, b, e, nodes, rhs, sc);
@@ -517,9 +522,10 @@ int launch_any(tal_handle *h, const tal_params *p, int variant, int scatter, cud
 {
     if (variant == TAL_VARIANT_RSP)
         return launch_run(h, p, scatter, s, launches);
-    if (h->has_press && (variant == TAL_VARIANT_B || variant == TAL_VARIANT_RS))
+    const bool shape = variant == TAL_VARIANT_B || variant == TAL_VARIANT_RS || variant == TAL_VARIANT_P;
+    if (h->has_press && shape)
         return fail(TAL_EINVAL, "the pressure-gradient term is implemented for the RSP shape only");
-    if (variant == TAL_VARIANT_B || variant == TAL_VARIANT_RS)
+    if (shape)
         return launch_shape(h, p, variant, scatter, s, launches);
     return fail(TAL_EINVAL, "unknown variant " + std::to_string(variant));
 }

@@ -16,6 +16,8 @@
 //     at every Gauss point, a dense 12x12 elemental matrix is built and
 //     multiplied by the nodal unknowns, and the element vector is scattered
 //     by a separate loop.  The per-element arrays live in local memory.
+//  P  (study only; "P"): the B statements with literal trip
+//     counts and unrolled loops (privatised arrays, no restructuring).
 //  RS (variants.py:373-464, _chunk_restructured): tet4-specialised -- fixed
 //     trip counts, geometry / gradient / viscosity once per element, explicit
 //     4-point Gauss loop for the convective term, RHS entries computed
@@ -82,7 +84,7 @@ __device__ __forceinline__ void scatter_elem(const int ids[4], const double r[4]
 // ---------------------------------------------------------------------------
 // B: generic baseline shape
 // ---------------------------------------------------------------------------
-template <bool COLORED>
+template <bool COLORED, bool FIXED = false>
 __global__ void __launch_bounds__(256) k_assemble_baseline(const int4 *__restrict__ conn, int64_t e_begin,
                                                            int64_t e_end, const double *__restrict__ nrec,
                                                            RhsSoA rhs, ShapeConsts sc)
@@ -90,27 +92,31 @@ __global__ void __launch_bounds__(256) k_assemble_baseline(const int4 *__restric
     const int64_t e = e_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e_end)
         return;
-    const int nn = sc.nn, nd = sc.nd, ng = sc.ng;
+    // FIXED (the paper's "P" shape, study only): the same statements with
+    // literal trip counts and unrolled loops, so the per-element arrays can be
+    // privatised into registers (what does not fit spills)
+    constexpr int UR = FIXED ? 16 : 1;
+    const int nn = FIXED ? 4 : sc.nn, nd = FIXED ? 3 : sc.nd, ng = FIXED ? 4 : sc.ng;
     const int4 q = conn[e];
     const int ids[4] = {q.x, q.y, q.z, q.w};
     double xe[4][3], ue[4][3];
-#pragma unroll 1
+#pragma unroll UR
     for (int a = 0; a < nn; ++a)
-#pragma unroll 1
+#pragma unroll UR
         for (int k = 0; k < nd; ++k) {
             xe[a][k] = nrec[6 * (int64_t)ids[a] + k];
             ue[a][k] = nrec[6 * (int64_t)ids[a] + 3 + k];
         }
     double gpcar[4][4][3], gpvol[4], gpvel[4][3], gpvis[4];
-#pragma unroll 1
+#pragma unroll UR
     for (int ig = 0; ig < ng; ++ig) {
         double xjac[3][3];
-#pragma unroll 1
+#pragma unroll UR
         for (int k = 0; k < nd; ++k)
-#pragma unroll 1
+#pragma unroll UR
             for (int l = 0; l < nd; ++l) {
                 double s = 0.0;
-#pragma unroll 1
+#pragma unroll UR
                 for (int a = 0; a < nn; ++a)
                     s += xe[a][k] * sc.dshape[ig][a][l];
                 xjac[k][l] = s;
@@ -129,12 +135,12 @@ __global__ void __launch_bounds__(256) k_assemble_baseline(const int4 *__restric
         xinv[2][0] = (xjac[1][0] * xjac[2][1] - xjac[1][1] * xjac[2][0]) / det;
         xinv[2][1] = (xjac[0][1] * xjac[2][0] - xjac[0][0] * xjac[2][1]) / det;
         xinv[2][2] = (xjac[0][0] * xjac[1][1] - xjac[0][1] * xjac[1][0]) / det;
-#pragma unroll 1
+#pragma unroll UR
         for (int a = 0; a < nn; ++a)
-#pragma unroll 1
+#pragma unroll UR
             for (int k = 0; k < nd; ++k) {
                 double s = 0.0;
-#pragma unroll 1
+#pragma unroll UR
                 for (int l = 0; l < nd; ++l)
                     s += sc.dshape[ig][a][l] * xinv[l][k];
                 gpcar[ig][a][k] = s;
@@ -143,20 +149,20 @@ __global__ void __launch_bounds__(256) k_assemble_baseline(const int4 *__restric
         gpvol[ig] = sc.wts[ig] * vol;
         const double dlt = cbrt(6.0 * vol);
         double gve[3][3];
-#pragma unroll 1
+#pragma unroll UR
         for (int i = 0; i < nd; ++i) {
             double s = 0.0;
-#pragma unroll 1
+#pragma unroll UR
             for (int a = 0; a < nn; ++a)
                 s += sc.npts[ig][a] * ue[a][i];
             gpvel[ig][i] = s;
         }
-#pragma unroll 1
+#pragma unroll UR
         for (int k = 0; k < nd; ++k)
-#pragma unroll 1
+#pragma unroll UR
             for (int i = 0; i < nd; ++i) {
                 double s = 0.0;
-#pragma unroll 1
+#pragma unroll UR
                 for (int a = 0; a < nn; ++a)
                     s += gpcar[ig][a][k] * ue[a][i];
                 gve[k][i] = s;
@@ -165,19 +171,19 @@ __global__ void __launch_bounds__(256) k_assemble_baseline(const int4 *__restric
     }
     // dense elemental matrix (nn*nd)^2, then elrhs = -elemat . u
     double elemat[12][12];
-#pragma unroll 1
+#pragma unroll UR
     for (int r = 0; r < nn * nd; ++r)
-#pragma unroll 1
+#pragma unroll UR
         for (int c = 0; c < nn * nd; ++c)
             elemat[r][c] = 0.0;
-#pragma unroll 1
+#pragma unroll UR
     for (int ig = 0; ig < ng; ++ig)
-#pragma unroll 1
+#pragma unroll UR
         for (int a = 0; a < nn; ++a)
-#pragma unroll 1
+#pragma unroll UR
             for (int b = 0; b < nn; ++b) {
                 double cdot = 0.0, ddot = 0.0;
-#pragma unroll 1
+#pragma unroll UR
                 for (int k = 0; k < nd; ++k) {
                     cdot += gpvel[ig][k] * gpcar[ig][b][k];
                     ddot += gpcar[ig][a][k] * gpcar[ig][b][k];
@@ -185,15 +191,15 @@ __global__ void __launch_bounds__(256) k_assemble_baseline(const int4 *__restric
                 const double conv = sc.rho * gpvol[ig] * sc.npts[ig][a] * cdot;
                 const double diff = gpvis[ig] * gpvol[ig] * ddot;
                 const double s_ab = conv + diff;
-#pragma unroll 1
+#pragma unroll UR
                 for (int i = 0; i < nd; ++i)
                     elemat[a * nd + i][b * nd + i] += s_ab;
             }
     double elrhs[4][3];
-#pragma unroll 1
+#pragma unroll UR
     for (int r = 0; r < nn * nd; ++r) {
         double s = 0.0;
-#pragma unroll 1
+#pragma unroll UR
         for (int c = 0; c < nn * nd; ++c)
             s += elemat[r][c] * ue[c / nd][c % nd];
         elrhs[r / nd][r % nd] = -s;

@@ -265,3 +265,18 @@ def test_perfmodel_dataset_has_knee_and_points():
     assert any(r.kind == "roof" and r.ai == pytest.approx(pm.machine_balance(spec)) for r in rows)
     csv = pm.roofline_csv(rows)
     assert csv.startswith("label,ai_flop_per_byte,gflops,kind\n") and "RSP-star" in csv
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scatter", ["atomic", "colored"])
+def test_study_shape_p_matches_oracle(oracle, scatter):
+    """The study-only "P" shape (B statements, literal trip counts)."""
+    m = tb.generate_box_mesh(7, 6, 5)
+    u = tb.make_velocity(m, "random:3")
+    asm = tb.Assembler(m, tb.RunConfig(scatter=scatter), build_colors=True)
+    rhs, _ = asm.assemble(u, P, variant="p")
+    ref = oracle.assemble_reference(m.coords, m.connectivity, u)
+    assert oracle.compare(rhs, ref, m.coords, m.connectivity, u).passed
+    with pytest.raises(ValueError):
+        asm.assemble(u, P, variant="q")
+    asm.close()

@@ -10,6 +10,7 @@ from pathlib import Path
 D = Path(sys.argv[1] if len(sys.argv) > 1 else "profiles/round1/shapes")
 E = 12582912  # 128^3 Kuhn box
 rows = [("B", "ncu_b.json", "bench_shape_b_atomic.json"),
+        ("P (study only)", "ncu_p.json", "bench_shape_p_atomic.json"),
         ("RS", "ncu_rs.json", "bench_shape_rs_atomic.json"),
         ("RSP thread/tet", "ncu_rsp_atomic.json", "bench_shape_rsp_atomic.json"),
         ("RSP edge-star (production)", "../ncu_full_private_atomic.json", "../bench_default.json")]
