@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--permute", action="store_true", help="config 3: random node permutation")
     ap.add_argument("--pressure", action="store_true",
                     help="add the P1 pressure-gradient term (extension; uniform [-1,1) nodal p, seed 2)")
+    ap.add_argument("--partition", choices=["slab", "rcb"], default="slab",
+                    help="N>1: z-slabs of the box (weak scaling) or RCB of the (optionally "
+                         "--permute'd) global box mesh, exchange-path interface sum")
     ap.add_argument("--check", action="store_true",
                     help="N>1: gather the owned RHS rows to rank 0 and check them against the oracle")
     return ap.parse_args()
@@ -237,7 +240,18 @@ def run_ours(a) -> None:
                        device=dev)
     c = a.cells
     t0 = time.perf_counter()
-    if ws > 1:
+    gperm = None
+    if ws > 1 and a.partition == "rcb":
+        from paper_2403_08777_b200.distributed import PartitionedDomain
+        g = tb.generate_box_mesh(c, c, c * ws)
+        if a.permute:
+            gperm = np.random.default_rng(0).permutation(g.n_nodes)
+            g = tb.permute_nodes(g, gperm)
+        dom = PartitionedDomain(g, rank, ws, cfg)
+        mesh, u = dom.mesh, dom.set_velocity(tb.make_velocity(g, a.init))
+        asm = dom.assembler
+        del g
+    elif ws > 1:
         from paper_2403_08777_b200.distributed import SlabDomain
         dom = SlabDomain((c, c, c * ws), rank, ws, cfg)
         mesh, u = dom.mesh, dom.velocity(a.init)
@@ -433,11 +447,14 @@ def run_ours(a) -> None:
             from oracle import oracle as O
             O.build()
             g = O.box_mesh(c, c, c * ws)
+            if gperm is not None:  # the permuted global mesh the ranks partitioned
+                gm = tb.permute_nodes(tb.Mesh(coords=g.coords, connectivity=g.connectivity), gperm)
+                g = O.OracleMesh(np.ascontiguousarray(gm.coords), np.ascontiguousarray(gm.connectivity))
             ug = O.velocity(g.coords, a.init)
             ref = O.assemble_rsp(g.coords, g.connectivity, ug, n_threads=O.default_threads())
             full = np.full_like(ref, np.nan)
-            for lo, blk in rows:
-                full[lo:lo + blk.shape[0]] = blk
+            for ids, blk in rows:
+                full[ids] = blk
             chk = O.compare(full, ref, g.coords, g.connectivity, ug)
             parity = {"reference_rel_diff": chk.rel_diff, "rel_l2": chk.rel_l2,
                       "entry_rel": chk.entry_rel, "passed": bool(chk.passed),
@@ -471,7 +488,8 @@ def run_ours(a) -> None:
                    "pressure_term": bool(a.pressure),
                    "l2": "flushed (256 MiB write) before every step, outside the timed events"
                          if flush_buf is not None else "not flushed",
-                   "parallelism": f"dp{ws} z-slabs" if ws > 1 else "single GPU",
+                   "parallelism": (f"dp{ws} z-slabs" if a.partition == "slab" else f"dp{ws} RCB parts")
+                   if ws > 1 else "single GPU",
                    "interface_sum": None if dom is None else (
                        "fused: assembly kernel REDs into the neighbours' RHS (CUDA IPC peer memory)"
                        if dom.fused else "exchange: NCCL send/recv of the interface planes + halo add"

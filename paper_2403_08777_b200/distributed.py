@@ -14,6 +14,13 @@ sum on both ranks.
 
 ``SlabPartition`` is pure host logic (tested with gloo on CPU);
 ``SlabDomain`` binds it to an ``Assembler`` on the rank's GPU.
+
+General (unstructured or renumbered) meshes: ``MeshPartition`` cuts the
+elements by recursive coordinate bisection of their centroids (SURVEY.md
+section 8e); a node may then be shared by several ranks and a rank may have
+many neighbours, so ``PartitionedDomain`` sums with the NCCL exchange (each
+rank sends its local partial of every node it shares with a neighbour, then
+adds what it receives: every sharer ends with the full sum).
 """
 
 from __future__ import annotations
@@ -143,7 +150,88 @@ class SlabPartition:
         return make_velocity(mesh, spec)
 
 
-def exchange_interfaces(part: SlabPartition, send: dict, recv: dict, group=None) -> None:
+def rcb_parts(points: np.ndarray, world: int) -> np.ndarray:
+    """Recursive coordinate bisection: a part id in [0, world) per point.
+
+    Each level splits the current set along its largest extent at the count
+    that gives the two halves floor(k/2) and ceil(k/2) of the k parts
+    (balanced to one element); ties resolved by a stable sort, so every rank
+    computes the same partition."""
+    pts = np.asarray(points, dtype=np.float64)
+    n = pts.shape[0]
+    part = np.zeros(n, dtype=np.int32)
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    stack = [(np.arange(n), 0, world)]
+    while stack:
+        idx, first, k = stack.pop()
+        if k == 1 or idx.size == 0:
+            part[idx] = first
+            continue
+        kl = k // 2
+        sub = pts[idx]
+        ax = int(np.argmax(sub.max(axis=0) - sub.min(axis=0))) if idx.size else 0
+        order = np.argsort(sub[:, ax], kind="stable")
+        cut = (idx.size * kl) // k
+        stack.append((idx[order[:cut]], first, kl))
+        stack.append((idx[order[cut:]], first + kl, k - kl))
+    return part
+
+
+class MeshPartition:
+    """Rank ``rank``'s share of a general mesh cut into ``world`` parts.
+
+    ``parts`` (element -> rank) defaults to RCB of the element centroids.
+    Local nodes are the rank's element nodes in ascending global id, so a
+    shared node has the same relative order on every sharer; its owner (for
+    a gathered global vector) is the lowest sharing rank."""
+
+    def __init__(self, mesh, rank: int, world: int, parts: Optional[np.ndarray] = None):
+        if not 0 <= rank < world:
+            raise ValueError("rank out of range")
+        self.rank, self.world = rank, world
+        coords = np.asarray(mesh.coords, dtype=np.float64)
+        conn = np.asarray(mesh.connectivity, dtype=np.int64)
+        self.n_global_nodes = coords.shape[0]
+        if parts is None:
+            parts = rcb_parts(coords[conn].mean(axis=1), world)
+        self.parts = np.asarray(parts, dtype=np.int32)
+        if self.parts.shape != (conn.shape[0],) or (self.parts.size and (
+                self.parts.min() < 0 or self.parts.max() >= world)):
+            raise ValueError("parts must give a rank in [0, world) per element")
+        mine = np.flatnonzero(self.parts == rank)
+        self.elements = mine                                   # global element ids
+        self.global_nodes = np.unique(conn[mine])              # local -> global node id
+        self._coords = coords[self.global_nodes]
+        self._conn = np.searchsorted(self.global_nodes, conn[mine])
+        # (node, rank) incidence -> sharers of each of my nodes
+        nv = np.unique(conn.ravel() * world + np.repeat(self.parts.astype(np.int64), 4))
+        node, rk = nv // world, (nv % world).astype(np.int32)
+        owner = np.full(self.n_global_nodes, world, dtype=np.int32)
+        np.minimum.at(owner, node, rk)
+        self._owner = owner[self.global_nodes]
+        on_me = np.isin(node, self.global_nodes)
+        self._ifaces = {}
+        for nbr in np.unique(rk[on_me & (rk != rank)]):
+            g = node[on_me & (rk == nbr)]                      # ascending global ids
+            self._ifaces[int(nbr)] = np.searchsorted(self.global_nodes, g)
+
+    def local_mesh(self) -> Mesh:
+        return Mesh(coords=self._coords, connectivity=self._conn)
+
+    def interfaces(self) -> dict[int, np.ndarray]:
+        """Neighbour rank -> local ids of the nodes shared with it (ascending
+        global id: the same order on both sides)."""
+        return dict(self._ifaces)
+
+    def owned_mask(self) -> np.ndarray:
+        return self._owner == self.rank
+
+    def velocity(self, u_global: np.ndarray) -> np.ndarray:
+        return np.ascontiguousarray(np.asarray(u_global)[self.global_nodes])
+
+
+def exchange_interfaces(part, send: dict, recv: dict, group=None) -> None:
     """Post the interface-plane send/recv pairs with every neighbour and wait.
 
     ``send[nbr]`` / ``recv[nbr]`` are same-shaped tensors (CUDA under NCCL, CPU
@@ -258,12 +346,48 @@ class SlabDomain:
         import torch.distributed as dist
         return dist.is_initialized() and dist.get_backend() == "gloo"
 
-    def owned_rhs(self) -> tuple[int, np.ndarray]:
-        """(first global node id, rhs rows this rank reports) after a step."""
+    def owned_rhs(self) -> tuple[np.ndarray, np.ndarray]:
+        """(global node ids, rhs rows) this rank reports after a step."""
         rhs = self.assembler.get_rhs_host(stream=0)
         self.assembler.synchronize(stream=0)
-        lo, _ = self.part.node_range
-        return lo, rhs[self.part.owned_mask()]
+        mask = self.part.owned_mask()
+        return self._global_ids()[mask], rhs[mask]
+
+    def _global_ids(self) -> np.ndarray:
+        lo, hi = self.part.node_range
+        return np.arange(lo, hi, dtype=np.int64)
 
     def close(self) -> None:
         self.assembler.close()
+
+
+class PartitionedDomain(SlabDomain):
+    """One rank's part of a general mesh (``MeshPartition``) on its GPU: local
+    assembly, then the NCCL exchange of the shared-node partial sums with
+    every neighbour (``SlabDomain.step``'s exchange path).  The fused
+    peer-memory sum needs the slab's at most two neighbours, so it is not
+    used here."""
+
+    def __init__(self, mesh, rank: int, world: int, cfg=None, parts: Optional[np.ndarray] = None):
+        import torch
+
+        from .assembly import Assembler, RunConfig
+        self.part = MeshPartition(mesh, rank, world, parts)
+        self.cfg = cfg or RunConfig()
+        self.mesh = self.part.local_mesh()
+        self.fused, self.fused_error = False, None
+        self.assembler = Assembler(self.mesh, self.cfg)
+        dev = torch.device("cuda", self.cfg.device)
+        self._lists, self._send, self._recv = {}, {}, {}
+        for nbr, ids in self.part.interfaces().items():
+            self._lists[nbr] = torch.as_tensor(self.assembler.map_nodes(ids), device=dev)
+            self._send[nbr] = torch.empty((ids.size, 3), dtype=torch.float64, device=dev)
+            self._recv[nbr] = torch.empty((ids.size, 3), dtype=torch.float64, device=dev)
+
+    def set_velocity(self, u_global: np.ndarray) -> np.ndarray:
+        u = self.part.velocity(u_global)
+        self.assembler.set_velocity_host(u, stream=0)
+        return u
+
+    def _global_ids(self) -> np.ndarray:
+        return self.part.global_nodes

@@ -106,3 +106,91 @@ def test_interface_exchange_gloo_matches_single_domain(tmp_path, world, oracle):
     assert not np.isnan(full).any()
     chk = oracle.compare(full, ref, g.coords, g.connectivity, ug)
     assert chk.passed, chk
+
+
+# ---------------------------------------------------------------------------
+# general meshes: recursive coordinate bisection (MeshPartition)
+# ---------------------------------------------------------------------------
+
+def _perm_box(cells, seed=0):
+    g = tb.generate_box_mesh(*cells)
+    return tb.permute_nodes(g, np.random.default_rng(seed).permutation(g.n_nodes))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5, 8])
+def test_rcb_parts_balanced_and_deterministic(world):
+    from paper_2403_08777_b200.distributed import rcb_parts
+    m = _perm_box((6, 5, 4))
+    cen = m.coords[m.connectivity].mean(axis=1)
+    p = rcb_parts(cen, world)
+    assert p.shape == (m.n_elems,) and p.min() == 0 and p.max() == world - 1
+    counts = np.bincount(p, minlength=world)
+    assert counts.max() - counts.min() <= np.ceil(np.log2(max(world, 2)))  # one per bisection level
+    np.testing.assert_array_equal(p, rcb_parts(cen, world))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 7])
+def test_mesh_partition_invariants(world):
+    from paper_2403_08777_b200.distributed import MeshPartition
+    m = _perm_box((5, 4, 6), seed=1)
+    parts = [MeshPartition(m, r, world) for r in range(world)]
+    # every element exactly once, local meshes are re-indexed slices
+    elems = np.sort(np.concatenate([p.elements for p in parts]))
+    np.testing.assert_array_equal(elems, np.arange(m.n_elems))
+    owned = np.zeros(m.n_nodes, dtype=int)
+    for p in parts:
+        lm = p.local_mesh()
+        np.testing.assert_array_equal(p.global_nodes[lm.connectivity], m.connectivity[p.elements])
+        np.testing.assert_array_equal(lm.coords, m.coords[p.global_nodes])
+        owned[p.global_nodes[p.owned_mask()]] += 1
+        for nbr, ids in p.interfaces().items():
+            q = parts[nbr]
+            other = q.interfaces()[p.rank]
+            np.testing.assert_array_equal(p.global_nodes[ids], q.global_nodes[other])
+    assert (owned == 1).all()  # each global node reported by exactly one rank
+
+
+def _worker_rcb(rank, world, port, cells, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    from paper_2403_08777_b200.distributed import MeshPartition
+    g = _perm_box(cells, seed=2)
+    p = MeshPartition(g, rank, world)
+    m = p.local_mesh()
+    u = p.velocity(tb.make_velocity(g, "random:1"))
+    rhs = O.assemble_rsp(m.coords, m.connectivity, u)  # stand-in for the GPU local assembly
+    send = {n: torch.from_numpy(rhs[ids].copy()) for n, ids in p.interfaces().items()}
+    recv = {n: torch.empty_like(t) for n, t in send.items()}
+    exchange_interfaces(p, send, recv)
+    for nbr, ids in p.interfaces().items():
+        rhs[ids] += recv[nbr].numpy()
+    np.save(os.path.join(out_dir, f"rhs_{rank}.npy"), rhs)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [3, 4])
+def test_rcb_exchange_gloo_matches_single_domain(tmp_path, world, oracle):
+    """Nodes shared by up to 4 ranks and ranks with several neighbours: the
+    pairwise exchange of local partials still gives every sharer the sum."""
+    from paper_2403_08777_b200.distributed import MeshPartition
+    cells = (5, 4, 6)
+    mp.start_processes(_worker_rcb, args=(world, _free_port(), cells, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    g = _perm_box(cells, seed=2)
+    ug = tb.make_velocity(g, "random:1")
+    ref = oracle.assemble_rsp(g.coords, g.connectivity, ug)
+    full = np.full_like(ref, np.nan)
+    nbrs = 0
+    for r in range(world):
+        p = MeshPartition(g, r, world)
+        loc = np.load(tmp_path / f"rhs_{r}.npy")
+        full[p.global_nodes[p.owned_mask()]] = loc[p.owned_mask()]
+        ref_loc = ref[p.global_nodes]
+        assert np.abs(loc - ref_loc).max() <= 1e-12 * np.abs(ref).max()  # every sharer has the sum
+        nbrs = max(nbrs, len(p.interfaces()))
+    assert nbrs >= 2
+    assert not np.isnan(full).any()
+    assert oracle.compare(full, ref, g.coords, g.connectivity, ug).passed
