@@ -1,0 +1,28 @@
+"""Small assemblies in every scatter mode / shape / pressure setting, for
+compute-sanitizer (memcheck, racecheck, synccheck, initcheck) runs."""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2403_08777_b200 as tb  # noqa: E402
+
+# default: 10x9x8 (every path once); "big": 64^3 = 2048 chunks, so each of the
+# 592 persistent CTAs walks 3-4 chunks (blob/record buffer reuse across iterations)
+dims = (64, 64, 64) if "big" in sys.argv else (10, 9, 8)
+m = tb.generate_box_mesh(*dims)
+u = tb.make_velocity(m, "random:1")
+p = np.random.default_rng(3).uniform(-1, 1, m.n_nodes)
+P = tb.PhysParams()
+modes = ("private", "private-atomic") if "big" in sys.argv else tb.SCATTER_MODES
+for mode in modes:
+    tb.assemble_rsp(m, u, P, tb.RunConfig(scatter=mode))
+    tb.assemble_rsp(m, u, P, tb.RunConfig(scatter=mode), pressure=p)
+for fn in () if "big" in sys.argv else (tb.assemble_baseline, tb.assemble_rs):
+    fn(m, u, P, tb.RunConfig(scatter="atomic"))
+asm = tb.Assembler(m, tb.RunConfig(scatter="private-atomic", cta_patches=64, chunk_nodes=144))
+asm.assemble(u, P)
+asm.close()
+tb.clear_cache()
+print("sanitize workload done")
