@@ -45,10 +45,11 @@ def up_to_date() -> bool:
 
 
 def build(verbose: bool = False, force: bool = False, out: Path = OUT, defines=(),
-          tag: str = "") -> Path:
-    """Compile libtal_b200.so.  ``defines``/``out``/``tag`` build tuning
-    variants (e.g. ``TAL_RING_UNROLL=2``) side by side for A/B timing."""
-    if out == OUT and not defines and not force and up_to_date():
+          tag: str = "", nvcc_flags=()) -> Path:
+    """Compile libtal_b200.so.  ``defines``/``nvcc_flags``/``out``/``tag``
+    build tuning variants (e.g. ``TAL_RING_UNROLL=2``,
+    ``-Xptxas --register-usage-level=3``) side by side for A/B timing."""
+    if out == OUT and not defines and not nvcc_flags and not force and up_to_date():
         return OUT
     BUILD.mkdir(exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
@@ -63,7 +64,7 @@ def build(verbose: bool = False, force: bool = False, out: Path = OUT, defines=(
     for src in sorted(CSRC.glob("*.cu")):
         obj = BUILD / (src.stem + tag + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *dflags,
-               "-Xptxas", "-v", "--expt-relaxed-constexpr", "-c", str(src), "-o", str(obj)]
+               "-Xptxas", "-v", "--expt-relaxed-constexpr", *nvcc_flags, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, check=False, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:
