@@ -10,7 +10,8 @@ torchrun (N>1) every rank assembles its own 128^3 slab of a 128x128x(128N)
 box and the interface planes are summed over NCCL (weak scaling).
 
 One step = one full RHS assembly (zero/merge + element kernel) with inputs
-resident in HBM; L2 is flushed (256 MiB write) before every step, outside
+resident in HBM, replayed as one captured CUDA graph at N=1 (``--no-graph``:
+direct launches); L2 is flushed (256 MiB write) before every step, outside
 the CUDA-event-timed interval.  ``e2e`` repeats the step through the public
 host API (pinned host u -> H2D -> assembly -> D2H rhs) and times it by wall
 clock.  ``--impl reference`` times the reference algorithm's CPU port
@@ -56,6 +57,9 @@ def parse():
     ap.add_argument("--cta-patches", type=int, default=128)
     ap.add_argument("--chunk-nodes", type=int, default=256)
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N=1: launch each step's zeroing + kernel directly instead of replaying "
+                         "one captured CUDA graph per step (tal_graph_capture)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--permute", action="store_true", help="config 3: random node permutation")
@@ -274,7 +278,11 @@ def run_ours(a) -> None:
 
     stream = torch.cuda.current_stream().cuda_stream
 
+    use_graph = not a.no_graph and dom is None
+
     def one_step():
+        if use_graph:
+            return asm.replay(stream=stream)
         if dom is None:
             return asm.run(P, stream=stream, variant=a.variant)
         return dom.step(P, stream=stream)
@@ -312,6 +320,8 @@ def run_ours(a) -> None:
         if flush_buf is not None:
             flush_buf.fill_(1)
 
+    if use_graph:
+        asm.capture(P, variant=a.variant)
     asm.profile(True)
     for _ in range(max(a.warmup, 0)):
         flush()
@@ -341,6 +351,12 @@ def run_ours(a) -> None:
     wall1 = time.perf_counter()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     kern_ms = asm.profile_read()
+    if use_graph:  # the graph carries no profile events: time the kernel in plain steps
+        for _ in range(min(a.steps, 50)):
+            flush()
+            asm.run(P, stream=stream, variant=a.variant)
+        torch.cuda.synchronize()
+        kern_ms = asm.profile_read()
     total_ms = float(sum(step_ms))
     if dist:
         t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
@@ -485,7 +501,7 @@ def run_ours(a) -> None:
                    "renumber": a.renumber, "element_order": a.element_order,
                    "patches": a.patches, "cta_patches": a.cta_patches, "chunk_nodes": a.chunk_nodes,
                    "permuted": bool(a.permute), "variant": a.variant,
-                   "pressure_term": bool(a.pressure),
+                   "pressure_term": bool(a.pressure), "cuda_graph": bool(use_graph),
                    "l2": "flushed (256 MiB write) before every step, outside the timed events"
                          if flush_buf is not None else "not flushed",
                    "parallelism": (f"dp{ws} z-slabs" if a.partition == "slab" else f"dp{ws} RCB parts")

@@ -194,6 +194,14 @@ int tal_set_pressure_device(tal_handle *h, const double *d_p, void *stream);
 /* tal_run for any code shape (TAL_VARIANT_*) */
 int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter,
                     void *stream, int64_t *kernel_launches);
+/* CUDA graph of one assembly step (zeroing + kernels + merge) on the
+ * internal buffers, captured with the current parameters, variant, scatter
+ * and pressure setting; replay with tal_graph_launch on any stream.  Not for
+ * handles with attached peers (TAL_EINVAL).  Re-capture after changing any of
+ * them; the mesh upload destroys the graph. */
+int tal_graph_capture(tal_handle *h, const tal_params *p, int variant, int scatter);
+int tal_graph_launch(tal_handle *h, void *stream, int64_t *kernel_launches);
+int tal_graph_destroy(tal_handle *h);
 int tal_get_rhs_host(tal_handle *h, double *rhs, void *stream);
 int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream);
 int tal_synchronize(tal_handle *h, void *stream);

@@ -417,6 +417,22 @@ class Assembler:
                                         _stream(stream), ctypes.byref(nl)))
         return int(nl.value)
 
+    def capture(self, params: PhysParams, scatter: Optional[str] = None, pmat=None,
+                variant: VariantId = VariantId.RSP) -> None:
+        """Capture one assembly step (zeroing + kernels + merge) as a CUDA
+        graph (tal_graph_capture) for cheap replays with ``replay``."""
+        scatter = scatter or self.cfg.scatter
+        if scatter not in N.SCATTER:
+            raise ValueError(f"unknown scatter mode {scatter!r}")
+        N.check(N.lib().tal_graph_capture(self._h, ctypes.byref(_params(params, pmat)),
+                                          N.VARIANT[_variant_key(variant)], N.SCATTER[scatter]))
+
+    def replay(self, stream=None) -> int:
+        """Launch the captured step; returns the kernels it launches."""
+        nl = ctypes.c_int64(0)
+        N.check(N.lib().tal_graph_launch(self._h, _stream(stream), ctypes.byref(nl)))
+        return int(nl.value)
+
     def get_rhs_host(self, out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
         out = np.empty((self.n_nodes, 3)) if out is None else out
         N.check(N.lib().tal_get_rhs_host(self._h, N.ptr(out), _stream(stream)))

@@ -116,6 +116,16 @@ struct tal_handle {
     static constexpr int PROF_RING = 4096;
     bool prof_on = false;
     std::vector<cudaEvent_t> prof_ev;  // 2 per slot
+    // one captured assembly step (tal_graph_capture / tal_graph_launch)
+    cudaGraphExec_t gexec = nullptr;
+    int64_t g_launches = 0;
+    void free_graph()
+    {
+        if (gexec)
+            cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+        g_launches = 0;
+    }
     int64_t prof_head = 0, prof_count = 0;
 
     double *REC() const { return nodebuf; }
@@ -145,6 +155,7 @@ struct tal_handle {
 
     void free_mesh()
     {
+        free_graph();
         free_peers();
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
                         d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press};
@@ -1068,6 +1079,67 @@ int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter
         return rc;
     DeviceGuard g(h->device);
     return launch_any(h, p, variant, scatter, stream ? (cudaStream_t)stream : h->stream, kernel_launches);
+}
+
+int tal_graph_capture(tal_handle *h, const tal_params *p, int variant, int scatter)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    if (h->n_peers())
+        return fail(TAL_EINVAL, "graph capture of the fused interface sum is not supported "
+                                "(its flag epochs advance per step on the host)");
+    int rc = check_params(p);
+    if (rc)
+        return rc;
+    DeviceGuard g(h->device);
+    h->free_graph();
+    TAL_CK(cudaStreamSynchronize(h->stream));
+    TAL_CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    const bool prof = h->prof_on;
+    h->prof_on = false;  // the profile event ring is per call, not per replay
+    int64_t nl = 0;
+    rc = launch_any(h, p, variant, scatter, h->stream, &nl);
+    h->prof_on = prof;
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+    if (rc == TAL_OK && ce != cudaSuccess)
+        rc = fail(TAL_ECUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
+    if (rc == TAL_OK) {
+        const cudaError_t ie = cudaGraphInstantiate(&h->gexec, graph, 0);
+        if (ie != cudaSuccess) {
+            h->gexec = nullptr;
+            rc = fail(TAL_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+        }
+    }
+    if (graph)
+        cudaGraphDestroy(graph);
+    cudaGetLastError();
+    h->g_launches = rc == TAL_OK ? nl : 0;
+    return rc;
+}
+
+int tal_graph_launch(tal_handle *h, void *stream, int64_t *kernel_launches)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (!h->gexec)
+        return fail(TAL_ESTATE, "no captured graph (tal_graph_capture)");
+    DeviceGuard g(h->device);
+    TAL_CK(cudaGraphLaunch(h->gexec, stream ? (cudaStream_t)stream : h->stream));
+    if (kernel_launches)
+        *kernel_launches = h->g_launches;
+    return TAL_OK;
+}
+
+int tal_graph_destroy(tal_handle *h)
+{
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    DeviceGuard g(h->device);
+    h->free_graph();
+    return TAL_OK;
 }
 
 int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream)

@@ -464,3 +464,47 @@ def test_rcb_partitions_loopback_on_one_gpu(oracle, world):
         asm.close()
     assert not np.isnan(full).any()
     assert_parity(oracle, full, ref, g, ug)
+
+
+def test_cuda_graph_replay_matches_run(oracle):
+    """tal_graph_capture/launch: one captured step replays the assembly on the
+    handle's buffers -- bitwise equal to run() for 'private', picks up new
+    velocity and pressure contents, refuses handles with peers."""
+    import torch
+    m = tb.generate_box_mesh(12, 10, 9)
+    fields = [tb.make_velocity(m, f"random:{s}") for s in (1, 2)]
+    for scatter in ("private", "private-atomic", "atomic", "colored"):
+        asm = tb.Assembler(m, tb.RunConfig(scatter=scatter))
+        asm.set_velocity_host(fields[0], stream=0)
+        asm.run(P, stream=0)
+        ref = asm.get_rhs_host(stream=0)
+        asm.synchronize(stream=0)
+        asm.capture(P)
+        for u in fields:
+            asm.set_velocity_host(u, stream=0)
+            n = asm.replay(stream=0)
+            got = asm.get_rhs_host(stream=0)
+            asm.synchronize(stream=0)
+            assert n >= 1
+            want = oracle.assemble_rsp(m.coords, m.connectivity, u)
+            assert_parity(oracle, got, want, m, u)
+        asm.set_velocity_host(fields[0], stream=0)
+        asm.replay(stream=0)
+        again = asm.get_rhs_host(stream=0)
+        asm.synchronize(stream=0)
+        if scatter in ("private", "colored"):
+            np.testing.assert_array_equal(again, ref)
+        asm.close()
+    # pressure captured with the graph
+    p = np.random.default_rng(1).uniform(-1, 1, m.n_nodes)
+    asm = tb.Assembler(m, tb.RunConfig(scatter="private-atomic"))
+    asm.set_pressure(p)
+    asm.set_velocity_host(fields[1], stream=0)
+    asm.capture(P)
+    asm.replay(stream=torch.cuda.current_stream())
+    got = asm.get_rhs_host(stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    want = oracle.assemble_rsp(m.coords, m.connectivity, fields[1]) + \
+        oracle.pressure_gradient(m.coords, m.connectivity, p)
+    assert_parity(oracle, got, want, m, fields[1])
+    asm.close()
