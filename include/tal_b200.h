@@ -196,9 +196,11 @@ int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter
                     void *stream, int64_t *kernel_launches);
 /* CUDA graph of one assembly step (zeroing + kernels + merge) on the
  * internal buffers, captured with the current parameters, variant, scatter
- * and pressure setting; replay with tal_graph_launch on any stream.  Not for
- * handles with attached peers (TAL_EINVAL).  Re-capture after changing any of
- * them; the mesh upload destroys the graph. */
+ * and pressure setting; replay with tal_graph_launch on any stream.
+ * Re-capture after changing any of
+ * them (also after attaching peers); the mesh upload destroys the graph.  With
+ * peers attached the graph holds the whole fused step (flag epochs live on the
+ * device). */
 int tal_graph_capture(tal_handle *h, const tal_params *p, int variant, int scatter);
 int tal_graph_launch(tal_handle *h, void *stream, int64_t *kernel_launches);
 int tal_graph_destroy(tal_handle *h);

@@ -108,7 +108,6 @@ struct tal_handle {
     unsigned long long *d_flags = nullptr;  // own flag words (8): [0] zeroed, [1] done
     int32_t *d_pidx = nullptr;              // per chunk-node entry: slot<<30 | remote id
     std::vector<int32_t> h_pidx;
-    uint64_t peer_epoch = 0;
     std::vector<uint8_t> external;  // internal-id mask of nodes completed by peers
     tal_mesh_info info = {};
     tal_timings last = {};
@@ -137,6 +136,7 @@ struct tal_handle {
 
     void free_peers()
     {
+        free_graph();  // a captured step may hold the peer launches
         for (auto &p : peers) {
             if (p.ipc_rhs)
                 cudaIpcCloseMemHandle(p.ipc_rhs);
@@ -148,7 +148,6 @@ struct tal_handle {
             cudaFree(d_pidx);
         d_pidx = nullptr;
         h_pidx.clear();
-        peer_epoch = 0;
         if (d_flags)
             cudaMemset(d_flags, 0, 8 * sizeof(unsigned long long));
     }
@@ -403,9 +402,8 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             nl += TAL_ZERO_KERNEL;
         }
         if (np) {  // every neighbour has zeroed before anyone REDs into it
-            ++h->peer_epoch;
-            k_peer_signal<<<1, 1, 0, s>>>(h->peers[0].flags, h->peers[1].flags, 0);
-            k_peer_wait<<<1, 1, 0, s>>>(h->d_flags, 0, h->peer_epoch * np);
+            k_peer_signal<<<1, 1, 0, s>>>(h->peers[0].flags, h->peers[1].flags, 0, h->d_flags + 2);
+            k_peer_wait<<<1, 1, 0, s>>>(h->d_flags, 0, np);
             TAL_CK_LAUNCH();
             nl += 2;
         }
@@ -420,8 +418,8 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             ++nl;
         }
         if (np) {  // every neighbour's REDs into this RHS have landed
-            k_peer_signal<<<1, 1, 0, s>>>(h->peers[0].flags, h->peers[1].flags, 1);
-            k_peer_wait<<<1, 1, 0, s>>>(h->d_flags, 1, h->peer_epoch * np);
+            k_peer_signal<<<1, 1, 0, s>>>(h->peers[0].flags, h->peers[1].flags, 1, nullptr);
+            k_peer_wait<<<1, 1, 0, s>>>(h->d_flags, 1, np);
             TAL_CK_LAUNCH();
             nl += 2;
         }
@@ -1087,9 +1085,6 @@ int tal_graph_capture(tal_handle *h, const tal_params *p, int variant, int scatt
         return fail(TAL_EINVAL, "handle is NULL");
     if (!h->has_mesh)
         return fail(TAL_ESTATE, "no mesh uploaded");
-    if (h->n_peers())
-        return fail(TAL_EINVAL, "graph capture of the fused interface sum is not supported "
-                                "(its flag epochs advance per step on the host)");
     int rc = check_params(p);
     if (rc)
         return rc;
@@ -1554,6 +1549,8 @@ int tal_peer_attach(tal_handle *h, int slot, double *peer_rx, int64_t peer_n_nod
                     unsigned long long *peer_flags, const int64_t *my_ids, const int32_t *peer_ids,
                     int64_t n)
 {
+    if (h)
+        h->free_graph();  // captured without this neighbour
     if (!h || slot < 0 || slot > 1 || !peer_rx || !peer_flags || peer_n_nodes <= 0 || n < 0 ||
         (n && (!my_ids || !peer_ids)))
         return fail(TAL_EINVAL, "bad arguments");

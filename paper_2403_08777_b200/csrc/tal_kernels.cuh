@@ -567,9 +567,14 @@ __global__ void __launch_bounds__(256) k_unpack_aos(const double *__restrict__ r
 
 // cross-rank ordering of the fused interface sum: a rank signals each
 // neighbour (system-scope add on the neighbour's flag word) and waits until
-// its own flag word reached the epoch target
-__global__ void k_peer_signal(unsigned long long *f0, unsigned long long *f1, int which)
+// its own flag word reached epoch x n_neighbours.  The step epoch is a device
+// word (own flags[2], advanced by the first signal of a step), so a step is
+// free of host-side state and can be captured in a CUDA graph.
+__global__ void k_peer_signal(unsigned long long *f0, unsigned long long *f1, int which,
+                              unsigned long long *own_epoch)
 {
+    if (own_epoch)
+        own_epoch[0] += 1ull;
     __threadfence_system();
     if (f0)
         atomicAdd_system(f0 + which, 1ull);
@@ -577,8 +582,9 @@ __global__ void k_peer_signal(unsigned long long *f0, unsigned long long *f1, in
         atomicAdd_system(f1 + which, 1ull);
 }
 
-__global__ void k_peer_wait(const unsigned long long *flags, int which, unsigned long long target)
+__global__ void k_peer_wait(const unsigned long long *flags, int which, int n_peers)
 {
+    const unsigned long long target = flags[2] * (unsigned long long)n_peers;
     for (;;) {
         unsigned long long v;
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + which) : "memory");

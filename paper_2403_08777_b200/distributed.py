@@ -274,6 +274,7 @@ class SlabDomain:
         dev = torch.device("cuda", self.cfg.device)
         self._lists, self._send, self._recv = {}, {}, {}
         self.fused_error = None
+        self._graph_params = None
         if self.fused:
             if self._connect_peers(ifaces):
                 return
@@ -320,11 +321,16 @@ class SlabDomain:
         return u
 
     def step(self, params, stream=0) -> int:
-        """One assembly including the interface sum; returns kernels launched."""
+        """One assembly including the interface sum; returns kernels launched.
+        Fused: the whole step (zeroing, flag signals/waits, kernel) is one
+        captured CUDA graph, re-captured when ``params`` change."""
         asm = self.assembler
-        n = asm.run(params, stream=stream)
         if self.fused:
-            return n
+            if self._graph_params != params:
+                asm.capture(params)
+                self._graph_params = params
+            return asm.replay(stream=stream)
+        n = asm.run(params, stream=stream)
         for nbr, lst in self._lists.items():
             asm.halo_pack(lst.data_ptr(), lst.numel(), self._send[nbr].data_ptr(), stream=stream)
             n += 1
@@ -375,7 +381,7 @@ class PartitionedDomain(SlabDomain):
         self.part = MeshPartition(mesh, rank, world, parts)
         self.cfg = cfg or RunConfig()
         self.mesh = self.part.local_mesh()
-        self.fused, self.fused_error = False, None
+        self.fused, self.fused_error, self._graph_params = False, None, None
         self.assembler = Assembler(self.mesh, self.cfg)
         dev = torch.device("cuda", self.cfg.device)
         self._lists, self._send, self._recv = {}, {}, {}

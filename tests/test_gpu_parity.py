@@ -405,9 +405,15 @@ def test_fused_interface_sum_in_process(oracle, world):
     g = oracle.box_mesh(*cells)
     ug = oracle.velocity(g.coords, "random:1")
     ref = oracle.assemble_rsp(g.coords, g.connectivity, ug)
-    for step in range(3):
+    for step in range(5):
+        if step == 3:  # then as captured CUDA graphs (device-side flag epochs)
+            for p, m, asm in doms:
+                asm.capture(P)
         for p, m, asm in doms:
-            asm.run(P)  # internal streams: the ranks' flag waits overlap
+            if step < 3:
+                asm.run(P)  # internal streams: the ranks' flag waits overlap
+            else:
+                asm.replay()
         full = np.full_like(ref, np.nan)
         for p, m, asm in doms:
             loc = asm.get_rhs_host()
