@@ -243,6 +243,9 @@ bool make_consts(const tal_params *p, ElemConsts &kc, bool &sym)
         }
     kc.a_po = -p->rho * po / 24.0;
     kc.a_q = -p->rho * (pd - po) / 24.0;
+    kc.a_4 = 4.0 * kc.a_po + kc.a_q;
+    kc.rc6 = -kc.rc / 6.0;
+    kc.mu6 = -p->mu / 6.0;
     return std::isfinite(p->rho) && std::isfinite(p->mu) && std::isfinite(p->c_vreman);
 }
 

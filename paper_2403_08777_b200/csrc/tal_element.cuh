@@ -40,6 +40,9 @@ struct ElemConsts {
     double rc;    // rho * c_vreman
     double a_po;  // -rho * po / 24
     double a_q;   // -rho * (pd - po) / 24
+    double a_4;   // 4 a_po + a_q
+    double rc6;   // -rho * c_vreman / 6
+    double mu6;   // -mu / 6
     double pm[16];  // full pmat (general kernel only)
 };
 
@@ -70,7 +73,8 @@ __device__ __forceinline__ double rcbrt_fast(double x)
     const double e = fma(-m, (y * y) * y, 1.0);
     const double p = fma(e, fma(e, 14.0 / 81.0, 2.0 / 9.0), 1.0 / 3.0);
     y = fma(y * e, p, y);
-    return y * __hiloint2double((1023 - k) << 20, 0);
+    // y in (0.5, 1]: scale by 2^-k in the exponent field (INT pipe, no DMUL)
+    return __hiloint2double(__double2hiint(y) - (k << 20), __double2loint(y));
 }
 
 // t^(-1/2) for normal positive t: MUFU.RSQ64H seed + one third-order
@@ -89,6 +93,12 @@ __device__ __forceinline__ bool is_normal_pos(double x)
 {
     const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
     return e - 1u < 2046u;
+}
+
+// |x| on the INT pipe (fabs compiles to a DADD)
+__device__ __forceinline__ double abs_bits(double x)
+{
+    return __hiloint2double(__double2hiint(x) & 0x7fffffff, __double2loint(x));
 }
 
 // x with the sign of s flipped into it (x * sgn(s) for s != 0), integer ops only
@@ -120,21 +130,27 @@ __device__ __forceinline__ void pressure_add(double pbar, double det, const doub
 // weighted terms.  c[1..3] = cofactor rows, D = det, du[b] = u_b - u_0
 // (b = 1..3), U = the four corner velocities.  R = 4x3 element RHS; with
 // ACC the FMA chains of R start from R's incoming values (the ring kernel
-// folds its running sums into them instead of separate adds).
-template <bool ACC>
+// folds its running sums into them instead of separate adds).  With NEG3 the
+// c3 argument holds -c3 (the ring kernel carries c2 of the previous tet; the
+// negation becomes a free operand modifier instead of three DADDs).
+template <bool ACC, bool NEG3 = false>
 __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3], const double c3[3],
                                          double det, const double du1[3], const double du2[3],
                                          const double du3[3], const double U0[3], const double U1[3],
                                          const double S01[3], const double U2[3], const double U3[3],
                                          const ElemConsts &k, double R[4][3])
 {
-    const double ad = fabs(det);
+    const double ad = abs_bits(det);
+    double c3v[3];
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk)
+        c3v[kk] = NEG3 ? -c3[kk] : c3[kk];
     double Gh[3][3];
 #pragma unroll
     for (int kk = 0; kk < 3; ++kk)
 #pragma unroll
         for (int i = 0; i < 3; ++i)
-            Gh[kk][i] = fma(c1[kk], du1[i], fma(c2[kk], du2[i], c3[kk] * du3[i]));
+            Gh[kk][i] = fma(c1[kk], du1[i], fma(c2[kk], du2[i], c3v[kk] * du3[i]));
 
     // |Gh|^2 (three row partial sums) and the nine squared 2x2 minors
     // (rows m<n, columns i<j; three column-pair partial sums)
@@ -159,13 +175,12 @@ __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3],
     const double t = ssqh * aah;
     const double r3 = is_normal_pos(ad) ? rcbrt_fast(ad) : rcbrt(ad);
     const double inv = (r3 * r3) * r3;  // 1/|D|
-    double f = 0.0;                     // rho * nu_t / ssqh
+    double f = 0.0;                     // -rho * nu_t / (6 ssqh)
     if (aah * inv * inv > 1e-30 && t > 0.0)  // kernel.py:24 guard, in G units
-        f = (k.rc * r3) * (is_normal_pos(t) ? rsqrt_fast(t) : rsqrt(t));
-    const double vis = fma(f, ssqh, k.mu);  // mu + rho nu_t
-    const double B = vis * (inv * (-1.0 / 6.0));
+        f = (k.rc6 * r3) * (is_normal_pos(t) ? rsqrt_fast(t) : rsqrt(t));
+    const double B = fma(f, ssqh, k.mu6) * inv;  // -(mu + rho nu_t) / (6 |D|)
     const double As = mul_sign(k.a_po, det), Aq = mul_sign(k.a_q, det);
-    const double A4 = fma(4.0, As, Aq);
+    const double A4 = mul_sign(k.a_4, det);
     double w[4][3];
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
@@ -173,7 +188,7 @@ __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3],
         const double AsS = As * S;
         w[1][cc] = fma(Aq, U1[cc], fma(B, c1[cc], AsS));
         w[2][cc] = fma(Aq, U2[cc], fma(B, c2[cc], AsS));
-        w[3][cc] = fma(Aq, U3[cc], fma(B, c3[cc], AsS));
+        w[3][cc] = fma(Aq, U3[cc], fma(B, c3v[cc], AsS));
         // sum_a w_a = (4 As + Aq) S because the cofactor rows sum to zero
         w[0][cc] = fma(A4, S, -((w[1][cc] + w[2][cc]) + w[3][cc]));
     }

@@ -354,7 +354,8 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
             // ring recurrences for tet t = (a, b, r_t, r_t+1):
             //   e1 = x_b - x_a, du1 = u_b - u_a (patch constants),
             //   e2(t) = e3(t-1), du2(t) = du3(t-1), c3(t) = e1 x e2(t) = -c2(t-1)
-            double Xa[3], Ua[3], Ub[3], S01[3], e1[3], du1[3], e2[3], du2[3], U2[3], c3[3];
+            // (carried as nc3 = -c3 = c2(t-1): tet_tail<.., NEG3> folds the sign)
+            double Xa[3], Ua[3], Ub[3], S01[3], e1[3], du1[3], e2[3], du2[3], U2[3], nc3[3];
             {
                 double Xb[3], Xr[3];
                 load_record_s(nr, ID(1), Xa, Ua);
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
                     e2[q] = Xr[q] - Xa[q];
                     du2[q] = U2[q] - Ua[q];
                 }
-                cross3(e1, e2, c3);
+                cross3(e2, e1, nc3);
             }
             // R[0], R[1] carry the running sums of a and b, R[2] enters with the
             // previous tet's contribution to r_t and leaves complete for r_t,
@@ -392,9 +393,10 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
                 cross3(e2, e3, c1);
                 cross3(e3, e1, c2);
                 const double det = fma(e1[0], c1[0], fma(e1[1], c1[1], e1[2] * c1[2]));
-                tet_tail<true>(c1, c2, c3, det, du1, du2, du3, Ua, Ub, S01, U2, U3, kc, R);
+                tet_tail<true, true>(c1, c2, nc3, det, du1, du2, du3, Ua, Ub, S01, U2, U3, kc, R);
                 if (PR) {
                     const double p3 = pres_s[ID(3 + nxt)];
+                    const double c3[3] = {-nc3[0], -nc3[1], -nc3[2]};
                     pressure_add(0.25 * (pab + (p2 + p3)), det, c1, c2, c3, R);
                     p2 = p3;
                 }
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
                     e2[q] = e3[q];
                     du2[q] = du3[q];
                     U2[q] = U3[q];
-                    c3[q] = -c2[q];
+                    nc3[q] = c2[q];
                 }
             }
             double *carry = R[2], *acc_a = R[0], *acc_b = R[1];
