@@ -151,6 +151,12 @@ int tal_mesh_info_get(tal_handle *h, tal_mesh_info *out);
 int tal_plan_layout(const double *coords, const int64_t *conn, int64_t n_nodes,
                     int64_t n_elems, const tal_mesh_opts *opts, tal_mesh_info *out);
 int tal_default_mesh_opts(tal_mesh_opts *out);
+/* Layout diagnostic, summed over every chunking built in this process:
+ * out[0] = quarter-warp record-load groups of the ring walk, out[1] / out[2] =
+ * estimated shared-memory wavefronts of those loads with ascending-id slots /
+ * with the bank-aware placement used (TAL_BANK_PLACE=0 in the environment
+ * disables it; ideal = out[0]). */
+int tal_layout_bank_stats(int64_t out[3]);
 
 /* ---- assembly ------------------------------------------------------------- */
 /* End-to-end drop-in for assemble_rsp's kernel loop (variants.py:572-615):

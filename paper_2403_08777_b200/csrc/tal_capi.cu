@@ -929,6 +929,14 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
     return TAL_OK;
 }
 
+int tal_layout_bank_stats(int64_t out[3])
+{
+    if (!out)
+        return fail(TAL_EINVAL, "out is NULL");
+    bank_stats(out, out + 1, out + 2);
+    return TAL_OK;
+}
+
 int tal_plan_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
                     const tal_mesh_opts *opts_in, tal_mesh_info *out)
 {

@@ -2,6 +2,8 @@
 #include "tal_prep.hpp"
 
 #include <algorithm>
+#include <array>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -482,6 +484,179 @@ void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int m
     }
 }
 
+// ---------------------------------------------------------------------------
+// Bank-aware placement of a chunk's node records in shared memory.
+//
+// Phase B loads a 48-B record per ring node with three LDS.128; a quarter-warp
+// (8 lanes) is served conflict-free only if its 8 records sit in distinct
+// 16-B bank groups, i.e. (3 j + s) mod 8 distinct for record slot j -- which
+// holds iff the slots are distinct mod 8.  Every load instruction of the ring
+// walk (a, b, r_0, then r_{t+1} at tet t) defines, per quarter-warp, a group
+// of nodes; the placement colours nodes with the 8 residues (capacity
+// ceil((nn - c) / 8) each) minimising the sum over groups of colliding pairs:
+// greedy by group count, then pairwise-swap descent.  Returns the slot order.
+// ---------------------------------------------------------------------------
+namespace {
+struct BankStats {
+    int64_t groups = 0, wave_before = 0, wave_after = 0;
+};
+BankStats g_bank;
+
+int bank_place_mode()
+{
+    static int mode = [] {
+        const char *e = std::getenv("TAL_BANK_PLACE");
+        return e ? std::atoi(e) : 1;
+    }();
+    return mode;
+}
+
+void bank_place(const Patches &P, int64_t p0, int64_t p1, std::vector<int32_t> &nodes,
+                std::vector<int32_t> &idx)
+{
+    const int nn = (int)nodes.size();
+    for (int i = 0; i < nn; ++i)
+        idx[nodes[i]] = i;
+    constexpr int NI = 3 + PATCH_MAX_RING;  // load instructions of one ring walk
+    const int64_t npat = p1 - p0;
+    const int nq = (int)((npat + 7) / 8);
+    const int ng = nq * NI;
+    std::vector<std::vector<int32_t>> gm((size_t)ng);
+    for (int64_t g = p0; g < p1; ++g) {
+        const int q = (int)((g - p0) >> 3);
+        const int32_t *v = P.nodes.data() + P.off[g];
+        const int m = P.off[g + 1] - P.off[g] - 2;
+        const int k = P.closed[g] ? m : m - 1;
+        gm[(size_t)q * NI + 0].push_back(idx[v[0]]);
+        gm[(size_t)q * NI + 1].push_back(idx[v[1]]);
+        gm[(size_t)q * NI + 2].push_back(idx[v[2]]);
+        for (int t = 0; t < k; ++t)
+            gm[(size_t)q * NI + 3 + t].push_back(idx[v[2 + (t + 1 == m ? 0 : t + 1)]]);
+    }
+    std::vector<std::vector<int32_t>> ng_of((size_t)nn);  // groups of each node
+    for (int G = 0; G < ng; ++G) {
+        auto &v = gm[G];
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        for (int32_t i : v)
+            ng_of[i].push_back(G);
+    }
+    std::vector<int> cls(nn, -1), cap(8), used(8, 0);
+    for (int c = 0; c < 8; ++c)
+        cap[c] = (nn - c + 7) / 8;
+    std::vector<std::array<int, 8>> cnt((size_t)ng);
+    for (auto &a : cnt)
+        a.fill(0);
+    auto waves = [&]() {
+        int64_t w = 0;
+        for (int G = 0; G < ng; ++G)
+            if (!gm[G].empty())
+                w += *std::max_element(cnt[G].begin(), cnt[G].end());
+        return w;
+    };
+    // before: ascending node id in slot order
+    for (int i = 0; i < nn; ++i)
+        for (int G : ng_of[i])
+            cnt[G][i & 7]++;
+    int64_t groups = 0;
+    for (int G = 0; G < ng; ++G)
+        groups += !gm[G].empty();
+    const int64_t before = waves();
+    for (auto &a : cnt)
+        a.fill(0);
+    std::vector<int> ord(nn);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](int x, int y) { return ng_of[x].size() > ng_of[y].size(); });
+    for (int i : ord) {
+        int best = -1;
+        int64_t bc = 0;
+        for (int c = 0; c < 8; ++c) {
+            if (used[c] >= cap[c])
+                continue;
+            int64_t cost = 0;
+            for (int G : ng_of[i])
+                cost += cnt[G][c];
+            cost = cost * 1024 + used[c];
+            if (best < 0 || cost < bc)
+                best = c, bc = cost;
+        }
+        cls[i] = best;
+        used[best]++;
+        for (int G : ng_of[i])
+            cnt[G][best]++;
+    }
+    std::vector<std::vector<int32_t>> members(8);
+    for (int i = 0; i < nn; ++i)
+        members[cls[i]].push_back(i);
+    std::vector<int> mark((size_t)ng, -1);
+    auto move_cost = [&](int i, int from, int to) {  // colliding-pair change of moving i
+        int64_t d = 0;
+        for (int G : ng_of[i])
+            d += cnt[G][to] - (cnt[G][from] - 1);
+        return d;
+    };
+    for (int pass = 0; pass < 4; ++pass) {
+        bool any = false;
+        for (int u = 0; u < nn; ++u) {
+            const int a = cls[u];
+            int64_t best = 0;
+            int bv = -1;
+            for (int b = 0; b < 8; ++b) {
+                if (b == a)
+                    continue;
+                const int64_t mu = move_cost(u, a, b);
+                if (mu >= 0)
+                    continue;
+                for (int G : ng_of[u])
+                    mark[G] = u;
+                for (int32_t v : members[b]) {
+                    int shared = 0;
+                    for (int G : ng_of[v])
+                        shared += mark[G] == u;
+                    const int64_t d = mu + move_cost(v, b, a) - 2 * shared;
+                    if (d < best)
+                        best = d, bv = v;
+                }
+                for (int G : ng_of[u])
+                    mark[G] = -1;
+            }
+            if (bv < 0)
+                continue;
+            const int b = cls[bv];
+            for (int G : ng_of[u])
+                cnt[G][a]--, cnt[G][b]++;
+            for (int G : ng_of[bv])
+                cnt[G][b]--, cnt[G][a]++;
+            cls[u] = b, cls[bv] = a;
+            auto &ma = members[a], &mb = members[b];
+            *std::find(ma.begin(), ma.end(), u) = bv;
+            *std::find(mb.begin(), mb.end(), bv) = u;
+            any = true;
+        }
+        if (!any)
+            break;
+    }
+    g_bank.groups += groups;
+    g_bank.wave_before += before;
+    g_bank.wave_after += waves();
+    // slot j = c + 8 r: class c's members in ascending node id
+    std::vector<int32_t> out((size_t)nn);
+    for (int c = 0; c < 8; ++c) {
+        auto &mc = members[c];
+        std::sort(mc.begin(), mc.end());
+        for (size_t r = 0; r < mc.size(); ++r)
+            out[(size_t)c + 8 * r] = nodes[mc[r]];
+    }
+    nodes.swap(out);
+}
+}  // namespace
+
+void bank_stats(int64_t *groups, int64_t *before, int64_t *after)
+{
+    *groups = g_bank.groups, *before = g_bank.wave_before, *after = g_bank.wave_after;
+}
+
 bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_nodes, int max_contrib,
                   const uint8_t *external, Chunking &out, std::string &err)
 {
@@ -506,6 +681,8 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
     auto close_chunk = [&](int64_t p_end) {
         std::vector<int32_t> sorted(nodes);
         std::sort(sorted.begin(), sorted.end());  // local ids: ascending node id (gather order)
+        if (bank_place_mode())                    // or bank-aware slots (above)
+            bank_place(P, p_begin, p_end, sorted, local);
         const int32_t nn = (int32_t)sorted.size();
         for (int32_t j = 0; j < nn; ++j)
             local[sorted[j]] = j;

@@ -253,3 +253,21 @@ def test_plan_layout_general_mesh_and_errors():
     object.__setattr__(bad, "connectivity", base.connectivity + base.n_nodes)
     with pytest.raises(ValueError):
         plan_layout(bad)
+
+
+def test_bank_aware_record_placement_reduces_conflicts():
+    """The chunk record slots are coloured mod 8 (tal_prep.cpp bank_place):
+    the estimated LDS.128 wavefronts of the ring walk's record loads drop
+    against ascending-id slots and never go below one per quarter-warp."""
+    import ctypes
+    from paper_2403_08777_b200 import _native as N
+    from paper_2403_08777_b200.mesh import plan_layout
+    a0 = (ctypes.c_int64 * 3)()
+    N.lib().tal_layout_bank_stats(a0)
+    plan_layout(tb.generate_box_mesh(24, 16, 16))
+    a1 = (ctypes.c_int64 * 3)()
+    N.lib().tal_layout_bank_stats(a1)
+    groups, before, after = (a1[i] - a0[i] for i in range(3))
+    assert groups > 0
+    assert groups <= after < before
+    assert after / groups < 1.6 < before / groups
