@@ -287,30 +287,8 @@ def run_ours(a) -> None:
             return asm.run(P, stream=stream, variant=a.variant)
         return dom.step(P, stream=stream)
 
-    # parity + CPU baseline (rank 0, N=1): the oracle as checker / baseline only
     parity = None
     cpu_baseline = None
-    if ws == 1 and not a.no_cpu_baseline:
-        from oracle import oracle as O
-        O.build()
-        T = O.default_threads()
-        rhs_gpu, _ = asm.assemble(u, P, variant=a.variant)
-        O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)  # warm-up
-        ts = []
-        ref = None
-        for _ in range(3):
-            t1 = time.perf_counter()
-            ref = O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)
-            ts.append(time.perf_counter() - t1)
-        med = statistics.median(ts)
-        cpu_baseline = {"value": E / med, "unit": "elem/s", "cores": T, "kind": "port",
-                        "sample": f"full {c}^3 mesh ({E} tets), {a.init}; C port of the reference "
-                                  f"numba kernel + private driver, 1 warm-up + median of 3"}
-        if press is not None:
-            ref = ref + O.pressure_gradient(mesh.coords, mesh.connectivity, press)
-        chk = O.compare(rhs_gpu, ref, mesh.coords, mesh.connectivity, u)
-        parity = {"reference_rel_diff": chk.rel_diff, "rel_l2": chk.rel_l2,
-                  "entry_rel": chk.entry_rel, "passed": bool(chk.passed)}
 
     asm.set_velocity_host(u, stream=stream)
     flush_buf = None if a.no_flush else torch.empty(64 * 1024 * 1024, dtype=torch.int32,
@@ -377,7 +355,7 @@ def run_ours(a) -> None:
         pr = [N.PinnedArray((Nn, 3)) for _ in range(NSLOT)]
         for p_ in pu:
             p_.array[:] = u
-        ksteps = max(min(a.steps, 50), 3)
+        ksteps = max(min(a.steps, 200), 3)
         for _ in range(2):
             asm.assemble_into(pu[0].array, P, pr[0].array, a.scatter)
         torch.cuda.synchronize()
@@ -455,6 +433,30 @@ def run_ours(a) -> None:
                       + " (pinned), wall clock, max over ranks"}
         for p_ in pu + pr:
             p_.free()
+    # parity + CPU baseline (rank 0, N=1): the oracle as checker / baseline only.
+    # Runs after the e2e leg: its 16-thread host load right before the pinned
+    # copies was observed to depress the e2e number (9.3 vs 11.6 Gelem/s).
+    if ws == 1 and not a.no_cpu_baseline:
+        from oracle import oracle as O
+        O.build()
+        T = O.default_threads()
+        rhs_gpu, _ = asm.assemble(u, P, variant=a.variant)
+        O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)  # warm-up
+        ts = []
+        ref = None
+        for _ in range(3):
+            t1 = time.perf_counter()
+            ref = O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)
+            ts.append(time.perf_counter() - t1)
+        med = statistics.median(ts)
+        cpu_baseline = {"value": E / med, "unit": "elem/s", "cores": T, "kind": "port",
+                        "sample": f"full {c}^3 mesh ({E} tets), {a.init}; C port of the reference "
+                                  f"numba kernel + private driver, 1 warm-up + median of 3"}
+        if press is not None:
+            ref = ref + O.pressure_gradient(mesh.coords, mesh.connectivity, press)
+        chk = O.compare(rhs_gpu, ref, mesh.coords, mesh.connectivity, u)
+        parity = {"reference_rel_diff": chk.rel_diff, "rel_l2": chk.rel_l2,
+                  "entry_rel": chk.entry_rel, "passed": bool(chk.passed)}
     if dom is not None and a.check:  # N>1 parity: owned rows of every rank vs the oracle
         torch.cuda.synchronize()
         rows = [None] * ws
