@@ -487,7 +487,8 @@ def run_ours(a) -> None:
     hbm_peak, hbm_src = measured_hbm_peak()
     kname = {"private": "k_assemble_private<cfg,ordered=true>",
              "private-atomic": "k_assemble_private<cfg,ordered=false>",
-             "atomic": "k_assemble_atomic<true>", "colored": "k_assemble_colored<true> (all colours)"}[a.scatter]
+             "atomic": "k_assemble_atomic<true>", "colored": "k_assemble_colored<true> (all colours)",
+             "sequential": "k_assemble_sequential (reference order, strict IEEE)"}[a.scatter]
     if a.variant != "rsp":
         colored = a.scatter in ("private", "colored")
         kname = {"b": "k_assemble_baseline", "p": "k_assemble_baseline<fixed>",

@@ -51,6 +51,10 @@ extern "C" {
 #define TAL_SCATTER_COLORED 1        /* colour-by-colour plain read-modify-write: bitwise reproducible */
 #define TAL_SCATTER_ATOMIC 2         /* 12 FP64 REDs per element */
 #define TAL_SCATTER_PRIVATE_ATOMIC 3 /* CTA-private smem sums, FP64 RED per shared node */
+#define TAL_SCATTER_SEQUENTIAL 4     /* reference order: the numba kernel's operation order (no
+                                        FMA contraction) summed node by node in ascending element
+                                        id -- bitwise identical to the reference's one-thread
+                                        assemble_rsp; parity/debug path (4x the arithmetic) */
 
 /* code shapes of the paper's study (variants.py:28-60 VariantId).
  * RSP is the production path (all scatter modes above); B and RS are the

@@ -17,7 +17,7 @@ LIB_PATH = Path(os.environ.get("TAL_LIB_PATH") or Path(__file__).resolve().paren
 
 TAL_OK, TAL_EINVAL, TAL_ECUDA, TAL_ENOMEM, TAL_ESTATE = 0, 1, 2, 3, 4
 
-SCATTER = {"private": 0, "colored": 1, "atomic": 2, "private-atomic": 3}
+SCATTER = {"private": 0, "colored": 1, "atomic": 2, "private-atomic": 3, "sequential": 4}
 VARIANT = {"b": 0, "rs": 1, "rsp": 2, "p": 3}  # TAL_VARIANT_* ("p": study-only shape)
 RENUMBER = {"none": 0, "rcm": 1, "sfc": 2}
 EORDER = {"keep": 0, "node": 1, "sfc": 2}

@@ -63,7 +63,12 @@ class RunConfig:
     * ``colored``        colour-by-colour plain read-modify-write (bitwise
                          reproducible; uses ``mesh.colors`` or a greedy colouring),
     * ``atomic``         12 FP64 REDs per element,
-    * ``private-atomic`` CTA-private sums, one FP64 RED per shared node.
+    * ``private-atomic`` CTA-private sums, one FP64 RED per shared node,
+    * ``sequential``     reference order: the numba kernel's operations without
+                         FMA contraction, summed node by node in ascending
+                         element id -- bitwise identical to the reference's
+                         one-thread ``assemble_rsp`` (parity/debug path,
+                         tal_strict.cuh; 4x the arithmetic).
 
     GPU knobs: ``device``, ``renumber`` (rcm | sfc | none), ``element_order``
     (sfc | node | keep), ``patches`` (star: edge-star patches, the rings of

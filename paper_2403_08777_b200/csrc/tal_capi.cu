@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -15,6 +16,7 @@
 
 #include "../../include/tal_b200.h"
 #include "tal_kernels.cuh"
+#include "tal_strict.cuh"
 #include "tal_prep.hpp"
 #include "tal_shapes.cuh"
 
@@ -85,6 +87,11 @@ struct tal_handle {
     int32_t *perm = nullptr, *iperm = nullptr;
     std::vector<int32_t> h_iperm;  // caller -> internal (host)
     int4 *conn = nullptr;          // element order of the chunking
+    std::vector<int32_t> h_eperm;  // conn row -> caller element id (empty: identity)
+    // reference-order scatter (built on first use): node -> incident conn rows
+    int64_t *d_seq_off = nullptr;  // N+1
+    int32_t *d_seq_ent = nullptr;  // 4E: row << 2 | corner, ascending caller element id
+    double *d_seq_dlt = nullptr;   // E: Vreman filter width cbrt(6 vol) per conn row (host libm)
     // colouring
     int4 *conn_col = nullptr;
     std::vector<int64_t> col_off;
@@ -157,11 +164,15 @@ struct tal_handle {
         free_graph();
         free_peers();
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
-                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press};
+                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press, d_seq_off, d_seq_ent, d_seq_dlt};
         for (void *p : ptrs)
             if (p)
                 cudaFree(p);
         nodebuf = staging = d_partial = d_press = nullptr;
+        d_seq_off = nullptr;
+        d_seq_ent = nullptr;
+        d_seq_dlt = nullptr;
+        h_eperm.clear();
         has_press = false;
         for (int s = 0; s < ASYNC_SLOTS; ++s) {
             if (astage_u[s])
@@ -315,6 +326,60 @@ struct ProfMark {
     }
 };
 
+// node -> (conn row, corner) lists in ascending caller element id, for the
+// reference-order scatter; built on the host from the device connectivity
+int build_sequential(tal_handle *h)
+{
+    const int64_t N = h->N, E = h->E;
+    if (4 * E > INT32_MAX)
+        return fail(TAL_EINVAL, "scatter 'sequential' supports up to 2^29 elements");
+    std::vector<int32_t> cord((size_t)(4 * E));
+    if (E)
+        TAL_CK(cudaMemcpy(cord.data(), h->conn, sizeof(int32_t) * 4 * E, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> row((size_t)E);  // caller element id -> conn row
+    for (int64_t e = 0; e < E; ++e)
+        row[h->h_eperm.empty() ? e : h->h_eperm[e]] = (int32_t)e;
+    std::vector<int64_t> off((size_t)N + 1, 0);
+    for (int64_t i = 0; i < 4 * E; ++i)
+        off[cord[i] + 1]++;
+    for (int64_t v = 0; v < N; ++v)
+        off[v + 1] += off[v];
+    std::vector<int64_t> fill(off.begin(), off.end() - 1);
+    std::vector<int32_t> ent((size_t)(4 * E));
+    for (int64_t eo = 0; eo < E; ++eo) {
+        const int32_t r = row[eo];
+        for (int a = 0; a < 4; ++a)
+            ent[fill[cord[4 * (int64_t)r + a]]++] = r << 2 | a;
+    }
+    // filter width per element, _rsp_kernels.py:45-62 in the reference's
+    // operation order (baseline x86-64 code: no FMA contraction possible) and
+    // the reference's libm pow -- see tal_strict.cuh for why on the host
+    std::vector<double> rec((size_t)(6 * N));
+    if (N)
+        TAL_CK(cudaMemcpy(rec.data(), h->REC(), sizeof(double) * 6 * N, cudaMemcpyDeviceToHost));
+    std::vector<double> dlt((size_t)E);
+    for (int64_t e = 0; e < E; ++e) {
+        const double *x0 = &rec[6 * (int64_t)cord[4 * e]];
+        double ed[4][3];
+        for (int b = 1; b < 4; ++b)
+            for (int c = 0; c < 3; ++c)
+                ed[b][c] = rec[6 * (int64_t)cord[4 * e + b] + c] - x0[c];
+        const double c0 = ed[2][1] * ed[3][2] - ed[2][2] * ed[3][1];
+        const double c1 = ed[2][2] * ed[3][0] - ed[2][0] * ed[3][2];
+        const double c2 = ed[2][0] * ed[3][1] - ed[2][1] * ed[3][0];
+        const double det = ed[1][0] * c0 + ed[1][1] * c1 + ed[1][2] * c2;
+        const double x = 6.0 * (std::fabs(det) / 6.0);
+        dlt[e] = std::isnan(x) ? x : std::pow(x, 1.0 / 3.0);  // numba np.cbrt, x >= 0
+    }
+    if (int rc = dev_upload(&h->d_seq_off, off.data(), off.size()))
+        return rc;
+    if (!E)
+        return TAL_OK;
+    if (int rc = dev_upload(&h->d_seq_dlt, dlt.data(), dlt.size()))
+        return rc;
+    return dev_upload(&h->d_seq_ent, ent.data(), ent.size());
+}
+
 int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, int64_t *launches)
 {
     ProfMark pm{h, s};
@@ -430,6 +495,24 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         if (ordered && nb) {
             k_merge_partials<<<grid_for(nb, 256), 256, 0, s>>>(h->d_bnd_nodes, h->d_bnd_off, h->d_bnd_pos,
                                                               nb, pa.part, rhs);
+            TAL_CK_LAUNCH();
+            ++nl;
+        }
+        break;
+    }
+    case TAL_SCATTER_SEQUENTIAL: {
+        if (h->has_press)
+            return fail(TAL_EINVAL, "scatter 'sequential' reproduces the reference operator, which has no "
+                                    "pressure term; clear the pressure first");
+        if (N && !h->d_seq_off)
+            if (int rc = build_sequential(h))
+                return rc;
+        if (N) {
+            pm.begin();
+            k_assemble_sequential<<<grid_for(N, 128), 128, 0, s>>>(h->d_seq_off, h->d_seq_ent, N, h->conn,
+                                                                  nodes, h->d_seq_dlt, rhs.rx, rhs.ry,
+                                                                  rhs.rz, kc);
+            pm.end();
             TAL_CK_LAUNCH();
             ++nl;
         }
@@ -917,6 +1000,7 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
         return rc;
     TAL_CK(cudaDeviceSynchronize());
 
+    h->h_eperm.swap(eperm);
     h->has_mesh = true;
     h->info.n_nodes = n_nodes;
     h->info.n_elems = n_elems;
@@ -1102,6 +1186,10 @@ int tal_graph_capture(tal_handle *h, const tal_params *p, int variant, int scatt
     DeviceGuard g(h->device);
     h->free_graph();
     TAL_CK(cudaStreamSynchronize(h->stream));
+    // lazily built tables (allocation + copies) cannot happen inside a capture
+    if (scatter == TAL_SCATTER_SEQUENTIAL && h->N && !h->d_seq_off)
+        if ((rc = build_sequential(h)))
+            return rc;
     TAL_CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     const bool prof = h->prof_on;
     h->prof_on = false;  // the profile event ring is per call, not per replay
