@@ -227,6 +227,17 @@ int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
                           double rho, double mu, double cvre,
                           const double *pmat, const int64_t *ids, int64_t k,
                           double *rhs);
+/* Same signature and semantics, bitwise identical to the numba loop: every
+ * node continues from its incoming rhs value through its elements in ids
+ * order, element arithmetic in the reference's operation order without FMA
+ * contraction (tal_strict.cuh).  Dropped into the reference's own driver
+ * (variants.py:573-596, any thread count), it reproduces assemble_rsp bit for
+ * bit. */
+int tal_assemble_elements_strict(int device, const double *coords, const int64_t *conn,
+                                 int64_t n_nodes, int64_t n_elems, const double *u,
+                                 double rho, double mu, double cvre,
+                                 const double *pmat, const int64_t *ids, int64_t k,
+                                 double *rhs);
 
 /* ---- multi-GPU interface (domain decomposition) ----------------------------- */
 /* Gather rhs of internal node ids list[0..n) into a packed buffer d_out

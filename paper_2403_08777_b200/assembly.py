@@ -618,9 +618,13 @@ def assemble(variant: VariantId, mesh, u, params, cfg=None) -> AssemblyResult:
     return ASSEMBLERS[variant](mesh, u, params, cfg)
 
 
-def assemble_elements(coords, conn, u, rho, mu, cvre, pmat, ids, rhs, device: int = 0) -> None:
+def assemble_elements(coords, conn, u, rho, mu, cvre, pmat, ids, rhs, device: int = 0,
+                      strict: bool = False) -> None:
     """The numba seam ``_rsp_kernels.assemble_elements`` on the GPU: assemble
-    elements ``ids`` and ADD into ``rhs`` (in place, like the numba loop)."""
+    elements ``ids`` and ADD into ``rhs`` (in place, like the numba loop).
+    ``strict=True`` (``tal_assemble_elements_strict``) is bitwise the numba
+    loop: each node continues from its incoming ``rhs`` through its elements in
+    ``ids`` order with the reference's operation order (tal_strict.cuh)."""
     coords = np.ascontiguousarray(coords, dtype=np.float64)
     conn = np.ascontiguousarray(conn, dtype=np.int64)
     u = np.ascontiguousarray(u, dtype=np.float64)
@@ -631,7 +635,8 @@ def assemble_elements(coords, conn, u, rho, mu, cvre, pmat, ids, rhs, device: in
     if coords.shape[1:] != (3,) or conn.shape[1:] != (4,) or u.shape != coords.shape \
             or rhs.shape != coords.shape or pm.shape != (4, 4):
         raise ValueError("bad array shapes")
-    N.check(N.lib().tal_assemble_elements(device, N.ptr(coords), N.ptr(conn), coords.shape[0],
+    fn = N.lib().tal_assemble_elements_strict if strict else N.lib().tal_assemble_elements
+    N.check(fn(device, N.ptr(coords), N.ptr(conn), coords.shape[0],
                                           conn.shape[0], N.ptr(u), float(rho), float(mu),
                                           float(cvre), N.ptr(pm), N.ptr(ids), ids.shape[0],
                                           N.ptr(rhs)))

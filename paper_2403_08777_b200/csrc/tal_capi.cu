@@ -326,6 +326,26 @@ struct ProfMark {
     }
 };
 
+// Vreman filter width delta = cbrt(6 vol) of one element as the reference
+// computes it (_rsp_kernels.py:45-62: edges, cofactor row 1, det, vol, numba's
+// np.cbrt = libm pow(x, 1/3)); host code, baseline x86-64 (no FMA contraction
+// possible).  xyz: node coordinates with 'stride' doubles per node.
+template <class Id>
+double filter_width(const double *xyz, int stride, const Id *nodes4)
+{
+    const double *x0 = xyz + stride * (int64_t)nodes4[0];
+    double ed[4][3];
+    for (int b = 1; b < 4; ++b)
+        for (int c = 0; c < 3; ++c)
+            ed[b][c] = xyz[stride * (int64_t)nodes4[b] + c] - x0[c];
+    const double c0 = ed[2][1] * ed[3][2] - ed[2][2] * ed[3][1];
+    const double c1 = ed[2][2] * ed[3][0] - ed[2][0] * ed[3][2];
+    const double c2 = ed[2][0] * ed[3][1] - ed[2][1] * ed[3][0];
+    const double det = ed[1][0] * c0 + ed[1][1] * c1 + ed[1][2] * c2;
+    const double x = 6.0 * (std::fabs(det) / 6.0);
+    return std::isnan(x) ? x : std::pow(x, 1.0 / 3.0);  // x >= 0: the sign-symmetric branch is moot
+}
+
 // node -> (conn row, corner) lists in ascending caller element id, for the
 // reference-order scatter; built on the host from the device connectivity
 int build_sequential(tal_handle *h)
@@ -358,19 +378,8 @@ int build_sequential(tal_handle *h)
     if (N)
         TAL_CK(cudaMemcpy(rec.data(), h->REC(), sizeof(double) * 6 * N, cudaMemcpyDeviceToHost));
     std::vector<double> dlt((size_t)E);
-    for (int64_t e = 0; e < E; ++e) {
-        const double *x0 = &rec[6 * (int64_t)cord[4 * e]];
-        double ed[4][3];
-        for (int b = 1; b < 4; ++b)
-            for (int c = 0; c < 3; ++c)
-                ed[b][c] = rec[6 * (int64_t)cord[4 * e + b] + c] - x0[c];
-        const double c0 = ed[2][1] * ed[3][2] - ed[2][2] * ed[3][1];
-        const double c1 = ed[2][2] * ed[3][0] - ed[2][0] * ed[3][2];
-        const double c2 = ed[2][0] * ed[3][1] - ed[2][1] * ed[3][0];
-        const double det = ed[1][0] * c0 + ed[1][1] * c1 + ed[1][2] * c2;
-        const double x = 6.0 * (std::fabs(det) / 6.0);
-        dlt[e] = std::isnan(x) ? x : std::pow(x, 1.0 / 3.0);  // numba np.cbrt, x >= 0
-    }
+    for (int64_t e = 0; e < E; ++e)
+        dlt[e] = filter_width(rec.data(), 6, &cord[4 * e]);
     if (int rc = dev_upload(&h->d_seq_off, off.data(), off.size()))
         return rc;
     if (!E)
@@ -511,7 +520,7 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             pm.begin();
             k_assemble_sequential<<<grid_for(N, 128), 128, 0, s>>>(h->d_seq_off, h->d_seq_ent, N, h->conn,
                                                                   nodes, h->d_seq_dlt, rhs.rx, rhs.ry,
-                                                                  rhs.rz, kc);
+                                                                  rhs.rz, kc, false);
             pm.end();
             TAL_CK_LAUNCH();
             ++nl;
@@ -1399,9 +1408,15 @@ int tal_assemble_variant(tal_handle *h, const double *u, const tal_params *p, do
     return TAL_OK;
 }
 
-int tal_assemble_elements(int device, const double *coords, const int64_t *conn, int64_t n_nodes,
-                          int64_t n_elems, const double *u, double rho, double mu, double cvre,
-                          const double *pmat, const int64_t *ids, int64_t k, double *rhs)
+namespace {
+// the numba seam (_rsp_kernels.py:20-164): elements ids[0..k) ADDED into rhs.
+// strict=false: one thread per element, FP64 REDs into a zeroed buffer, added
+// to rhs on the host (parity to tolerance).  strict=true: tal_strict.cuh --
+// each node continues from its incoming rhs value through its elements in
+// ids order with the reference's operation order: bitwise the numba loop.
+int seam_impl(int device, const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
+              const double *u, double rho, double mu, double cvre, const double *pmat, const int64_t *ids,
+              int64_t k, double *rhs, bool strict)
 {
     if (n_nodes < 0 || n_elems < 0 || k < 0)
         return fail(TAL_EINVAL, "negative sizes");
@@ -1445,8 +1460,36 @@ int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
             soa[6 * i + c] = coords[3 * i + c];  // node records x y z ux uy uz
             soa[6 * i + 3 + c] = u[3 * i + c];
         }
-    double *buf = nullptr;
+    // strict: incoming rhs as SoA start values; node -> (entry t, corner) in
+    // ids order; filter width per entry from the host libm (tal_strict.cuh)
+    std::vector<double> rin, dlt;
+    std::vector<int64_t> off;
+    std::vector<int32_t> ent;
+    if (strict) {
+        if (4 * k > INT32_MAX)
+            return fail(TAL_EINVAL, "strict seam supports up to 2^29 element ids per call");
+        rin.resize((size_t)(3 * n_nodes));
+        for (int64_t i = 0; i < n_nodes; ++i)
+            for (int c = 0; c < 3; ++c)
+                rin[c * n_nodes + i] = rhs[3 * i + c];
+        off.assign((size_t)n_nodes + 1, 0);
+        for (int64_t i = 0; i < 4 * k; ++i)
+            off[sub[i] + 1]++;
+        for (int64_t v = 0; v < n_nodes; ++v)
+            off[v + 1] += off[v];
+        std::vector<int64_t> fill(off.begin(), off.end() - 1);
+        ent.resize((size_t)(4 * k));
+        dlt.resize((size_t)k);
+        for (int64_t t = 0; t < k; ++t) {
+            for (int a = 0; a < 4; ++a)
+                ent[fill[sub[4 * t + a]]++] = (int32_t)(t << 2 | a);
+            dlt[t] = filter_width(coords, 3, &sub[4 * t]);
+        }
+    }
+    double *buf = nullptr, *ddlt = nullptr;
     int4 *dconn = nullptr;
+    int64_t *doff = nullptr;
+    int32_t *dent = nullptr;
     TAL_CK(cudaMalloc((void **)&buf, sizeof(double) * 9 * n_nodes));
     rc = TAL_OK;
     do {
@@ -1454,14 +1497,31 @@ int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
         if ((e = cudaMalloc((void **)&dconn, sizeof(int4) * k)) != cudaSuccess ||
             (e = cudaMemcpy(buf, soa.data(), sizeof(double) * 6 * n_nodes, cudaMemcpyHostToDevice)) !=
                 cudaSuccess ||
-            (e = cudaMemset(buf + 6 * n_nodes, 0, sizeof(double) * 3 * n_nodes)) != cudaSuccess ||
+            (e = strict ? cudaMemcpy(buf + 6 * n_nodes, rin.data(), sizeof(double) * 3 * n_nodes,
+                                     cudaMemcpyHostToDevice)
+                        : cudaMemset(buf + 6 * n_nodes, 0, sizeof(double) * 3 * n_nodes)) != cudaSuccess ||
             (e = cudaMemcpy(dconn, sub.data(), sizeof(int4) * k, cudaMemcpyHostToDevice)) != cudaSuccess) {
+            rc = fail(TAL_ECUDA, std::string("assemble_elements upload: ") + cudaGetErrorString(e));
+            break;
+        }
+        if (strict && ((e = cudaMalloc((void **)&doff, sizeof(int64_t) * off.size())) != cudaSuccess ||
+                       (e = cudaMalloc((void **)&dent, sizeof(int32_t) * ent.size())) != cudaSuccess ||
+                       (e = cudaMalloc((void **)&ddlt, sizeof(double) * dlt.size())) != cudaSuccess ||
+                       (e = cudaMemcpy(doff, off.data(), sizeof(int64_t) * off.size(),
+                                       cudaMemcpyHostToDevice)) != cudaSuccess ||
+                       (e = cudaMemcpy(dent, ent.data(), sizeof(int32_t) * ent.size(),
+                                       cudaMemcpyHostToDevice)) != cudaSuccess ||
+                       (e = cudaMemcpy(ddlt, dlt.data(), sizeof(double) * dlt.size(),
+                                       cudaMemcpyHostToDevice)) != cudaSuccess)) {
             rc = fail(TAL_ECUDA, std::string("assemble_elements upload: ") + cudaGetErrorString(e));
             break;
         }
         const double *nodes = buf;
         RhsSoA r{buf + 6 * n_nodes, buf + 7 * n_nodes, buf + 8 * n_nodes};
-        if (sym)
+        if (strict)
+            k_assemble_sequential<<<grid_for(n_nodes, 128), 128>>>(doff, dent, n_nodes, dconn, nodes, ddlt,
+                                                                   r.rx, r.ry, r.rz, kc, true);
+        else if (sym)
             k_assemble_atomic<true><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc, nullptr);
         else
             k_assemble_atomic<false><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc, nullptr);
@@ -1475,13 +1535,33 @@ int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
             break;
         }
         for (int64_t i = 0; i < n_nodes; ++i)
-            for (int c = 0; c < 3; ++c)
-                rhs[3 * i + c] += soa[c * n_nodes + i];
+            for (int c = 0; c < 3; ++c) {
+                if (strict)
+                    rhs[3 * i + c] = soa[c * n_nodes + i];  // accumulated on the device
+                else
+                    rhs[3 * i + c] += soa[c * n_nodes + i];
+            }
     } while (0);
-    cudaFree(buf);
-    if (dconn)
-        cudaFree(dconn);
+    void *tmp[] = {buf, dconn, doff, dent, ddlt};
+    for (void *q : tmp)
+        if (q)
+            cudaFree(q);
     return rc;
+}
+}  // namespace
+
+int tal_assemble_elements(int device, const double *coords, const int64_t *conn, int64_t n_nodes,
+                          int64_t n_elems, const double *u, double rho, double mu, double cvre,
+                          const double *pmat, const int64_t *ids, int64_t k, double *rhs)
+{
+    return seam_impl(device, coords, conn, n_nodes, n_elems, u, rho, mu, cvre, pmat, ids, k, rhs, false);
+}
+
+int tal_assemble_elements_strict(int device, const double *coords, const int64_t *conn, int64_t n_nodes,
+                                 int64_t n_elems, const double *u, double rho, double mu, double cvre,
+                                 const double *pmat, const int64_t *ids, int64_t k, double *rhs)
+{
+    return seam_impl(device, coords, conn, n_nodes, n_elems, u, rho, mu, cvre, pmat, ids, k, rhs, true);
 }
 
 int tal_halo_pack(tal_handle *h, const int32_t *d_list, int64_t n, double *d_out, void *stream)

@@ -126,18 +126,23 @@ __device__ __forceinline__ void element_row_strict(const double X[4][3], const d
 // One thread per node v (internal numbering): its incident elements in
 // ascending caller element id (CSR ent[off[v] .. off[v+1]), entry = e << 2 | a
 // with e the row of 'conn' and a the node's corner), summed in that order from
-// zero -- the reference's one-accumulator private loop, node by node.
+// zero -- the reference's one-accumulator private loop, node by node.  With
+// 'accumulate' the sums start from the incoming rx/ry/rz (the numba seam's
+// rhs += semantics, tal_assemble_elements_strict).
 __global__ void __launch_bounds__(128) k_assemble_sequential(const int64_t *__restrict__ off,
                                                              const int32_t *__restrict__ ent, int64_t n_nodes,
                                                              const int4 *__restrict__ conn,
                                                              const double *__restrict__ nrec,
                                                              const double *__restrict__ dlt, double *rx,
-                                                             double *ry, double *rz, ElemConsts kc)
+                                                             double *ry, double *rz, ElemConsts kc,
+                                                             bool accumulate)
 {
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n_nodes)
         return;
     double acc[3] = {0.0, 0.0, 0.0};
+    if (accumulate)
+        acc[0] = rx[v], acc[1] = ry[v], acc[2] = rz[v];
     for (int64_t k = off[v]; k < off[v + 1]; ++k) {
         const int32_t en = __ldg(ent + k);
         const int4 q = __ldg(conn + (en >> 2));
