@@ -215,6 +215,9 @@ struct PrivCfg<0> {  // 64 patches / chunk
 #define TAL_RING_UNROLL 1
 #endif
 constexpr int kRingUnroll = TAL_RING_UNROLL;
+#ifndef TAL_GATHER_COOP
+#define TAL_GATHER_COOP 1
+#endif
 #ifndef TAL_DIAG_NO_C
 #define TAL_DIAG_NO_C 0
 #endif
@@ -298,6 +301,18 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);
         const int32_t *gl = reinterpret_cast<const int32_t *>(bl + 16 + L::TABLES + 2 * BLOB_LEVELS);
         double *dst = nrec_s;
+#if TAL_GATHER_COOP
+        // 16-B segment per lane, lane-consecutive segments: a warp's copies
+        // cover ~11 contiguous records (fewer L1 sectors / smem wavefronts
+        // per instruction than one record per lane)
+        for (int q = tid; q < 3 * hdr.y; q += T) {
+            const int j = q / 3, sg = q - 3 * j;
+            cp_async16(dst + 6 * j + 2 * sg, nrec_g + 6 * (int64_t)gl[j] + 2 * sg);
+        }
+        if (PR)
+            for (int j = tid; j < hdr.y; j += T)
+                cp_async8(pres_s + j, pa.press + gl[j]);
+#else
         for (int j = tid; j < hdr.y; j += T) {
             const double *src = nrec_g + 6 * (int64_t)gl[j];
             cp_async16(dst + 6 * j, src);
@@ -306,6 +321,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
             if (PR)
                 cp_async8(pres_s + j, pa.press + gl[j]);
         }
+#endif
         cp_async_commit();
     };
 
