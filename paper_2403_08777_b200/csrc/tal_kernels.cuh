@@ -221,6 +221,9 @@ constexpr int kRingUnroll = TAL_RING_UNROLL;
 #ifndef TAL_DIAG_NO_C
 #define TAL_DIAG_NO_C 0
 #endif
+#ifndef TAL_DIAG_NO_GATHER
+#define TAL_DIAG_NO_GATHER 0
+#endif
 
 template <>
 struct PrivCfg<1> {  // 128 patches / chunk
@@ -456,7 +459,9 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
         // phase B(i) is done; its blob has had all of phase B(i) to land
         if (i + 1 < n_my) {
             mbar_wait(&bar[b ^ 1], ((i + 1) >> 1) & 1);
+#if !TAL_DIAG_NO_GATHER  // diagnostic build only (results wrong): cost of the record gather
             gather(b ^ 1);
+#endif
         }
 
         // phase C: one node per thread, nodes in rank order (contribution count
