@@ -335,6 +335,9 @@ def run_ours(a) -> None:
             asm.run(P, stream=stream, variant=a.variant)
         torch.cuda.synchronize()
         kern_ms = asm.profile_read()
+    # nvidia-smi polls the driver every 50 ms: stop it before the wall-clock
+    # e2e leg (observed to depress e2e to 9-10 Gelem/s from 11.6)
+    clocks = sampler.stop()
     total_ms = float(sum(step_ms))
     if dist:
         t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
@@ -434,8 +437,7 @@ def run_ours(a) -> None:
         for p_ in pu + pr:
             p_.free()
     # parity + CPU baseline (rank 0, N=1): the oracle as checker / baseline only.
-    # Runs after the e2e leg: its 16-thread host load right before the pinned
-    # copies was observed to depress the e2e number (9.3 vs 11.6 Gelem/s).
+    # Runs after the e2e leg, so its 16-thread host load cannot disturb it.
     if ws == 1 and not a.no_cpu_baseline:
         from oracle import oracle as O
         O.build()
@@ -477,7 +479,6 @@ def run_ours(a) -> None:
             parity = {"reference_rel_diff": chk.rel_diff, "rel_l2": chk.rel_l2,
                       "entry_rel": chk.entry_rel, "passed": bool(chk.passed),
                       "gathered": f"owned rows of {ws} ranks vs single-domain oracle"}
-    clocks = sampler.stop()
     asm.profile(False)
 
     kmean = float(np.mean(kern_ms)) if len(kern_ms) else float("nan")

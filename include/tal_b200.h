@@ -158,9 +158,11 @@ int tal_default_mesh_opts(tal_mesh_opts *out);
 /* Layout diagnostic, summed over every chunking built in this process:
  * out[0] = quarter-warp record-load groups of the ring walk, out[1] / out[2] =
  * estimated shared-memory wavefronts of those loads with ascending-id slots /
- * with the bank-aware placement used (TAL_BANK_PLACE=0 in the environment
- * disables it; ideal = out[0]). */
-int tal_layout_bank_stats(int64_t out[3]);
+ * with the bank-aware placement used; out[3..5] = the same for the half-warp
+ * contribution stores (STS.64) before / after the bank-aware level and rank
+ * choice.  Ideal = out[0] / out[3].  TAL_BANK_PLACE=0 / TAL_POS_PLACE=0 in the
+ * environment disable the two placements. */
+int tal_layout_bank_stats(int64_t out[6]);
 
 /* ---- assembly ------------------------------------------------------------- */
 /* End-to-end drop-in for assemble_rsp's kernel loop (variants.py:572-615):

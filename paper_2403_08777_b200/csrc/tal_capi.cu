@@ -1022,11 +1022,12 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
     return TAL_OK;
 }
 
-int tal_layout_bank_stats(int64_t out[3])
+int tal_layout_bank_stats(int64_t out[6])
 {
     if (!out)
         return fail(TAL_EINVAL, "out is NULL");
     bank_stats(out, out + 1, out + 2);
+    pos_stats(out + 3, out + 4, out + 5);
     return TAL_OK;
 }
 

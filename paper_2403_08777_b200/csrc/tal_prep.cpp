@@ -657,6 +657,147 @@ void bank_stats(int64_t *groups, int64_t *before, int64_t *after)
     *groups = g_bank.groups, *before = g_bank.wave_before, *after = g_bank.wave_after;
 }
 
+// ---------------------------------------------------------------------------
+// Bank-aware contribution positions.  Phase B stores each patch node's sum at
+// p = lev[s] + rank[node] (three 8-B arrays); a half-warp (16 lanes) of one
+// STS.64 is conflict-free iff its positions are distinct mod 16.  Free
+// choices that keep the jagged layout valid: which of a node's contributions
+// takes which level s, and the rank order among nodes of equal contribution
+// count.  Pairwise-swap descent on the colliding pairs per (half-warp, store
+// instruction) group over the level choice (rank swaps among equal counts,
+// measured: 1.95 -> 1.87 wavefronts per group for 2.5x the host prep time,
+// are not done).  'lvl' (in: patch-order levels, out: chosen levels) is
+// indexed like the patch-order contribution enumeration of close_chunk.
+// ---------------------------------------------------------------------------
+namespace {
+BankStats g_pos;
+
+#ifndef POS_PASSES
+#define POS_PASSES 2
+#endif
+int pos_place_mode()
+{
+    static int mode = [] {
+        const char *e = std::getenv("TAL_POS_PLACE");
+        return e ? std::atoi(e) : 1;
+    }();
+    return mode;
+}
+
+void pos_place(const Patches &P, int64_t p0, int64_t p1, const std::vector<int32_t> &local,
+               const std::vector<int32_t> &ncnt, std::vector<int32_t> &order, std::vector<int32_t> &rank,
+               const uint16_t *lev, std::vector<int32_t> &lvl)
+{
+    constexpr int NI = PATCH_MAX_RING + 3;  // loop stores, then ring end, a, b
+    const int nn = (int)rank.size();
+    const int64_t npat = p1 - p0;
+    const int ng = (int)((npat + 15) / 16) * NI;
+    struct Con {
+        int32_t node, g0, g1;  // g1 = -1 or the second group (closed ring's r_0 RMW)
+    };
+    std::vector<Con> con;
+    con.reserve((size_t)npat * (PATCH_MAX_RING + 2));
+    for (int64_t g = p0; g < p1; ++g) {
+        const int32_t *v = P.nodes.data() + P.off[g];
+        const int m = P.off[g + 1] - P.off[g] - 2;
+        const bool closed = P.closed[g];
+        const int kk = closed ? m : m - 1;
+        const int base = (int)((g - p0) >> 4) * NI;
+        for (int k = 0; k < m + 2; ++k) {
+            Con c{local[v[k]], -1, -1};
+            if (k == 0)
+                c.g0 = base + PATCH_MAX_RING + 1;
+            else if (k == 1)
+                c.g0 = base + PATCH_MAX_RING + 2;
+            else {
+                const int i = k - 2;
+                if (i < kk)
+                    c.g0 = base + i;
+                if ((closed && i == 0) || (!closed && i == m - 1))
+                    (c.g0 < 0 ? c.g0 : c.g1) = base + PATCH_MAX_RING;
+            }
+            con.push_back(c);
+        }
+    }
+    const int nc = (int)con.size();
+    std::vector<std::vector<int32_t>> of_node((size_t)nn);  // contributions per node
+    for (int c = 0; c < nc; ++c)
+        of_node[con[c].node].push_back(c);
+    std::vector<std::array<int16_t, 16>> cnt((size_t)ng);
+    for (auto &a : cnt)
+        a.fill(0);
+    auto cls = [&](int c) { return (lev[lvl[c]] + rank[con[c].node]) & 15; };
+    auto add = [&](int c, int d) {  // returns the pair-count change of adding (d=+1) / removing (d=-1)
+        const int k = cls(c);
+        int64_t delta = 0;
+        for (int G : {con[c].g0, con[c].g1})
+            if (G >= 0) {
+                if (d > 0)
+                    delta += cnt[G][k]++;
+                else
+                    delta -= --cnt[G][k];
+            }
+        return delta;
+    };
+    auto waves = [&]() {
+        int64_t w = 0, groups = 0;
+        for (int G = 0; G < ng; ++G) {
+            int mx = 0, tot = 0;
+            for (int x : cnt[G])
+                mx = std::max(mx, x), tot += x;
+            w += mx;
+            groups += tot > 0;
+        }
+        return std::make_pair(w, groups);
+    };
+    for (int c = 0; c < nc; ++c)
+        add(c, +1);
+    const auto before = waves();
+    // try a change: remove the affected contributions, mutate, re-add; keep if better
+    auto attempt = [&](const std::vector<int32_t> &cs, auto &&mutate, auto &&undo) {
+        int64_t d = 0;
+        for (int c : cs)
+            d += add(c, -1);
+        mutate();
+        for (int c : cs)
+            d += add(c, +1);
+        if (d < 0)
+            return true;
+        for (int c : cs)
+            add(c, -1);
+        undo();
+        for (int c : cs)
+            add(c, +1);
+        return false;
+    };
+    std::vector<int32_t> cs;
+    for (int pass = 0; pass < POS_PASSES; ++pass) {
+        bool any = false;
+        // (a) level swaps between two contributions of one node
+        for (int j = 0; j < nn; ++j) {
+            auto &L = of_node[j];
+            for (size_t x = 0; x < L.size(); ++x)
+                for (size_t y = x + 1; y < L.size(); ++y) {
+                    const int a = L[x], b = L[y];
+                    cs = {a, b};
+                    any |= attempt(cs, [&] { std::swap(lvl[a], lvl[b]); }, [&] { std::swap(lvl[a], lvl[b]); });
+                }
+        }
+        if (!any)
+            break;
+    }
+    const auto after = waves();
+    g_pos.groups += before.second;
+    g_pos.wave_before += before.first;
+    g_pos.wave_after += after.first;
+}
+}  // namespace
+
+void pos_stats(int64_t *groups, int64_t *before, int64_t *after)
+{
+    *groups = g_pos.groups, *before = g_pos.wave_before, *after = g_pos.wave_after;
+}
+
 bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_nodes, int max_contrib,
                   const uint8_t *external, Chunking &out, std::string &err)
 {
@@ -674,7 +815,7 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
     out.ppos.assign((size_t)np * PATCH_SLOTS, 0);
     std::vector<int32_t> stamp((size_t)n_nodes, -1), local((size_t)n_nodes, 0), cnt((size_t)n_nodes, 0);
     std::vector<int32_t> cnt_chunks((size_t)n_nodes, 0);
-    std::vector<int32_t> nodes, order, rank, fill;
+    std::vector<int32_t> nodes, order, rank, fill, lvl, ncnt;
     int32_t chunk = 0;
     int64_t p_begin = 0, contrib = 0;
 
@@ -702,6 +843,19 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
                 alive += cnt[sorted[order[q]]] > s - 1;
             lev[s] = (uint16_t)(lev[s - 1] + alive);
         }
+        // levels of the patch-order contributions (fill order), then the
+        // bank-aware choice of levels / equal-count ranks (above)
+        fill.assign(nn, 0);
+        lvl.clear();
+        for (int64_t g = p_begin; g < p_end; ++g)
+            for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k)
+                lvl.push_back(fill[local[P.nodes[k]]]++);
+        if (pos_place_mode()) {
+            ncnt.resize(nn);
+            for (int32_t j = 0; j < nn; ++j)
+                ncnt[j] = cnt[sorted[j]];
+            pos_place(P, p_begin, p_end, local, ncnt, order, rank, lev, lvl);
+        }
         const size_t node_begin = out.cnodes.size();
         for (int32_t j = 0; j < nn; ++j)
             out.gather_nodes.push_back(sorted[j]);
@@ -713,7 +867,7 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
         }
         for (int s = 0; s < CHUNK_LEVELS; ++s)
             out.levels.push_back(lev[s]);
-        fill.assign(nn, 0);  // contributions placed so far per local node (patch order)
+        size_t ci = 0;  // contribution index in patch order (lvl)
         for (int64_t g = p_begin; g < p_end; ++g) {
             uint16_t *ids = out.pids.data() + PATCH_SLOTS * g, *pos = out.ppos.data() + PATCH_SLOTS * g;
             const int32_t m = P.off[g + 1] - P.off[g] - 2;
@@ -721,7 +875,7 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
             for (int32_t k = 0; k < m + 2; ++k) {
                 const int32_t l = local[P.nodes[P.off[g] + k]];
                 ids[1 + k] = (uint16_t)l;
-                pos[1 + k] = (uint16_t)(lev[fill[l]++] + rank[l]);
+                pos[1 + k] = (uint16_t)(lev[lvl[ci++]] + rank[l]);
             }
         }
         for (int32_t v : sorted)

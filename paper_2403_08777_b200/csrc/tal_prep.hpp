@@ -75,6 +75,9 @@ bool build_chunks(const Patches &p, int64_t n_nodes, int max_patches, int max_no
 // Estimated LDS.128 wavefronts of the ring walk's record loads, summed over
 // all chunks built so far (quarter-warp groups, before/after bank placement).
 void bank_stats(int64_t *groups, int64_t *before, int64_t *after);
+// Same for the phase-B contribution stores (half-warp STS.64 groups, before /
+// after the bank-aware level and rank choice).
+void pos_stats(int64_t *groups, int64_t *before, int64_t *after);
 // One contiguous 16-B aligned record per chunk (layout: tal_kernels.cuh,
 // patch tables transposed with stride 'cta_threads'); blob_off in 16-B units.
 void pack_blobs(const Chunking &ch, int cta_threads, std::vector<uint8_t> &blobs,

@@ -262,12 +262,14 @@ def test_bank_aware_record_placement_reduces_conflicts():
     import ctypes
     from paper_2403_08777_b200 import _native as N
     from paper_2403_08777_b200.mesh import plan_layout
-    a0 = (ctypes.c_int64 * 3)()
+    a0 = (ctypes.c_int64 * 6)()
     N.lib().tal_layout_bank_stats(a0)
     plan_layout(tb.generate_box_mesh(24, 16, 16))
-    a1 = (ctypes.c_int64 * 3)()
+    a1 = (ctypes.c_int64 * 6)()
     N.lib().tal_layout_bank_stats(a1)
-    groups, before, after = (a1[i] - a0[i] for i in range(3))
-    assert groups > 0
+    groups, before, after, sgroups, sbefore, safter = (a1[i] - a0[i] for i in range(6))
+    assert groups > 0 and sgroups > 0
     assert groups <= after < before
     assert after / groups < 1.6 < before / groups
+    # contribution stores (half-warp STS.64 groups): levels / equal-count ranks
+    assert sgroups <= safter < sbefore
