@@ -155,6 +155,15 @@ int tal_mesh_info_get(tal_handle *h, tal_mesh_info *out);
 int tal_plan_layout(const double *coords, const int64_t *conn, int64_t n_nodes,
                     int64_t n_elems, const tal_mesh_opts *opts, tal_mesh_info *out);
 int tal_default_mesh_opts(tal_mesh_opts *out);
+/* Host-only dump of the private-scatter chunk blobs tal_upload_mesh_ex would
+ * build (layout: csrc/tal_kernels.cuh at k_assemble_private), for inspection
+ * and CPU-side layout tests.  Call once with NULL buffers to get sizes[0] =
+ * blob bytes, [1] = blob_off entries (16-B units, n_chunks+1), [2] = CTA
+ * threads (table stride), [3] = perm entries (internal -> caller node id; 0 =
+ * identity); then again with buffers of those sizes. */
+int tal_plan_blobs(const double *coords, const int64_t *conn, int64_t n_nodes,
+                   int64_t n_elems, const tal_mesh_opts *opts, int64_t sizes[4],
+                   uint8_t *blobs, int32_t *blob_off, int32_t *perm);
 /* Layout diagnostic, summed over every chunking built in this process:
  * out[0] = quarter-warp record-load groups of the ring walk, out[1] / out[2] =
  * estimated shared-memory wavefronts of those loads with ascending-id slots /

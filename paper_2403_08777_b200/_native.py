@@ -74,6 +74,7 @@ SIGNATURES = [
     ("tal_upload_mesh_ex", _I, [_P, _P, _P, _I64, _I64, _P, ctypes.POINTER(TalMeshOpts), _P, _I64]),
     ("tal_mesh_info_get", _I, [_P, ctypes.POINTER(TalMeshInfo)]),
     ("tal_layout_bank_stats", _I, [_P]),
+    ("tal_plan_blobs", _I, [_P, _P, _I64, _I64, ctypes.POINTER(TalMeshOpts), _P, _P, _P, _P]),
     ("tal_plan_layout", _I, [_P, _P, _I64, _I64, ctypes.POINTER(TalMeshOpts),
                              ctypes.POINTER(TalMeshInfo)]),
     ("tal_peer_local", _I, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_I64)]),

@@ -1031,6 +1031,41 @@ int tal_layout_bank_stats(int64_t out[6])
     return TAL_OK;
 }
 
+int tal_plan_blobs(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
+                   const tal_mesh_opts *opts_in, int64_t sizes[4], uint8_t *blobs, int32_t *blob_off,
+                   int32_t *perm)
+{
+    if (!sizes || n_nodes < 0 || n_elems < 0 || (n_nodes && !coords) || (n_elems && !conn))
+        return fail(TAL_EINVAL, "bad arguments");
+    if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
+        return fail(TAL_EINVAL, "meshes are limited to 2^31-1 nodes/elements per device");
+    for (int64_t i = 0; i < 4 * n_elems; ++i)
+        if (conn[i] < 0 || conn[i] >= n_nodes)
+            return fail(TAL_EINVAL, "connectivity index out of range [0, n_nodes)");
+    tal_mesh_opts opts;
+    tal_default_mesh_opts(&opts);
+    if (opts_in)
+        opts = *opts_in;
+    HostLayout L;
+    if (int rc = host_layout(coords, conn, n_nodes, n_elems, opts, nullptr, 0, L))
+        return rc;
+    std::vector<uint8_t> b;
+    std::vector<int32_t> off;
+    const int T = cfg_threads(L.cfg);
+    pack_blobs(L.ch, T, b, off);
+    sizes[0] = (int64_t)b.size();
+    sizes[1] = (int64_t)off.size();
+    sizes[2] = T;
+    sizes[3] = L.perm.empty() ? 0 : n_nodes;
+    if (blobs)
+        std::memcpy(blobs, b.data(), b.size());
+    if (blob_off)
+        std::memcpy(blob_off, off.data(), 4 * off.size());
+    if (perm && !L.perm.empty())
+        std::memcpy(perm, L.perm.data(), 4 * L.perm.size());
+    return TAL_OK;
+}
+
 int tal_plan_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
                     const tal_mesh_opts *opts_in, tal_mesh_info *out)
 {

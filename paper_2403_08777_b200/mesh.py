@@ -169,6 +169,31 @@ def edge_star_patches(mesh, mode: str = "star"):
     return out
 
 
+def plan_blobs(mesh, cfg=None) -> dict:
+    """Host-only dump of the private-scatter chunk blobs (tal_plan_blobs):
+    ``blobs`` (uint8), ``blob_off`` (int32, 16-B units), ``threads`` (table
+    stride) and ``perm`` (internal -> caller node id, or None for identity).
+    The layout is documented at k_assemble_private (csrc/tal_kernels.cuh)."""
+    from . import _native as N
+    from .assembly import RunConfig
+    cfg = cfg or RunConfig()
+    coords = np.ascontiguousarray(mesh.coords, dtype=np.float64)
+    conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int64)
+    o = N.TalMeshOpts()
+    check(lib().tal_default_mesh_opts(ctypes.byref(o)))
+    o.renumber, o.element_order = N.RENUMBER[cfg.renumber], N.EORDER[cfg.element_order]
+    o.cta_patches, o.chunk_nodes, o.patch_mode = cfg.cta_patches, cfg.chunk_nodes, N.PATCHES[cfg.patches]
+    sizes = np.zeros(4, dtype=np.int64)
+    args = (ptr(coords), ptr(conn), coords.shape[0], conn.shape[0], ctypes.byref(o), ptr(sizes))
+    check(lib().tal_plan_blobs(*args, None, None, None))
+    blobs = np.zeros(max(int(sizes[0]), 1), dtype=np.uint8)
+    off = np.zeros(max(int(sizes[1]), 1), dtype=np.int32)
+    perm = np.zeros(max(int(sizes[3]), 1), dtype=np.int32)
+    check(lib().tal_plan_blobs(*args, ptr(blobs), ptr(off), ptr(perm)))
+    return {"blobs": blobs[:sizes[0]], "blob_off": off[:sizes[1]], "threads": int(sizes[2]),
+            "perm": perm[:sizes[3]] if sizes[3] else None}
+
+
 def plan_layout(mesh, cfg=None) -> dict:
     """Host-only dry run of the device upload (tal_plan_layout): renumbering,
     element order, edge-star patches and CTA chunks for ``cfg`` (a RunConfig);

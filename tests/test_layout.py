@@ -1,0 +1,145 @@
+"""CPU-side checks of the private-scatter chunk layout (tal_plan_blobs): the
+blobs the sm_100a kernel consumes are decoded here and their invariants
+checked, and a host emulation of the kernel's phases B and C over the decoded
+tables (element arithmetic from the oracle, one tet at a time) reproduces the
+oracle RHS -- so the bank-aware slot / level placements (tal_prep.cpp) are
+validated without a GPU.  Layout: csrc/tal_kernels.cuh at k_assemble_private.
+"""
+import numpy as np
+import pytest
+
+import paper_2403_08777_b200 as tb
+from paper_2403_08777_b200.mesh import plan_blobs
+
+SLOTS, LEVELS = 12, 32
+
+
+def pad16(x):
+    return (x + 15) // 16 * 16
+
+
+def decode(plan):
+    T, B, off = plan["threads"], plan["blobs"], plan["blob_off"]
+    out = []
+    for c in range(len(off) - 1):
+        b = B[off[c] * 16: off[c + 1] * 16]
+        n_patch, n_node, node_begin, n_contrib = b[:16].view(np.int32)
+        q = 16
+        ids = b[q: q + 2 * SLOTS * T].view(np.uint16).reshape(SLOTS, T)
+        q += 2 * SLOTS * T
+        pos = b[q: q + 2 * SLOTS * T].view(np.uint16).reshape(SLOTS, T)
+        q += 2 * SLOTS * T
+        lev = b[q: q + 2 * LEVELS].view(np.uint16).astype(np.int64)
+        q += 2 * LEVELS
+        gather = b[q: q + 4 * n_node].view(np.int32)
+        q += pad16(4 * n_node)
+        cnode = b[q: q + 4 * n_node].view(np.int32)
+        q += pad16(4 * n_node)
+        run = b[q: q + n_node].astype(np.int64)
+        out.append(dict(n_patch=int(n_patch), n_node=int(n_node), node_begin=int(node_begin),
+                        n_contrib=int(n_contrib), ids=ids, pos=pos, lev=lev, gather=gather,
+                        cnode=cnode, run=run))
+    return out
+
+
+def patches_of(ch):
+    for p in range(ch["n_patch"]):
+        head = int(ch["ids"][0, p])
+        m, closed = head & 0xFF, head >> 8
+        slots = list(range(1, m + 3))  # a, b, r_0 .. r_{m-1}
+        yield p, m, bool(closed), slots
+
+
+@pytest.fixture(scope="module", params=[(12, 10, 8), (16, 16, 16)])
+def layout(request):
+    m = tb.generate_box_mesh(*request.param)
+    return m, plan_blobs(m), decode(plan_blobs(m))
+
+
+def test_blob_invariants(layout):
+    mesh, plan, chunks = layout
+    assert plan["threads"] == 128
+    node_begin = 0
+    for ch in chunks:
+        nn = ch["n_node"]
+        assert ch["node_begin"] == node_begin
+        node_begin += nn
+        assert len(np.unique(ch["gather"])) == nn  # a slot per distinct node
+        rank_of = {int(v) & 0x7FFFFFFF: q for q, v in enumerate(ch["cnode"])}
+        assert sorted(rank_of) == sorted(int(g) for g in ch["gather"])
+        assert np.all(np.diff(ch["run"]) <= 0)  # rank order: contribution count descending
+        # jagged levels: level s holds every node with more than s contributions
+        for s in range(1, LEVELS):
+            assert ch["lev"][s] - ch["lev"][s - 1] == np.count_nonzero(ch["run"] > s - 1)
+        used = []
+        per_node = {}
+        for p, m_, closed, slots in patches_of(ch):
+            for s in slots:
+                node = int(ch["gather"][ch["ids"][s, p]])
+                used.append(int(ch["pos"][s, p]))
+                per_node.setdefault(node, []).append(int(ch["pos"][s, p]))
+        # every contribution has its own position, together exactly [0, n_contrib)
+        assert sorted(used) == list(range(ch["n_contrib"]))
+        # a node's positions are lev[s] + rank for s < its run length
+        for node, ps in per_node.items():
+            q = rank_of[node]
+            assert sorted(ps) == sorted(int(ch["lev"][s]) + q for s in range(int(ch["run"][q])))
+
+
+def test_bank_placements_are_effective(layout):
+    """Ring-walk record loads: quarter-warp slots mostly distinct mod 8;
+    contribution stores: half-warp positions mostly distinct mod 16."""
+    _, _, chunks = layout
+    rec_w = rec_g = st_w = st_g = 0
+    for ch in chunks:
+        ring = {}
+        store = {}
+        for p, m_, closed, slots in patches_of(ch):
+            k = m_ if closed else m_ - 1
+            for t in range(k):
+                nxt = 0 if t + 1 == m_ else t + 1
+                ring.setdefault((p >> 3, t), set()).add(int(ch["ids"][3 + nxt, p]))
+                store.setdefault((p >> 4, t), []).append(int(ch["pos"][3 + t, p]))
+        for sl in ring.values():
+            rec_w += np.bincount(np.array(list(sl)) % 8, minlength=8).max()
+            rec_g += 1
+        for ps in store.values():
+            st_w += np.bincount(np.array(ps) % 16, minlength=16).max()
+            st_g += 1
+    assert rec_w / rec_g < 1.6
+    assert st_w / st_g < 2.2
+
+
+def test_host_emulation_of_phases_b_and_c(layout, oracle):
+    """Walk the decoded tables like the kernel (ring tets (a, b, r_t, r_t+1),
+    per-patch node sums stored at their positions, per-node level sums) and
+    compare the assembled RHS with the oracle."""
+    mesh, plan, chunks = layout
+    u = tb.make_velocity(mesh, "random:1")
+    perm = plan["perm"] if plan["perm"] is not None else np.arange(mesh.n_nodes)
+    pm = oracle.pmat()
+    rhs = np.zeros((mesh.n_nodes, 3))
+    scratch = np.zeros((mesh.n_nodes, 3))
+    for ch in chunks:
+        res = np.zeros((ch["n_contrib"], 3))
+        for p, m_, closed, slots in patches_of(ch):
+            loc = [int(ch["gather"][ch["ids"][s, p]]) for s in slots]  # internal ids
+            a, b, ring = loc[0], loc[1], loc[2:]
+            k = m_ if closed else m_ - 1
+            sums = {}
+            for t in range(k):
+                tet = [a, b, ring[t], ring[(t + 1) % m_]]
+                caller = np.array([perm[v] for v in tet], dtype=np.int64)
+                scratch[caller] = 0.0
+                oracle.assemble_elements(mesh.coords, caller.reshape(1, 4), u, 1.0, 1e-3, 0.07, pm,
+                                         np.zeros(1, dtype=np.int64), scratch)
+                for v, cv in zip(tet, caller):
+                    sums[v] = sums.get(v, 0.0) + scratch[cv]
+            for s, v in zip(slots, loc):
+                res[int(ch["pos"][s, p])] = sums[v]
+        for q, raw in enumerate(ch["cnode"]):
+            v = int(raw) & 0x7FFFFFFF
+            tot = sum(res[int(ch["lev"][s]) + q] for s in range(int(ch["run"][q])))
+            rhs[perm[v]] += tot
+    ref = oracle.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=1)
+    assert np.abs(rhs - ref).max() <= 1e-13 * np.abs(ref).max()
