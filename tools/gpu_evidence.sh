@@ -8,6 +8,8 @@ timeout 300 python bench.py --scatter private --no-cpu-baseline > $OUT/bench_pri
 timeout 300 python bench.py --permute --no-cpu-baseline --no-e2e > $OUT/bench_permuted_rcm.json 2>> $OUT/bench.err
 timeout 300 python bench.py --permute --renumber none --element-order keep --no-cpu-baseline --no-e2e > $OUT/bench_permuted_none.json 2>> $OUT/bench.err
 timeout 300 python bench.py --scatter atomic --no-cpu-baseline --no-e2e > $OUT/bench_atomic.json 2>> $OUT/bench.err
+timeout 300 python bench.py --scatter colored --no-cpu-baseline --no-e2e > $OUT/bench_colored.json 2>> $OUT/bench.err
+timeout 300 python bench.py --scatter sequential --no-cpu-baseline --no-e2e --steps 20 --warmup 3 > $OUT/bench_sequential.json 2>> $OUT/bench.err
 timeout 300 python bench.py --pressure --no-cpu-baseline --no-e2e > $OUT/bench_pressure.json 2>> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/bench_reference.json 2>> $OUT/bench.err
 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 50 --warmup 5 > $OUT/bench_torchrun1.json 2>> $OUT/bench.err
