@@ -18,7 +18,15 @@ P = tb.PhysParams()
 modes = ("private", "private-atomic") if "big" in sys.argv else tb.SCATTER_MODES
 for mode in modes:
     tb.assemble_rsp(m, u, P, tb.RunConfig(scatter=mode))
-    tb.assemble_rsp(m, u, P, tb.RunConfig(scatter=mode), pressure=p)
+    if mode != "sequential":  # the reference-order mode has no pressure term
+        tb.assemble_rsp(m, u, P, tb.RunConfig(scatter=mode), pressure=p)
+if "big" not in sys.argv:  # the numba seam, fast and strict
+    from paper_2403_08777_b200.fields import interpolation_table
+    rhs = np.zeros_like(u)
+    ids = np.arange(m.n_elems, dtype=np.int64)
+    pm = interpolation_table()
+    tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, rhs)
+    tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, rhs, strict=True)
 for fn in () if "big" in sys.argv else (tb.assemble_baseline, tb.assemble_rs):
     fn(m, u, P, tb.RunConfig(scatter="atomic"))
 asm = tb.Assembler(m, tb.RunConfig(scatter="private-atomic", cta_patches=64, chunk_nodes=144))
