@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -691,6 +692,15 @@ struct HostLayout {
 int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
                 const tal_mesh_opts &opts, const int64_t *external, int64_t n_external, HostLayout &L)
 {
+    static const bool times = std::getenv("TAL_PREP_TIMES") != nullptr;  // phase timings to stderr
+    auto tick = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what) {
+        const auto now = std::chrono::steady_clock::now();
+        if (times)
+            std::fprintf(stderr, "[tal prep] %-14s %8.3f s\n", what,
+                         std::chrono::duration<double>(now - tick).count());
+        tick = now;
+    };
     // node renumbering: perm[new] = old
     if (opts.renumber == TAL_RENUMBER_RCM)
         renumber_rcm(conn, n_nodes, n_elems, L.perm);
@@ -698,6 +708,7 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
         renumber_sfc(coords, n_nodes, L.perm);
     else if (opts.renumber != TAL_RENUMBER_NONE)
         return fail(TAL_EINVAL, "unknown renumber method");
+    lap("renumber");
     const bool renum = !L.perm.empty();
     if (renum) {
         L.iperm.resize((size_t)n_nodes);
@@ -715,6 +726,7 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
         cin[i] = renum ? L.iperm[conn[i]] : (int32_t)conn[i];
     // element order
     element_order(opts.element_order, cin.data(), L.xin.data(), n_nodes, n_elems, L.eperm);
+    lap("element order");
     L.cord.resize((size_t)(4 * n_elems));
     for (int64_t e = 0; e < n_elems; ++e)
         for (int a = 0; a < 4; ++a)
@@ -729,6 +741,7 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
                                     "], patch_mode 0|1");
     L.cfg = cfg;
     build_patches(L.cord.data(), n_nodes, n_elems, opts.patch_mode, L.patches);
+    lap("patches");
     std::vector<uint8_t> ext;
     if (n_external) {
         ext.assign((size_t)n_nodes, 0);
@@ -738,6 +751,7 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
     if (!build_chunks(L.patches, n_nodes, opts.cta_patches, opts.chunk_nodes, cfg_max_contrib(cfg),
                       ext.empty() ? nullptr : ext.data(), L.ch, err))
         return fail(TAL_EINVAL, err);
+    lap("chunks");
     return TAL_OK;
 }
 
