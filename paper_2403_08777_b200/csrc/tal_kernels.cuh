@@ -536,11 +536,30 @@ __global__ void __launch_bounds__(256) k_merge_partials(const int32_t *__restric
     if (i >= n_bnd)
         return;
     double ax = 0.0, ay = 0.0, az = 0.0;
-    for (int p = bnd_off[i]; p < bnd_off[i + 1]; ++p) {
-        const double *e = part + 3 * (int64_t)bnd_pos[p];  // one 24-B entry
-        ax += e[0];
-        ay += e[1];
-        az += e[2];
+    const int p0 = bnd_off[i], p1 = bnd_off[i + 1];
+    // batches of 4 partials: all position and value loads of a batch are in
+    // flight together; the sum keeps the chunk order (bitwise unchanged)
+    for (int p = p0; p < p1; p += 4) {
+        int q[4];
+        double x[4][3];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            q[k] = p + k < p1 ? __ldg(bnd_pos + p + k) : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (q[k] >= 0) {
+                const double *e = part + 3 * (int64_t)q[k];  // one 24-B entry
+                x[k][0] = e[0];
+                x[k][1] = e[1];
+                x[k][2] = e[2];
+            }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (q[k] >= 0) {
+                ax += x[k][0];
+                ay += x[k][1];
+                az += x[k][2];
+            }
     }
     const int v = bnd_nodes[i];
     rhs.rx[v] = ax;
