@@ -81,6 +81,7 @@ struct tal_handle {
     double *astage_u[ASYNC_SLOTS] = {}, *astage_r[ASYNC_SLOTS] = {};
     int64_t async_next = 0;  // next ticket
     int64_t N = 0, E = 0;
+    int64_t n_interior = 0;  // internal ids [0, n_interior) are chunk-interior (HostLayout)
     bool has_mesh = false;
     // node data (internal order): records x y z ux uy uz (6*N) then rx ry rz (3*N)
     double *nodebuf = nullptr;
@@ -189,6 +190,7 @@ struct tal_handle {
         col_off.clear();
         h_iperm.clear();
         ch = Chunking();
+        n_interior = 0;
         priv_grid = 0;
         has_mesh = false;
         info = tal_mesh_info{};
@@ -215,11 +217,20 @@ struct DeviceGuard {
 #ifndef TAL_ZERO_KERNEL
 #define TAL_ZERO_KERNEL 0  // 1: k_zero (10 us alone, but the step measured 1.8 us slower than the memset)
 #endif
-cudaError_t zero_rhs(tal_handle *h, cudaStream_t s)
+cudaError_t zero_rhs(tal_handle *h, cudaStream_t s, bool tail_only = false)
 {
     const int64_t n = 3 * h->N;
     if (!n)
         return cudaSuccess;
+    if (tail_only && h->n_interior > 0) {  // interior nodes are plain-stored by their chunk
+        const int64_t t = h->N - h->n_interior;
+        cudaError_t e = cudaSuccess;
+        if (t > 0)
+            for (double *r : {h->RX(), h->RY(), h->RZ()})
+                if ((e = cudaMemsetAsync(r + h->n_interior, 0, sizeof(double) * t, s)) != cudaSuccess)
+                    break;
+        return e;
+    }
 #if TAL_ZERO_KERNEL
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->device);
@@ -476,8 +487,8 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         // zeroing inside the kernel, by thread or TMA bulk stores, measured
         // ~45 us slower -- DESIGN.md)
         if (!ordered && N) {
-            TAL_CK(zero_rhs(h, s));
-            nl += TAL_ZERO_KERNEL;
+            TAL_CK(zero_rhs(h, s, true));
+            nl += h->n_interior > 0 ? 0 : TAL_ZERO_KERNEL;
         }
         if (np) {  // every neighbour has zeroed before anyone REDs into it
             k_peer_signal<<<1, 1, 0, s>>>(h->peers[0].flags, h->peers[1].flags, 0, h->d_flags + 2);
@@ -687,7 +698,60 @@ struct HostLayout {
     Patches patches;
     Chunking ch;
     int cfg = 1;
+    int64_t n_interior = 0;  // internal ids [0, n_interior): chunk-interior nodes (shared_tail)
 };
+
+// Renumber so that the chunk-interior nodes come first, in chunk / slot
+// order, and the shared (and isolated) nodes form the tail [n_interior, N):
+// scatter 'private-atomic' then zeroes only the tail (interior nodes are
+// plain-stored by their one chunk), and a chunk's interior records are one
+// contiguous block for the gather.  TAL_SHARED_TAIL=0 disables it.
+void shared_tail_renumber(int64_t n_nodes, HostLayout &L)
+{
+    static const bool on = [] {
+        const char *e = std::getenv("TAL_SHARED_TAIL");
+        return !e || std::atoi(e) != 0;
+    }();
+    if (!on || !n_nodes)
+        return;
+    std::vector<uint8_t> interior((size_t)n_nodes, 0);
+    for (int32_t raw : L.ch.cnodes)
+        if (raw < 0)
+            interior[raw & 0x7fffffff] = 1;
+    std::vector<int32_t> nid((size_t)n_nodes, -1);
+    int32_t next = 0;
+    for (int32_t v : L.ch.gather_nodes)
+        if (interior[v] && nid[v] < 0)
+            nid[v] = next++;
+    L.n_interior = next;
+    for (int64_t v = 0; v < n_nodes; ++v)
+        if (nid[v] < 0)
+            nid[v] = next++;
+    const bool had = !L.perm.empty();
+    std::vector<int32_t> perm((size_t)n_nodes), iperm((size_t)n_nodes);
+    for (int64_t v = 0; v < n_nodes; ++v) {
+        const int32_t caller = had ? L.perm[v] : (int32_t)v;
+        perm[nid[v]] = caller;
+        iperm[caller] = nid[v];
+    }
+    L.perm.swap(perm);
+    L.iperm.swap(iperm);
+    std::vector<double> xin((size_t)(3 * n_nodes));
+    for (int64_t v = 0; v < n_nodes; ++v)
+        for (int c = 0; c < 3; ++c)
+            xin[3 * (int64_t)nid[v] + c] = L.xin[3 * v + c];
+    L.xin.swap(xin);
+    for (auto &x : L.cord)
+        x = nid[x];
+    for (auto &x : L.patches.nodes)
+        x = nid[x];
+    for (auto &x : L.ch.gather_nodes)
+        x = nid[x];
+    for (auto &x : L.ch.bnd_nodes)
+        x = nid[x];
+    for (auto &x : L.ch.cnodes)
+        x = (int32_t)(((uint32_t)x & 0x80000000u) | (uint32_t)nid[x & 0x7fffffff]);
+}
 
 int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
                 const tal_mesh_opts &opts, const int64_t *external, int64_t n_external, HostLayout &L)
@@ -752,6 +816,9 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
                       ext.empty() ? nullptr : ext.data(), L.ch, err))
         return fail(TAL_EINVAL, err);
     lap("chunks");
+    if (opts.renumber != TAL_RENUMBER_NONE)  // 'none' keeps the caller's numbering
+        shared_tail_renumber(n_nodes, L);
+    lap("tail renumber");
     return TAL_OK;
 }
 
@@ -929,6 +996,7 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
         return rc;
     const int cfg = L.cfg;
     h->priv_cfg = cfg;
+    h->n_interior = L.n_interior;
     h->ch = std::move(L.ch);
     std::vector<int32_t> &perm = L.perm, &iperm = L.iperm, &eperm = L.eperm, &cord = L.cord;
     std::vector<double> &xin = L.xin;
