@@ -94,6 +94,7 @@ struct tal_handle {
     int64_t *d_seq_off = nullptr;  // N+1
     int32_t *d_seq_ent = nullptr;  // 4E: row << 2 | corner, ascending caller element id
     double *d_seq_dlt = nullptr;   // E: Vreman filter width cbrt(6 vol) per conn row (host libm)
+    double *d_seq_rows = nullptr;  // 12 E: strict element rows (two-pass sequential scatter)
     // colouring
     int4 *conn_col = nullptr;
     std::vector<int64_t> col_off;
@@ -166,7 +167,7 @@ struct tal_handle {
         free_graph();
         free_peers();
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
-                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press, d_seq_off, d_seq_ent, d_seq_dlt};
+                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press, d_seq_off, d_seq_ent, d_seq_dlt, d_seq_rows};
         for (void *p : ptrs)
             if (p)
                 cudaFree(p);
@@ -174,6 +175,7 @@ struct tal_handle {
         d_seq_off = nullptr;
         d_seq_ent = nullptr;
         d_seq_dlt = nullptr;
+        d_seq_rows = nullptr;
         h_eperm.clear();
         has_press = false;
         for (int s = 0; s < ASYNC_SLOTS; ++s) {
@@ -358,6 +360,18 @@ double filter_width(const double *xyz, int stride, const Id *nodes4)
     return std::isnan(x) ? x : std::pow(x, 1.0 / 3.0);  // x >= 0: the sign-symmetric branch is moot
 }
 
+// two-pass reference-order scatter (rows once, then ordered sums); the
+// single-pass form evaluates every element once per node.  TAL_SEQ_TWO_PASS=0
+// selects the single pass.
+bool seq_two_pass()
+{
+    static const bool on = [] {
+        const char *e = std::getenv("TAL_SEQ_TWO_PASS");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 // node -> (conn row, corner) lists in ascending caller element id, for the
 // reference-order scatter; built on the host from the device connectivity
 int build_sequential(tal_handle *h)
@@ -398,6 +412,10 @@ int build_sequential(tal_handle *h)
         return TAL_OK;
     if (int rc = dev_upload(&h->d_seq_dlt, dlt.data(), dlt.size()))
         return rc;
+    if (seq_two_pass() && cudaMalloc((void **)&h->d_seq_rows, sizeof(double) * 12 * (size_t)E) != cudaSuccess) {
+        cudaGetLastError();  // not enough memory for the row buffer: single-pass form
+        h->d_seq_rows = nullptr;
+    }
     return dev_upload(&h->d_seq_ent, ent.data(), ent.size());
 }
 
@@ -530,9 +548,18 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
                 return rc;
         if (N) {
             pm.begin();
-            k_assemble_sequential<<<grid_for(N, 128), 128, 0, s>>>(h->d_seq_off, h->d_seq_ent, N, h->conn,
-                                                                  nodes, h->d_seq_dlt, rhs.rx, rhs.ry,
-                                                                  rhs.rz, kc, false);
+            if (h->d_seq_rows) {
+                if (E)
+                    k_strict_rows<<<grid_for(E, 128), 128, 0, s>>>(E, h->conn, nodes, h->d_seq_dlt,
+                                                                  h->d_seq_rows, kc);
+                k_sum_rows_ordered<<<grid_for(N, 256), 256, 0, s>>>(h->d_seq_off, h->d_seq_ent, N,
+                                                                    h->d_seq_rows, rhs.rx, rhs.ry, rhs.rz);
+                nl += E ? 1 : 0;
+            } else {
+                k_assemble_sequential<<<grid_for(N, 128), 128, 0, s>>>(h->d_seq_off, h->d_seq_ent, N, h->conn,
+                                                                      nodes, h->d_seq_dlt, rhs.rx, rhs.ry,
+                                                                      rhs.rz, kc, false);
+            }
             pm.end();
             TAL_CK_LAUNCH();
             ++nl;

@@ -39,9 +39,11 @@ namespace tal {
 // Row a (node a's three entries) of the element RHS, reference operation
 // order.  X, U: the four corner coordinates / velocities in the element's own
 // node order; pm: the 16 pmat values (variants.py:559).
-__device__ __forceinline__ void element_row_strict(const double X[4][3], const double U[4][3], double dlt,
-                                                   double rho, double mu, double cvre, const double *pm,
-                                                   int a, double r[3])
+// Rows a0 .. a1-1 (r: 3 doubles per row); the geometry / gradient / Vreman
+// prefix is computed once per call.
+__device__ __forceinline__ void element_rows_strict(const double X[4][3], const double U[4][3], double dlt,
+                                                    double rho, double mu, double cvre, const double *pm,
+                                                    int a0, int a1, double *r)
 {
     double ed[4][3];  // edges x_b - x_0 (_rsp_kernels.py:45-47)
 #pragma unroll
@@ -102,21 +104,30 @@ __device__ __forceinline__ void element_row_strict(const double X[4][3], const d
     const double vis = TA(mu, TM(rho, nut));         // :122
     const double nrv = -TM(TM(rho, vol), 0.25);      // :123
     const double nvv = -TM(vis, vol);                // :124
-    double m[3];                                     // :126-164, node a
+#pragma unroll 1
+    for (int a = a0; a < a1; ++a) {  // :126-164, node a
+        double m[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-        m[c] = TA(TA(TA(TM(pm[4 * a + 0], U[0][c]), TM(pm[4 * a + 1], U[1][c])), TM(pm[4 * a + 2], U[2][c])),
-                  TM(pm[4 * a + 3], U[3][c]));
-    double bsel[3];
+        for (int c = 0; c < 3; ++c)
+            m[c] = TA(TA(TA(TM(pm[4 * a + 0], U[0][c]), TM(pm[4 * a + 1], U[1][c])), TM(pm[4 * a + 2], U[2][c])),
+                      TM(pm[4 * a + 3], U[3][c]));
+        double bsel[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-        bsel[c] = a == 0 ? bg[0][c] : a == 1 ? bg[1][c] : a == 2 ? bg[2][c] : bg[3][c];
+        for (int c = 0; c < 3; ++c)
+            bsel[c] = a == 0 ? bg[0][c] : a == 1 ? bg[1][c] : a == 2 ? bg[2][c] : bg[3][c];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const double cv = TA(TA(TM(m[0], g[0][i]), TM(m[1], g[1][i])), TM(m[2], g[2][i]));
-        const double df = TA(TA(TM(bsel[0], g[0][i]), TM(bsel[1], g[1][i])), TM(bsel[2], g[2][i]));
-        r[i] = TA(TM(nrv, cv), TM(nvv, df));
+        for (int i = 0; i < 3; ++i) {
+            const double cv = TA(TA(TM(m[0], g[0][i]), TM(m[1], g[1][i])), TM(m[2], g[2][i]));
+            const double df = TA(TA(TM(bsel[0], g[0][i]), TM(bsel[1], g[1][i])), TM(bsel[2], g[2][i]));
+            r[3 * (a - a0) + i] = TA(TM(nrv, cv), TM(nvv, df));
+        }
     }
+}
+__device__ __forceinline__ void element_row_strict(const double X[4][3], const double U[4][3], double dlt,
+                                                   double rho, double mu, double cvre, const double *pm,
+                                                   int a, double r[3])
+{
+    element_rows_strict(X, U, dlt, rho, mu, cvre, pm, a, a + 1, r);
 }
 
 #undef TM
@@ -164,6 +175,55 @@ __global__ void __launch_bounds__(128) k_assemble_sequential(const int64_t *__re
     rx[v] = acc[0];
     ry[v] = acc[1];
     rz[v] = acc[2];
+}
+
+}  // namespace tal
+
+namespace tal {
+
+// Two-pass form of the reference-order scatter: every element's four strict
+// rows computed once (one thread per conn row) into contrib[e][a][i] ...
+__global__ void __launch_bounds__(128) k_strict_rows(int64_t n_elems, const int4 *__restrict__ conn,
+                                                     const double *__restrict__ nrec,
+                                                     const double *__restrict__ dlt, double *contrib,
+                                                     ElemConsts kc)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_elems)
+        return;
+    const int4 q = __ldg(conn + e);
+    const int ids[4] = {q.x, q.y, q.z, q.w};
+    double X[4][3], U[4][3];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const double2 *p = reinterpret_cast<const double2 *>(nrec + 6 * (int64_t)ids[b]);
+        const double2 s0 = __ldg(p), s1 = __ldg(p + 1), s2 = __ldg(p + 2);
+        X[b][0] = s0.x, X[b][1] = s0.y, X[b][2] = s1.x;
+        U[b][0] = s1.y, U[b][1] = s2.x, U[b][2] = s2.y;
+    }
+    const double d = __ldg(dlt + e);
+    element_rows_strict(X, U, d, kc.rho, kc.mu, kc.cvre, kc.pm, 0, 4, contrib + 12 * e);
+}
+
+// ... then each node sums its rows in ascending caller element id from zero.
+__global__ void __launch_bounds__(256) k_sum_rows_ordered(const int64_t *__restrict__ off,
+                                                          const int32_t *__restrict__ ent, int64_t n_nodes,
+                                                          const double *__restrict__ contrib, double *rx,
+                                                          double *ry, double *rz)
+{
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n_nodes)
+        return;
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    for (int64_t k = off[v]; k < off[v + 1]; ++k) {
+        const double *r = contrib + 3 * (int64_t)__ldg(ent + k);  // (row << 2 | corner) * 3
+        ax = __dadd_rn(ax, r[0]);
+        ay = __dadd_rn(ay, r[1]);
+        az = __dadd_rn(az, r[2]);
+    }
+    rx[v] = ax;
+    ry[v] = ay;
+    rz[v] = az;
 }
 
 }  // namespace tal
