@@ -143,3 +143,19 @@ def test_host_emulation_of_phases_b_and_c(layout, oracle):
             rhs[perm[v]] += tot
     ref = oracle.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=1)
     assert np.abs(rhs - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_shared_tail_numbering(layout):
+    """Chunk-interior nodes (plain-stored by their one chunk) take the lowest
+    internal ids, in chunk / slot order; shared nodes form the tail that the
+    private-atomic step zeroes (tal_capi.cu shared_tail_renumber)."""
+    mesh, plan, chunks = layout
+    interior, shared = [], set()
+    for ch in chunks:
+        slot_of = {int(v): j for j, v in enumerate(ch["gather"])}
+        mine = sorted((slot_of[int(r) & 0x7FFFFFFF], int(r) & 0x7FFFFFFF) for r in ch["cnode"] if r < 0)
+        interior += [v for _, v in mine]
+        shared |= {int(r) for r in ch["cnode"] if r >= 0}
+    assert interior == list(range(len(interior)))  # contiguous, in chunk / slot order
+    assert min(shared) >= len(interior)
+    assert len(interior) + len(shared) == mesh.n_nodes  # no isolated nodes in a box
