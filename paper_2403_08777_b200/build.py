@@ -23,6 +23,9 @@ OUT = PKG / "libtal_b200.so"
 BUILD = ROOT / "build"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# ptxas register allocation effort: level 10 measured 0.7% faster on the
+# private kernel than the default 5 (0 and 7 were not)
+PTXAS = ["-Xptxas", "--register-usage-level=10"]
 
 
 def _nvcc() -> str:
@@ -64,7 +67,7 @@ def build(verbose: bool = False, force: bool = False, out: Path = OUT, defines=(
     for src in sorted(CSRC.glob("*.cu")):
         obj = BUILD / (src.stem + tag + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *dflags,
-               "-Xptxas", "-v", "--expt-relaxed-constexpr", *nvcc_flags, "-c", str(src), "-o", str(obj)]
+               "-Xptxas", "-v", *PTXAS, "--expt-relaxed-constexpr", *nvcc_flags, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, check=False, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:
