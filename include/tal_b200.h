@@ -44,6 +44,7 @@ extern "C" {
 #define TAL_ECUDA 2  /* CUDA failure / no device      -> RuntimeError */
 #define TAL_ENOMEM 3 /* host or device allocation     -> MemoryError  */
 #define TAL_ESTATE 4 /* call order (e.g. no mesh yet) -> RuntimeError */
+#define TAL_EINTERNAL 5 /* unexpected internal failure  -> RuntimeError */
 
 /* scatter strategies (the reference RunConfig.scatter, variants.py:74-101,
  * offers 'private' and 'colored'; the GPU adds two atomic forms) */
@@ -225,6 +226,7 @@ int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter
 int tal_graph_capture(tal_handle *h, const tal_params *p, int variant, int scatter);
 int tal_graph_launch(tal_handle *h, void *stream, int64_t *kernel_launches);
 int tal_graph_destroy(tal_handle *h);
+/* tal_get_rhs_host blocks until rhs (caller order, (N,3) AoS) is complete. */
 int tal_get_rhs_host(tal_handle *h, double *rhs, void *stream);
 int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream);
 int tal_synchronize(tal_handle *h, void *stream);

@@ -117,6 +117,27 @@ class RunConfig:
             raise ValueError(f"chunk_nodes must be in [16, {nmax}] for cta_patches={self.cta_patches}")
 
 
+_REF_FIELDS = ("vector_dim", "n_threads", "reps", "scatter", "cache_capacity_bytes")
+
+
+def as_run_config(cfg) -> RunConfig:
+    """Accept this package's ``RunConfig``, ``None`` or any object with the
+    reference's five fields (``tet_assembly_lab.variants.RunConfig``, which
+    the reference's ``verify_variants``, ``run_bench`` and CLI pass to
+    whatever sits in ``ASSEMBLERS``).  GPU-only knobs a foreign config lacks
+    take their defaults; its values are validated like ours."""
+    if cfg is None:
+        return RunConfig()
+    if isinstance(cfg, RunConfig):
+        return cfg
+    missing = [f for f in _REF_FIELDS if not hasattr(cfg, f)]
+    if missing:
+        raise TypeError(f"not a RunConfig: {type(cfg).__name__} lacks {missing}")
+    gpu = {f: getattr(cfg, f) for f in ("device", "renumber", "element_order", "patches",
+                                        "cta_patches", "chunk_nodes") if hasattr(cfg, f)}
+    return RunConfig(**{f: getattr(cfg, f) for f in _REF_FIELDS}, **gpu)
+
+
 @dataclass(frozen=True)
 class CounterLedger:
     """Static per-element counts (1 FMA = 2 Flop); bytes_dram_est is modeled."""
@@ -532,19 +553,34 @@ def _needs_colors(variant: VariantId, scatter: str) -> bool:
     return scatter == "colored" or (variant is not VariantId.RSP and scatter == "private")
 
 
+def _frozen(a) -> bool:
+    return isinstance(a, np.ndarray) and not a.flags.writeable
+
+
 def _cached_assembler(mesh, cfg: RunConfig, variant: VariantId = VariantId.RSP) -> Assembler:
+    """The resident mesh for (arrays, layout knobs).  Keys are the arrays'
+    identities; a read-only array (the reference ``Mesh`` clears the write
+    flags, mesh.py:71-75) cannot change under the key, a writeable one is
+    compared with a snapshot taken at upload (memcmp speed) on every hit so a
+    mutated duck-typed mesh is re-uploaded instead of served stale."""
     colors = getattr(mesh, "colors", None)
     need_colors = _needs_colors(variant, cfg.scatter)
     key = (id(mesh.coords), id(mesh.connectivity), id(colors), mesh.coords.shape,
            mesh.connectivity.shape, cfg.device, cfg.renumber, cfg.element_order,
            cfg.patches, cfg.cta_patches, cfg.chunk_nodes, need_colors)
+    arrays = (mesh.coords, mesh.connectivity, colors)
     hit = _CACHE.get(key)
     if hit is not None:
-        _CACHE.move_to_end(key)
-        return hit[0]
+        asm, held, snaps = hit
+        if all(s is None or np.array_equal(a, s) for a, s in zip(held, snaps)):
+            _CACHE.move_to_end(key)
+            return asm
+        del _CACHE[key]
+        asm.close()
     asm = Assembler(mesh, cfg, build_colors=need_colors)
     # hold the arrays so their ids cannot be recycled while cached
-    _CACHE[key] = (asm, mesh.coords, mesh.connectivity, colors)
+    snaps = tuple(None if a is None or _frozen(a) else np.array(a, copy=True) for a in arrays)
+    _CACHE[key] = (asm, arrays, snaps)
     while len(_CACHE) > _CACHE_SIZE:
         _, (old, *_) = _CACHE.popitem(last=False)
         old.close()
@@ -559,7 +595,7 @@ def clear_cache() -> None:
 
 def _assemble_variant(variant: VariantId, mesh, u, params: PhysParams,
                       cfg: Optional[RunConfig], pressure: Optional[np.ndarray] = None) -> AssemblyResult:
-    cfg = cfg or RunConfig()
+    cfg = as_run_config(cfg)
     u = validate_velocity(mesh, u)
     asm = _cached_assembler(mesh, cfg, variant)
     rhs = np.empty((asm.n_nodes, 3))
@@ -702,17 +738,32 @@ def _compare(variant: VariantId, rhs: np.ndarray, oracle: np.ndarray, denom: flo
     return VariantCheck(variant, max_abs, rel, denom, worst, rel <= REL_TOL)
 
 
+def reference_order_rhs(mesh, u: np.ndarray, params: PhysParams, device: int = 0) -> np.ndarray:
+    """The default oracle vector of ``oracle_compare`` / ``verify_variants``:
+    ``scatter='sequential'`` (csrc/tal_strict.cuh), an independent kernel
+    that restates ``_rsp_kernels.py:33-164`` operation by operation and sums
+    in the reference's order -- bitwise identical to the reference's
+    one-thread ``assemble_rsp`` (tests/test_sequential.py), i.e. the role the
+    reference gives its scalar ``assemble_reference`` (variants.py:739-741).
+    The CPU oracle of this repo (``oracle/``) is test infrastructure and is
+    never called from the package; pass its vector as ``oracle=`` instead."""
+    return assemble_rsp(mesh, u, params, RunConfig(scatter="sequential", device=device)).rhs
+
+
 def oracle_compare(mesh, u: np.ndarray, params: PhysParams, rhs: np.ndarray,
-                   variant: VariantId, oracle: Optional[np.ndarray] = None) -> VariantCheck:
-    """Compare one assembled vector with an oracle vector (variants.py:714-720).
-    The CPU oracle is test infrastructure (repo ``oracle/``), never called
-    from this package: pass its vector as ``oracle``; without one the B
-    shape on the GPU -- the most literal restatement of the operator --
-    stands in."""
+                   variant: VariantId, oracle: Optional[np.ndarray] = None,
+                   device: int = 0) -> VariantCheck:
+    """Compare one assembled vector with an oracle vector (variants.py:714-720);
+    without ``oracle`` the reference-order vector (:func:`reference_order_rhs`)."""
     u = validate_velocity(mesh, u)
+    note = ""
     if oracle is None:
-        oracle = assemble_baseline(mesh, u, params, RunConfig(scatter="colored")).rhs
-    return _compare(VariantId(variant), rhs, oracle, _denominator(mesh, u, params, oracle))
+        oracle, note = reference_order_rhs(mesh, u, params, device), "oracle: sequential (reference order)"
+    c = _compare(VariantId(variant), rhs, oracle, _denominator(mesh, u, params, oracle))
+    if note and not c.note:
+        c = VariantCheck(c.variant, c.max_abs_diff, c.rel_diff, c.denominator, c.worst_node,
+                         c.passed, note)
+    return c
 
 
 def verify_variants(mesh, u: np.ndarray, params: PhysParams, cfg: Optional[RunConfig] = None,
@@ -722,11 +773,10 @@ def verify_variants(mesh, u: np.ndarray, params: PhysParams, cfg: Optional[RunCo
     ``REL_TOL`` (variants.py:723-755); ``fault_inject`` (a variant value)
     perturbs that shape's output to prove the check can fail.  ``oracle`` as
     in :func:`oracle_compare`."""
-    cfg = cfg or RunConfig()
+    cfg = as_run_config(cfg)
     u = validate_velocity(mesh, u)
     if oracle is None:
-        oracle = assemble_baseline(mesh, u, params, RunConfig(scatter="colored",
-                                                              device=cfg.device)).rhs
+        oracle = reference_order_rhs(mesh, u, params, cfg.device)
     denom = _denominator(mesh, u, params, oracle)
     checks = []
     for variant, fn in ASSEMBLERS.items():

@@ -215,10 +215,8 @@ struct DeviceGuard {
     }
 };
 
-// RHS zeroing before RED accumulation
-#ifndef TAL_ZERO_KERNEL
-#define TAL_ZERO_KERNEL 0  // 1: k_zero (10 us alone, but the step measured 1.8 us slower than the memset)
-#endif
+// RHS zeroing before RED accumulation (cudaMemsetAsync: a streaming-store
+// zero kernel measured 1.8 us slower per step)
 cudaError_t zero_rhs(tal_handle *h, cudaStream_t s, bool tail_only = false)
 {
     const int64_t n = 3 * h->N;
@@ -233,16 +231,7 @@ cudaError_t zero_rhs(tal_handle *h, cudaStream_t s, bool tail_only = false)
                     break;
         return e;
     }
-#if TAL_ZERO_KERNEL
-    int n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->device);
-    const int64_t want = (n / 2 + 511) / 512;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, 4 * (int64_t)n_sm));
-    k_zero<<<grid, 512, 0, s>>>(h->RX(), n);
-    return cudaGetLastError();
-#else
     return cudaMemsetAsync(h->RX(), 0, sizeof(double) * n, s);
-#endif
 }
 
 bool make_consts(const tal_params *p, ElemConsts &kc, bool &sym)
@@ -430,11 +419,16 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
     RhsSoA rhs{h->RX(), h->RY(), h->RZ()};
     int64_t nl = 0;
     const int64_t N = h->N, E = h->E;
+    // the fused interface sum lives in the private-atomic kernel's phase C
+    // (and its signal/wait kernels): any other path would drop this rank's
+    // interface sums and leave the neighbours waiting
+    if (h->n_peers() && (scatter != TAL_SCATTER_PRIVATE_ATOMIC || !sym))
+        return fail(TAL_EINVAL, "peers are attached: only scatter='private-atomic' with the symmetric "
+                                "Gauss table performs the fused interface sum");
     switch (scatter) {
     case TAL_SCATTER_ATOMIC: {
         if (N) {
             TAL_CK(zero_rhs(h, s));
-            nl += TAL_ZERO_KERNEL;
         }
         if (E) {
             pm.begin();
@@ -457,7 +451,6 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             return fail(TAL_ESTATE, "mesh was uploaded without a colouring (build_colors=0, colors=NULL)");
         if (N) {
             TAL_CK(zero_rhs(h, s));
-            nl += TAL_ZERO_KERNEL;
         }
         pm.begin();  // colour launches together form the dominant work
         for (size_t c = 0; c + 1 < h->col_off.size(); ++c) {
@@ -480,7 +473,14 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
     }
     case TAL_SCATTER_PRIVATE:
     case TAL_SCATTER_PRIVATE_ATOMIC: {
-        if (!sym)  // patches permute tet corners: only valid for the symmetric rule
+        // patches permute tet corners: only valid for the symmetric rule.  A
+        // general table runs the per-element atomic kernel -- for
+        // 'private-atomic' (already order-free) only: 'private' promises a
+        // bitwise reproducible sum, which the atomic kernel cannot keep
+        if (!sym && scatter == TAL_SCATTER_PRIVATE)
+            return fail(TAL_EINVAL, "scatter='private' needs the symmetric Gauss table (pmat = P^T P of "
+                                    "quadrature_tet4); use 'colored' (reproducible) or 'atomic'");
+        if (!sym)
             return launch_run(h, p, TAL_SCATTER_ATOMIC, s, launches);
         const bool ordered = scatter == TAL_SCATTER_PRIVATE;
         PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr,
@@ -506,7 +506,6 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         // ~45 us slower -- DESIGN.md)
         if (!ordered && N) {
             TAL_CK(zero_rhs(h, s, true));
-            nl += h->n_interior > 0 ? 0 : TAL_ZERO_KERNEL;
         }
         if (np) {  // every neighbour has zeroed before anyone REDs into it
             k_peer_signal<<<1, 1, 0, s>>>(h->peers[0].flags, h->peers[1].flags, 0, h->d_flags + 2);
@@ -619,7 +618,6 @@ int launch_shape(tal_handle *h, const tal_params *p, int variant, int scatter, c
     int64_t nl = 0;
     if (N) {
         TAL_CK(zero_rhs(h, s));
-        nl += TAL_ZERO_KERNEL;
     }
     auto one = [&](const int4 *conn, int64_t b, int64_t e) -> int {
         const unsigned grid = grid_for(e - b, 256);
@@ -851,6 +849,16 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
 
 }  // namespace
 
+// No C++ exception may cross the C ABI: every entry
+// point's body runs inside this guard (allocation failures -> TAL_ENOMEM,
+// anything else -> TAL_EINTERNAL with the message kept for tal_last_error).
+#define TAL_GUARD_BEGIN try {
+#define TAL_GUARD_END                                                           \
+    }                                                                           \
+    catch (const std::bad_alloc &) { return fail(TAL_ENOMEM, "host allocation failed"); } \
+    catch (const std::exception &ex) { return fail(TAL_EINTERNAL, ex.what()); } \
+    catch (...) { return fail(TAL_EINTERNAL, "unknown C++ exception"); }
+
 extern "C" {
 
 const char *tal_last_error(void) { return g_err.c_str(); }
@@ -858,6 +866,7 @@ int tal_abi_version(void) { return TAL_ABI_VERSION; }
 
 int tal_device_count(int *count)
 {
+    TAL_GUARD_BEGIN
     if (!count)
         return fail(TAL_EINVAL, "count is NULL");
     *count = 0;
@@ -867,10 +876,12 @@ int tal_device_count(int *count)
         return fail(TAL_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
     }
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_create(int device, tal_handle **out)
 {
+    TAL_GUARD_BEGIN
     if (!out)
         return fail(TAL_EINVAL, "out is NULL");
     *out = nullptr;
@@ -908,10 +919,12 @@ int tal_create(int device, tal_handle **out)
     }
     *out = h;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_destroy(tal_handle *h)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return TAL_OK;
     DeviceGuard g(h->device);
@@ -935,25 +948,31 @@ int tal_destroy(tal_handle *h)
     cudaStreamDestroy(h->stream);
     delete h;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_host_alloc(int64_t bytes, void **out)
 {
+    TAL_GUARD_BEGIN
     if (!out || bytes < 0)
         return fail(TAL_EINVAL, "bad arguments");
     TAL_CK(cudaMallocHost(out, (size_t)std::max<int64_t>(bytes, 1)));
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_host_free(void *p)
 {
+    TAL_GUARD_BEGIN
     if (p)
         TAL_CK(cudaFreeHost(p));
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_default_mesh_opts(tal_mesh_opts *o)
 {
+    TAL_GUARD_BEGIN
     if (!o)
         return fail(TAL_EINVAL, "NULL");
     o->renumber = TAL_RENUMBER_RCM;
@@ -964,18 +983,22 @@ int tal_default_mesh_opts(tal_mesh_opts *o)
     o->validate = 1;
     o->build_colors = 0;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_upload_mesh(tal_handle *h, const double *coords, const int64_t *conn, int64_t n_nodes,
                     int64_t n_elems, const int64_t *colors, const tal_mesh_opts *opts_in)
 {
+    TAL_GUARD_BEGIN
     return tal_upload_mesh_ex(h, coords, conn, n_nodes, n_elems, colors, opts_in, nullptr, 0);
+    TAL_GUARD_END
 }
 
 int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn, int64_t n_nodes,
                        int64_t n_elems, const int64_t *colors, const tal_mesh_opts *opts_in,
                        const int64_t *external, int64_t n_external)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (n_external < 0 || (n_external && !external))
@@ -1009,8 +1032,13 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
                 return fail(TAL_EINVAL, buf);
             }
     }
-    if (colors && !check_coloring(conn, colors, n_nodes, n_elems))
-        return fail(TAL_EINVAL, "coloring invalid: elements sharing a node share a color");
+    if (colors) {  // colour ids index per-colour tables below: bound them first
+        for (int64_t e = 0; e < n_elems; ++e)
+            if (colors[e] < 0 || colors[e] >= std::max<int64_t>(n_elems, 1))
+                return fail(TAL_EINVAL, "colour ids must lie in [0, n_elems)");
+        if (!check_coloring(conn, colors, n_nodes, n_elems))
+            return fail(TAL_EINVAL, "coloring invalid: elements sharing a node share a color");
+    }
 
     DeviceGuard g(h->device);
     cudaStreamSynchronize(h->stream);
@@ -1129,21 +1157,25 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
     h->info.device_bytes = (int64_t)bytes;
     h->info.prep_seconds = std::chrono::duration<double>(t1 - t0).count();
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_layout_bank_stats(int64_t out[6])
 {
+    TAL_GUARD_BEGIN
     if (!out)
         return fail(TAL_EINVAL, "out is NULL");
     bank_stats(out, out + 1, out + 2);
     pos_stats(out + 3, out + 4, out + 5);
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_plan_blobs(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
                    const tal_mesh_opts *opts_in, int64_t sizes[4], uint8_t *blobs, int32_t *blob_off,
                    int32_t *perm)
 {
+    TAL_GUARD_BEGIN
     if (!sizes || n_nodes < 0 || n_elems < 0 || (n_nodes && !coords) || (n_elems && !conn))
         return fail(TAL_EINVAL, "bad arguments");
     if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
@@ -1173,11 +1205,13 @@ int tal_plan_blobs(const double *coords, const int64_t *conn, int64_t n_nodes, i
     if (perm && !L.perm.empty())
         std::memcpy(perm, L.perm.data(), 4 * L.perm.size());
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_plan_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
                     const tal_mesh_opts *opts_in, tal_mesh_info *out)
 {
+    TAL_GUARD_BEGIN
     if (!out || n_nodes < 0 || n_elems < 0 || (n_nodes && !coords) || (n_elems && !conn))
         return fail(TAL_EINVAL, "bad arguments");
     if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
@@ -1202,20 +1236,24 @@ int tal_plan_layout(const double *coords, const int64_t *conn, int64_t n_nodes, 
     out->n_shared_nodes = L.ch.n_shared;
     out->prep_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_mesh_info_get(tal_handle *h, tal_mesh_info *out)
 {
+    TAL_GUARD_BEGIN
     if (!h || !out)
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
         return fail(TAL_ESTATE, "no mesh uploaded");
     *out = h->info;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_buffers_get(tal_handle *h, tal_buffers *out)
 {
+    TAL_GUARD_BEGIN
     if (!h || !out)
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
@@ -1230,10 +1268,12 @@ int tal_buffers_get(tal_handle *h, tal_buffers *out)
     out->perm = h->perm;
     out->iperm = h->iperm;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_set_velocity_device(tal_handle *h, const double *d_u, void *stream)
 {
+    TAL_GUARD_BEGIN
     if (!h || (!d_u && h->N))
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
@@ -1245,10 +1285,12 @@ int tal_set_velocity_device(tal_handle *h, const double *d_u, void *stream)
         TAL_CK_LAUNCH();
     }
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_set_pressure_device(tal_handle *h, const double *d_p, void *stream)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (!h->has_mesh)
@@ -1267,10 +1309,12 @@ int tal_set_pressure_device(tal_handle *h, const double *d_p, void *stream)
     }
     h->has_press = true;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_set_pressure_host(tal_handle *h, const double *p, void *stream)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (!h->has_mesh)
@@ -1286,10 +1330,12 @@ int tal_set_pressure_host(tal_handle *h, const double *p, void *stream)
     if (rc == TAL_OK)
         TAL_CK(cudaStreamSynchronize(s));  // staging is reused by the next host call
     return rc;
+    TAL_GUARD_END
 }
 
 int tal_set_velocity_host(tal_handle *h, const double *u, void *stream)
 {
+    TAL_GUARD_BEGIN
     if (!h || (!u && h->N))
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
@@ -1299,10 +1345,12 @@ int tal_set_velocity_host(tal_handle *h, const double *u, void *stream)
     if (h->N)
         TAL_CK(cudaMemcpyAsync(h->staging, u, sizeof(double) * 3 * h->N, cudaMemcpyHostToDevice, s));
     return tal_set_velocity_device(h, h->staging, s);
+    TAL_GUARD_END
 }
 
 int tal_run(tal_handle *h, const tal_params *p, int scatter, void *stream, int64_t *kernel_launches)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (!h->has_mesh)
@@ -1312,11 +1360,13 @@ int tal_run(tal_handle *h, const tal_params *p, int scatter, void *stream, int64
         return rc;
     DeviceGuard g(h->device);
     return launch_run(h, p, scatter, stream ? (cudaStream_t)stream : h->stream, kernel_launches);
+    TAL_GUARD_END
 }
 
 int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter, void *stream,
                     int64_t *kernel_launches)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (!h->has_mesh)
@@ -1326,10 +1376,12 @@ int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter
         return rc;
     DeviceGuard g(h->device);
     return launch_any(h, p, variant, scatter, stream ? (cudaStream_t)stream : h->stream, kernel_launches);
+    TAL_GUARD_END
 }
 
 int tal_graph_capture(tal_handle *h, const tal_params *p, int variant, int scatter)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (!h->has_mesh)
@@ -1366,10 +1418,12 @@ int tal_graph_capture(tal_handle *h, const tal_params *p, int variant, int scatt
     cudaGetLastError();
     h->g_launches = rc == TAL_OK ? nl : 0;
     return rc;
+    TAL_GUARD_END
 }
 
 int tal_graph_launch(tal_handle *h, void *stream, int64_t *kernel_launches)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (!h->gexec)
@@ -1379,19 +1433,23 @@ int tal_graph_launch(tal_handle *h, void *stream, int64_t *kernel_launches)
     if (kernel_launches)
         *kernel_launches = h->g_launches;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_graph_destroy(tal_handle *h)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     DeviceGuard g(h->device);
     h->free_graph();
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream)
 {
+    TAL_GUARD_BEGIN
     if (!h || (!d_rhs && h->N))
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
@@ -1403,10 +1461,12 @@ int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream)
         TAL_CK_LAUNCH();
     }
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_get_rhs_host(tal_handle *h, double *rhs, void *stream)
 {
+    TAL_GUARD_BEGIN
     if (!h || (!rhs && h->N))
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
@@ -1418,21 +1478,29 @@ int tal_get_rhs_host(tal_handle *h, double *rhs, void *stream)
         return rc;
     if (h->N)
         TAL_CK(cudaMemcpyAsync(rhs, h->staging, sizeof(double) * 3 * h->N, cudaMemcpyDeviceToHost, s));
+    // blocking: rhs is complete on return, even if it is page-locked (the
+    // copy would otherwise still be in flight), and the shared staging
+    // buffer is free for the next host call on any stream
+    TAL_CK(cudaStreamSynchronize(s));
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_synchronize(tal_handle *h, void *stream)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     DeviceGuard g(h->device);
     TAL_CK(cudaStreamSynchronize(stream ? (cudaStream_t)stream : h->stream));
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_assemble_async(tal_handle *h, const double *u, const tal_params *p, double *rhs, int scatter,
                        int64_t *ticket)
 {
+    TAL_GUARD_BEGIN
     if (!h || !ticket)
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
@@ -1476,10 +1544,12 @@ int tal_assemble_async(tal_handle *h, const double *u, const tal_params *p, doub
     *ticket = n;
     h->async_next = n + 1;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_wait(tal_handle *h, int64_t ticket)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (ticket < 0 || ticket >= h->async_next)
@@ -1489,17 +1559,21 @@ int tal_wait(tal_handle *h, int64_t ticket)
     DeviceGuard g(h->device);
     TAL_CK(cudaEventSynchronize(h->ev_d2h[ticket % tal_handle::ASYNC_SLOTS]));
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_assemble(tal_handle *h, const double *u, const tal_params *p, double *rhs, int scatter,
                  tal_timings *t)
 {
+    TAL_GUARD_BEGIN
     return tal_assemble_variant(h, u, p, rhs, TAL_VARIANT_RSP, scatter, t);
+    TAL_GUARD_END
 }
 
 int tal_assemble_variant(tal_handle *h, const double *u, const tal_params *p, double *rhs, int variant,
                          int scatter, tal_timings *t)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     if (!h->has_mesh)
@@ -1551,6 +1625,7 @@ int tal_assemble_variant(tal_handle *h, const double *u, const tal_params *p, do
     if (t)
         *t = tt;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 namespace {
@@ -1699,18 +1774,23 @@ int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
                           int64_t n_elems, const double *u, double rho, double mu, double cvre,
                           const double *pmat, const int64_t *ids, int64_t k, double *rhs)
 {
+    TAL_GUARD_BEGIN
     return seam_impl(device, coords, conn, n_nodes, n_elems, u, rho, mu, cvre, pmat, ids, k, rhs, false);
+    TAL_GUARD_END
 }
 
 int tal_assemble_elements_strict(int device, const double *coords, const int64_t *conn, int64_t n_nodes,
                                  int64_t n_elems, const double *u, double rho, double mu, double cvre,
                                  const double *pmat, const int64_t *ids, int64_t k, double *rhs)
 {
+    TAL_GUARD_BEGIN
     return seam_impl(device, coords, conn, n_nodes, n_elems, u, rho, mu, cvre, pmat, ids, k, rhs, true);
+    TAL_GUARD_END
 }
 
 int tal_halo_pack(tal_handle *h, const int32_t *d_list, int64_t n, double *d_out, void *stream)
 {
+    TAL_GUARD_BEGIN
     if (!h || n < 0 || (n && (!d_list || !d_out)))
         return fail(TAL_EINVAL, "bad arguments");
     if (!h->has_mesh)
@@ -1722,10 +1802,12 @@ int tal_halo_pack(tal_handle *h, const int32_t *d_list, int64_t n, double *d_out
     k_halo_pack<<<grid_for(n, 256), 256, 0, s>>>(d_list, n, h->RX(), h->RY(), h->RZ(), d_out);
     TAL_CK_LAUNCH();
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_halo_accumulate(tal_handle *h, const int32_t *d_list, int64_t n, const double *d_in, void *stream)
 {
+    TAL_GUARD_BEGIN
     if (!h || n < 0 || (n && (!d_list || !d_in)))
         return fail(TAL_EINVAL, "bad arguments");
     if (!h->has_mesh)
@@ -1737,10 +1819,12 @@ int tal_halo_accumulate(tal_handle *h, const int32_t *d_list, int64_t n, const d
     k_halo_accumulate<<<grid_for(n, 256), 256, 0, s>>>(d_list, n, d_in, h->RX(), h->RY(), h->RZ());
     TAL_CK_LAUNCH();
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_map_nodes(tal_handle *h, const int64_t *caller_ids, int64_t n, int32_t *internal_ids)
 {
+    TAL_GUARD_BEGIN
     if (!h || n < 0 || (n && (!caller_ids || !internal_ids)))
         return fail(TAL_EINVAL, "bad arguments");
     if (!h->has_mesh)
@@ -1752,11 +1836,13 @@ int tal_map_nodes(tal_handle *h, const int64_t *caller_ids, int64_t n, int32_t *
         internal_ids[i] = h->h_iperm.empty() ? (int32_t)v : h->h_iperm[v];
     }
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_box_mesh(int64_t nx, int64_t ny, int64_t nz, double ex, double ey, double ez, double *coords,
                  int64_t *conn)
 {
+    TAL_GUARD_BEGIN
     if (nx < 1 || ny < 1 || nz < 1)
         return fail(TAL_EINVAL, "box dimensions must be positive");
     if (!(ex > 0.0 && ey > 0.0 && ez > 0.0))
@@ -1765,19 +1851,23 @@ int tal_box_mesh(int64_t nx, int64_t ny, int64_t nz, double ex, double ey, doubl
         return fail(TAL_EINVAL, "NULL output arrays");
     box_mesh(nx, ny, nz, ex, ey, ez, coords, conn);
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_signed_volumes(const double *coords, const int64_t *conn, int64_t n_elems, double *vols)
 {
+    TAL_GUARD_BEGIN
     if (n_elems < 0 || (n_elems && (!coords || !conn || !vols)))
         return fail(TAL_EINVAL, "bad arguments");
     signed_volumes(coords, conn, n_elems, vols);
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_color_elements(const int64_t *conn, int64_t n_nodes, int64_t n_elems, int64_t *colors,
                        int64_t *n_colors)
 {
+    TAL_GUARD_BEGIN
     if (n_elems < 0 || n_nodes < 0 || (n_elems && (!conn || !colors)) || !n_colors)
         return fail(TAL_EINVAL, "bad arguments");
     const int64_t nc = color_elements(conn, n_nodes, n_elems, colors);
@@ -1785,20 +1875,24 @@ int tal_color_elements(const int64_t *conn, int64_t n_nodes, int64_t n_elems, in
         return fail(TAL_EINVAL, "greedy colouring needs more than 256 colours");
     *n_colors = nc;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_check_coloring(const int64_t *conn, const int64_t *colors, int64_t n_nodes, int64_t n_elems,
                        int *valid)
 {
+    TAL_GUARD_BEGIN
     if (!valid || n_elems < 0 || (n_elems && (!conn || !colors)))
         return fail(TAL_EINVAL, "bad arguments");
     *valid = check_coloring(conn, colors, n_nodes, n_elems) ? 1 : 0;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_renumber_nodes(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
                        int method, int64_t *perm_out)
 {
+    TAL_GUARD_BEGIN
     if (n_nodes < 0 || n_elems < 0 || !perm_out)
         return fail(TAL_EINVAL, "bad arguments");
     std::vector<int32_t> perm;
@@ -1815,12 +1909,14 @@ int tal_renumber_nodes(const double *coords, const int64_t *conn, int64_t n_node
     for (int64_t i = 0; i < n_nodes; ++i)
         perm_out[i] = perm[i];
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_build_patches(const int64_t *conn, int64_t n_nodes, int64_t n_elems, int mode,
                       int64_t *n_patches, int64_t *n_patch_nodes, int32_t *off_out, int32_t *nodes_out,
                       uint8_t *closed_out)
 {
+    TAL_GUARD_BEGIN
     if (n_nodes < 0 || n_elems < 0 || (n_elems && !conn) || !n_patches || !n_patch_nodes ||
         (mode != 0 && mode != 1))
         return fail(TAL_EINVAL, "bad arguments");
@@ -1842,10 +1938,12 @@ int tal_build_patches(const int64_t *conn, int64_t n_nodes, int64_t n_elems, int
         std::memcpy(closed_out, p.closed.data(), p.closed.size());
     }
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_peer_local(tal_handle *h, double **rx, unsigned long long **flags, int64_t *n_nodes)
 {
+    TAL_GUARD_BEGIN
     if (!h || !rx || !flags || !n_nodes)
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
@@ -1854,10 +1952,12 @@ int tal_peer_local(tal_handle *h, double **rx, unsigned long long **flags, int64
     *flags = h->d_flags;
     *n_nodes = h->N;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_peer_export(tal_handle *h, void *rhs_handle, int64_t *rhs_offset, void *flags_handle)
 {
+    TAL_GUARD_BEGIN
     if (!h || !rhs_handle || !rhs_offset || !flags_handle)
         return fail(TAL_EINVAL, "NULL argument");
     if (!h->has_mesh)
@@ -1867,12 +1967,14 @@ int tal_peer_export(tal_handle *h, void *rhs_handle, int64_t *rhs_offset, void *
     TAL_CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)flags_handle, h->d_flags));
     *rhs_offset = (int64_t)((char *)h->RX() - (char *)h->nodebuf);
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_peer_attach(tal_handle *h, int slot, double *peer_rx, int64_t peer_n_nodes,
                     unsigned long long *peer_flags, const int64_t *my_ids, const int32_t *peer_ids,
                     int64_t n)
 {
+    TAL_GUARD_BEGIN
     if (h)
         h->free_graph();  // captured without this neighbour
     if (!h || slot < 0 || slot > 1 || !peer_rx || !peer_flags || peer_n_nodes <= 0 || n < 0 ||
@@ -1910,12 +2012,14 @@ int tal_peer_attach(tal_handle *h, int slot, double *peer_rx, int64_t peer_n_nod
     h->peers[slot].n = peer_n_nodes;
     h->peers[slot].flags = peer_flags;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_peer_open(tal_handle *h, int slot, const void *rhs_handle, int64_t rhs_offset,
                   const void *flags_handle, int64_t peer_n_nodes, const int64_t *my_ids,
                   const int32_t *peer_ids, int64_t n)
 {
+    TAL_GUARD_BEGIN
     if (!h || slot < 0 || slot > 1 || !rhs_handle || !flags_handle)
         return fail(TAL_EINVAL, "bad arguments");
     DeviceGuard g(h->device);
@@ -1939,20 +2043,24 @@ int tal_peer_open(tal_handle *h, int slot, const void *rhs_handle, int64_t rhs_o
     h->peers[slot].ipc_rhs = rb;
     h->peers[slot].ipc_flags = fb;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_peer_detach(tal_handle *h)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     DeviceGuard g(h->device);
     cudaStreamSynchronize(h->stream);
     h->free_peers();
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_profile(tal_handle *h, int enable)
 {
+    TAL_GUARD_BEGIN
     if (!h)
         return fail(TAL_EINVAL, "handle is NULL");
     DeviceGuard g(h->device);
@@ -1964,10 +2072,12 @@ int tal_profile(tal_handle *h, int enable)
     h->prof_on = enable != 0;
     h->prof_head = h->prof_count = 0;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_profile_read(tal_handle *h, double *ms_out, int64_t cap, int64_t *n_out)
 {
+    TAL_GUARD_BEGIN
     if (!h || !n_out || cap < 0 || (cap && !ms_out))
         return fail(TAL_EINVAL, "bad arguments");
     DeviceGuard g(h->device);
@@ -1983,10 +2093,12 @@ int tal_profile_read(tal_handle *h, double *ms_out, int64_t cap, int64_t *n_out)
     }
     *n_out = n;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 int tal_fp64_peak(int device, double ms_target, double *tflops, double *sm_clock_mhz)
 {
+    TAL_GUARD_BEGIN
     // Burst FP64 FMA throughput: launches sized to ~ms_target (comparable to
     // one assembly), best of 20; the SM clock of the best launch is measured
     // in-kernel (clock64 cycles / globaltimer ns of block 0).
@@ -2044,6 +2156,7 @@ int tal_fp64_peak(int device, double ms_target, double *tflops, double *sm_clock
     if (sm_clock_mhz)
         *sm_clock_mhz = best_clk[1] > 0 ? (double)best_clk[0] / (double)best_clk[1] * 1e3 : 0.0;
     return TAL_OK;
+    TAL_GUARD_END
 }
 
 }  // extern "C"

@@ -218,12 +218,6 @@ constexpr int kRingUnroll = TAL_RING_UNROLL;
 #ifndef TAL_GATHER_COOP
 #define TAL_GATHER_COOP 1
 #endif
-#ifndef TAL_DIAG_NO_C
-#define TAL_DIAG_NO_C 0
-#endif
-#ifndef TAL_DIAG_NO_GATHER
-#define TAL_DIAG_NO_GATHER 0
-#endif
 
 template <>
 struct PrivCfg<1> {  // 128 patches / chunk
@@ -459,19 +453,13 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
         // phase B(i) is done; its blob has had all of phase B(i) to land
         if (i + 1 < n_my) {
             mbar_wait(&bar[b ^ 1], ((i + 1) >> 1) & 1);
-#if !TAL_DIAG_NO_GATHER  // diagnostic build only (results wrong): cost of the record gather
             gather(b ^ 1);
-#endif
         }
 
         // phase C: one node per thread, nodes in rank order (contribution count
         // descending); its s-th contribution sits at lev[s] + q, so a warp
         // reads lane-contiguous addresses at every level
-#if TAL_DIAG_NO_C  // diagnostic build only (results wrong): cost of phase C
-        for (int q = tid; q < 0; q += T) {
-#else
         for (int q = tid; q < hdr.y; q += T) {
-#endif
             const int nr_ = run[q];
             double ax = 0.0, ay = 0.0, az = 0.0;
             for (int s = 0; s < nr_; ++s) {
@@ -508,20 +496,6 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
             }
         }
     }
-}
-
-// zero n doubles (16-B aligned start): 16-B streaming stores, grid-stride.
-// Replaces cudaMemsetAsync for the RHS (measured 3.2 TB/s for 51.5 MB).
-__global__ void __launch_bounds__(512) k_zero(double *__restrict__ p, int64_t n)
-{
-    const int64_t n2 = n >> 1;
-    double2 *q = reinterpret_cast<double2 *>(p);
-    const double2 z = make_double2(0.0, 0.0);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
-         i += (int64_t)gridDim.x * blockDim.x)
-        __stcs(q + i, z);
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
-        p[n - 1] = 0.0;
 }
 
 // ordered merge of chunk partials for nodes shared between chunks (and zero

@@ -196,10 +196,14 @@ def test_general_pmat_kernel(oracle):
     ids = np.arange(m.n_elems, dtype=np.int64)
     ref = np.zeros((m.n_nodes, 3))
     oracle.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, ref)
-    asm = tb.Assembler(m, tb.RunConfig())
-    rhs = np.empty((m.n_nodes, 3))
-    asm.assemble_into(u, P, rhs, "private", pmat=pm)
-    assert_parity(oracle, rhs, ref, m, u)
+    asm = tb.Assembler(m, tb.RunConfig(), build_colors=True)
+    for scatter in ("private-atomic", "atomic", "colored"):
+        rhs = np.empty((m.n_nodes, 3))
+        asm.assemble_into(u, P, rhs, scatter, pmat=pm)
+        assert_parity(oracle, rhs, ref, m, u)
+    # 'private' promises a bitwise reproducible sum: refused, not silently atomic
+    with pytest.raises(ValueError, match="symmetric"):
+        asm.assemble_into(u, P, np.empty((m.n_nodes, 3)), "private", pmat=pm)
     asm.close()
 
 
@@ -514,3 +518,15 @@ def test_cuda_graph_replay_matches_run(oracle):
         oracle.pressure_gradient(m.coords, m.connectivity, p)
     assert_parity(oracle, got, want, m, fields[1])
     asm.close()
+
+
+def test_bad_colour_ids_are_rejected():
+    """Negative or huge colour ids pass the (node, colour) uniqueness check
+    but index per-colour tables: refused with ValueError at upload."""
+    m = tb.generate_box_mesh(2, 2, 2)
+    for bad in (-1, m.n_elems, 1 << 40):
+        cols = np.arange(m.n_elems, dtype=np.int64)
+        cols[3] = bad
+        mc = tb.Mesh(coords=m.coords, connectivity=m.connectivity, colors=cols)
+        with pytest.raises(ValueError, match="colour ids"):
+            tb.Assembler(mc, tb.RunConfig(scatter="colored"))

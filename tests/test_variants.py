@@ -234,37 +234,23 @@ def test_shapes_device_resident_run(oracle, shape):
 
 
 # ---------------------------------------------------------------------------
-# CPU: the roofline model (reference perfmodel.py) with the B200 presets
+# CPU: the B200 roofline figures (perfmodel)
 # ---------------------------------------------------------------------------
 
-def test_perfmodel_classify_and_presets():
+def test_perfmodel_b200_ceilings_and_bounds():
     from paper_2403_08777_b200 import perfmodel as pm
-    b200 = pm.MACHINE_PRESETS["b200"]
-    assert pm.machine_balance(b200) == pytest.approx(33480.0 / 6554.2)
-    knee = pm.CodePoint("knee", pm.machine_balance(b200) * 10.0, 10.0)
-    assert pm.classify(b200, knee).bound == "compute"
-    # the production kernel is FP64-compute bound, the baseline memory bound
-    pts = {p.label: p for p in pm.COUNTER_PRESETS["b200-ncu"]}
-    star, base = pm.classify(b200, pts["RSP-star"]), pm.classify(b200, pts["B"])
-    assert star.bound == "compute" and base.bound == "memory"
-    assert 0.3 < star.utilization < 1.0
-    assert pts["B"].flops_per_elem > pts["RS"].flops_per_elem > pts["RSP"].flops_per_elem * 2
+    assert pm.B200.balance == pytest.approx(33.48 / 6.5542)
+    k = {r["kernel"]: r for r in pm.report()}
+    # the production kernel is FP64-compute bound, the baseline shape memory bound
+    assert k["RSP-star"]["bound"] == "fp64" and k["B"]["bound"] == "hbm"
+    assert 0.3 < k["RSP-star"]["frac"] < 1.0
+    assert k["RSP-star"]["measured_gelem_s"] > 3 * k["RSP"]["measured_gelem_s"]
+    # ceiling = min(compute, memory) per element
+    star = pm.SHAPES_128[-1]
+    assert pm.attainable_elem_per_s(star) == pytest.approx(
+        min(33.48e12 / star.flop, 6.5542e12 / star.dram_bytes))
     with pytest.raises(ValueError):
-        pm.MachineSpec("x", 0.0, 1.0)
-    with pytest.raises(ValueError):
-        pm.CodePoint("x", 1.0, 0.0)
-    assert pm.energy_estimate(1000.0, 0.25) == 250.0
-
-
-def test_perfmodel_dataset_has_knee_and_points():
-    from paper_2403_08777_b200 import perfmodel as pm
-    spec = pm.MACHINE_PRESETS["b200"]
-    rows = pm.roofline_dataset(spec, pm.COUNTER_PRESETS["b200-ncu"], extra_roofs=(20000.0,))
-    kinds = {r.kind for r in rows}
-    assert kinds == {"measured", "roof"}
-    assert any(r.kind == "roof" and r.ai == pytest.approx(pm.machine_balance(spec)) for r in rows)
-    csv = pm.roofline_csv(rows)
-    assert csv.startswith("label,ai_flop_per_byte,gflops,kind\n") and "RSP-star" in csv
+        pm.attainable_elem_per_s(pm.Kernel("x", 1.0, 0.0))
 
 
 @pytest.mark.gpu
