@@ -46,7 +46,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cells", type=int, default=128, help="cells per side (per rank slab)")
+    ap.add_argument("--cells", type=int, default=None,
+                    help="cells per side: of each rank's slab (--scaling weak; default 128, "
+                         "config 2 at N=1; 160 = config 5) or of the whole box split over the "
+                         "ranks (--scaling strong; default 256 = config 4)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N>1: weak = a cells^3 slab per rank of a cells x cells x (cells N) box; "
+                         "strong = one cells^3 box cut into N z-slabs")
     ap.add_argument("--init", default="random:1")
     ap.add_argument("--scatter", default="private-atomic")
     ap.add_argument("--variant", choices=["rsp", "rs", "b", "p"], default="rsp",
@@ -71,6 +77,32 @@ def parse():
     ap.add_argument("--check", action="store_true",
                     help="N>1: gather the owned RHS rows to rank 0 and check them against the oracle")
     return ap.parse_args()
+
+
+def cells_of(a) -> int:
+    return a.cells if a.cells is not None else (256 if a.scaling == "strong" else 128)
+
+
+def self_launch(a) -> int | None:
+    """``--gpus N`` without a torchrun environment: re-launch this command as
+    N ranks under torch.distributed.run (127.0.0.1 rendezvous, a free port)
+    and return its exit code; None when this process is already a rank.  A
+    torchrun world that disagrees with --gpus is refused."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != a.gpus:
+            sys.exit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={ws}; refusing a mismatched run")
+        return None
+    if a.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -146,55 +178,123 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# reference arm: the reference algorithm's CPU port on all host cores
+# reference arm: the reference's own CPU path on all host cores
 # ---------------------------------------------------------------------------
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def import_reference():
+    """tet-assembly-lab from baseline/_ref (pip-installed copy, git-ignored,
+    travels to the GPU box; numba is part of the image), else None."""
+    base = ROOT / "baseline" / "_ref"
+    if not (base / "tet_assembly_lab").is_dir():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/tal_numba_cache")
+    if str(base) not in sys.path:
+        sys.path.append(str(base))
+    try:
+        import tet_assembly_lab as ref
+        from tet_assembly_lab import harness, variants
+        return ref, variants, harness
+    except Exception:  # numba or numpy missing / incompatible
+        return None
+
+
+def reference_cpu(cells, init: str, steps: int, warmup: int, budget_s: float = 120.0) -> dict:
+    """Time the reference's own RSP assembly on the host: its harness
+    ``run_bench(mesh, u, VariantId.RSP, PhysParams(), RunConfig(n_threads=T,
+    scatter='private', reps=steps), verify=False)`` (harness.py:75-128, the
+    survey's CPU-baseline recipe), T = all host threads; the
+    value is the harness's own median-based elem/s.  The sample is the
+    (nx, ny, nz) box ``cells``, cut to fewer z layers when the whole run would
+    exceed ``budget_s``.  Falls back to the C port of the numba kernel
+    (oracle/, bitwise equal to it) when the reference cannot be imported."""
+    T = host_threads()
+    nx, ny, nz = cells
+    R = import_reference()
+    if R is not None:
+        ref, variants, harness = R
+        P = ref.PhysParams()
+        cfg1 = variants.RunConfig(n_threads=T, scatter="private", reps=1)
+        probe = ref.generate_box_mesh(nx, ny, max(1, min(nz, 8)))
+        up = ref.make_velocity(probe, init)
+        variants.assemble_rsp(probe, up, P, cfg1)  # numba JIT / cache load
+        t = variants.assemble_rsp(probe, up, P, cfg1).wall_time / probe.n_elems
+        per_step = t * 6 * nx * ny * nz
+        total = max(steps, 1) + max(warmup, 0) + 1
+        if per_step * total > budget_s:
+            nz = max(1, int(nz * budget_s / (per_step * total)))
+        mesh = ref.generate_box_mesh(nx, ny, nz)
+        u = ref.make_velocity(mesh, init)
+        for _ in range(max(warmup, 0)):
+            variants.assemble_rsp(mesh, u, P, cfg1)
+        rec, _ = harness.run_bench(mesh, u, variants.VariantId.RSP, P,
+                                   variants.RunConfig(n_threads=T, scatter="private",
+                                                      reps=max(steps, 1)), verify=False)
+        return {"value": rec.melems_per_s * 1e6, "unit": "elem/s", "cores": T, "kind": "reference",
+                "steps": rec.reps, "median_s": rec.median_time,
+                "sample": f"{nx}x{ny}x{nz} Kuhn box ({mesh.n_elems} tets), {init}; the reference "
+                          f"package (tet-assembly-lab 0.1.0, numba) harness.run_bench, RSP, "
+                          f"scatter=private, n_threads={T}, 1 warm-up + {max(warmup, 0)} + median of "
+                          f"{rec.reps}"}
+    from oracle import oracle as O
+    O.build()
+    m = O.box_mesh(nx, ny, nz)
+    u = O.velocity(m.coords, init)
+    O.assemble_rsp(m.coords, m.connectivity, u, n_threads=T)
+    t0 = time.perf_counter()
+    O.assemble_rsp(m.coords, m.connectivity, u, n_threads=T)
+    per_step = time.perf_counter() - t0
+    total = max(steps, 1) + max(warmup, 0)
+    E = m.n_elems
+    sample_elems = E if per_step * total <= budget_s else max(int(E * budget_s / (per_step * total)), 6)
+    conn = np.ascontiguousarray(m.connectivity[:sample_elems])
+    for _ in range(max(warmup, 0)):
+        O.assemble_rsp(m.coords, conn, u, n_threads=T)
+    ts = []
+    for _ in range(max(steps, 1)):
+        t0 = time.perf_counter()
+        O.assemble_rsp(m.coords, conn, u, n_threads=T)
+        ts.append(time.perf_counter() - t0)
+    med = statistics.median(ts)
+    return {"value": sample_elems / med, "unit": "elem/s", "cores": T, "kind": "port",
+            "steps": len(ts), "median_s": med,
+            "sample": f"{'all' if sample_elems == E else 'first %d of the' % sample_elems} "
+                      f"{E} tets of a {nx}x{ny}x{nz} Kuhn box, {init}; C port of "
+                      f"_rsp_kernels.assemble_elements + the variants.py private driver "
+                      f"(reference not importable), {T} threads, median of {len(ts)}"}
+
+
 def run_reference(a) -> None:
+    """``--impl reference``: rank 0 alone times the reference's own CPU path on
+    the host cores on the sample of one rank's share of our arm's workload
+    (N=1: the whole config-2 box); the other ranks exit without work."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle import oracle as O
-    O.build()
-    c = a.cells
-    m = O.box_mesh(c, c, c)
-    u = O.velocity(m.coords, a.init)
-    T = O.default_threads()
-    E = m.n_elems
-    # bounded sample: whole mesh per step unless that would exceed ~150 s total
-    t0 = time.perf_counter()
-    O.assemble_rsp(m.coords, m.connectivity, u, n_threads=T)
-    first = time.perf_counter() - t0
-    total_steps = max(a.steps, 1) + max(a.warmup, 0)
-    sample_elems = E
-    if first * total_steps > 150.0:
-        sample_elems = max(int(E * 150.0 / (first * total_steps)), 6)
-    ids = np.arange(sample_elems, dtype=np.int64)
-    conn = np.ascontiguousarray(m.connectivity[:sample_elems])
-
-    def step():
-        return O.assemble_rsp(m.coords, conn, u, n_threads=T)
-
-    for _ in range(max(a.warmup, 0)):
-        step()
-    times = []
-    for _ in range(max(a.steps, 1)):
-        t0 = time.perf_counter()
-        step()
-        times.append(time.perf_counter() - t0)
-    tot = sum(times)
-    value = sample_elems * len(times) / tot
-    del ids
-    sample = (f"{'full' if sample_elems == E else 'first %d of' % sample_elems} "
-              f"{c}^3 Kuhn box ({E} tets), {a.init}, C port of _rsp_kernels.assemble_elements "
-              f"with the variants.py private driver, {T} threads, per step")
+    c = cells_of(a)
+    gz = c * ws if a.scaling == "weak" else c
+    local_z = gz // ws if ws > 1 else gz
+    cb = reference_cpu((c, c, max(local_z, 1)), a.init, a.steps, a.warmup)
+    if ws == 1:
+        workload = f"{c}^3 Kuhn box, {a.init}"
+    elif a.scaling == "weak":
+        workload = f"{c}x{c}x{gz} Kuhn box, a {c}^3 slab per rank ({ws} ranks), {a.init}"
+    else:
+        workload = f"{c}^3 Kuhn box cut into {ws} z-slabs, {a.init}"
     line = {
-        "impl": "reference", "metric": "assembled elements/s", "value": value,
-        "unit": "elem/s", "n_gpus": ws, "steps": len(times), "warmup": a.warmup,
-        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "impl": "reference", "metric": "assembled elements/s", "value": cb["value"],
+        "unit": "elem/s", "n_gpus": ws, "steps": cb["steps"], "warmup": a.warmup,
+        "ms_per_step": 1e3 * cb["median_s"], "higher_is_better": True, "scaling": a.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{c}^3 Kuhn box, {a.init}", "n_elems": E, "n_nodes": m.n_nodes},
-        "cpu_baseline": {"value": value, "unit": "elem/s", "cores": T, "kind": "port",
-                         "sample": sample},
-        "e2e": {"value": value, "unit": "elem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": workload, "box_cells": [c, c, gz], "host_only": True},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "elem/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -211,14 +311,22 @@ def measured_hbm_peak():
         return 6532.9, "MEASURED_PEAKS.json value at round start (file absent on this box)"
 
 
-def ncu_traffic(kernel_key: str, workload: str):
+def traffic_key(a, workload: str) -> str:
+    """profiles/traffic.json key: the workload AND everything that changes the
+    kernel's memory behaviour (node numbering, element order, chunking)."""
+    return (f"{workload} | permuted={int(bool(a.permute))} renumber={a.renumber} "
+            f"element_order={a.element_order} patches={a.patches} cta={a.cta_patches} "
+            f"chunk_nodes={a.chunk_nodes} pressure={int(bool(a.pressure))}")
+
+
+def ncu_traffic(kernel_key: str, key: str) -> dict:
+    """ncu --set full figures for this exact configuration (tools/update_traffic.py),
+    or {} when none was captured."""
     p = ROOT / "profiles" / "traffic.json"
     try:
-        d = json.loads(p.read_text())
-        ent = d.get(workload, {}).get(kernel_key)
-        return None if ent is None else float(ent["dram_bytes_per_launch"])
+        return dict(json.loads(p.read_text()).get(key, {}).get(kernel_key) or {})
     except Exception:
-        return None
+        return {}
 
 
 def run_ours(a) -> None:
@@ -233,7 +341,10 @@ def run_ours(a) -> None:
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        backend = os.environ.get("TAL_DIST_BACKEND", "nccl")  # gloo: host-staged validation
+        # gloo: host-staged validation runs with ranks time-sharing fewer GPUs
+        # (NCCL refuses two ranks on one device)
+        backend = os.environ.get("TAL_DIST_BACKEND",
+                                 "nccl" if torch.cuda.device_count() >= ws else "gloo")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
@@ -242,12 +353,15 @@ def run_ours(a) -> None:
     cfg = tb.RunConfig(scatter=a.scatter, renumber=a.renumber, element_order=a.element_order,
                        patches=a.patches, cta_patches=a.cta_patches, chunk_nodes=a.chunk_nodes,
                        device=dev)
-    c = a.cells
+    c = cells_of(a)
+    gz = c * ws if a.scaling == "weak" else c  # global box: (c, c, gz)
+    if gz < ws:
+        raise SystemExit(f"bench.py: {gz} cell layers cannot be split over {ws} ranks")
     t0 = time.perf_counter()
     gperm = None
     if ws > 1 and a.partition == "rcb":
         from paper_2403_08777_b200.distributed import PartitionedDomain
-        g = tb.generate_box_mesh(c, c, c * ws)
+        g = tb.generate_box_mesh(c, c, gz)
         if a.permute:
             gperm = np.random.default_rng(0).permutation(g.n_nodes)
             g = tb.permute_nodes(g, gperm)
@@ -257,7 +371,7 @@ def run_ours(a) -> None:
         del g
     elif ws > 1:
         from paper_2403_08777_b200.distributed import SlabDomain
-        dom = SlabDomain((c, c, c * ws), rank, ws, cfg)
+        dom = SlabDomain((c, c, gz), rank, ws, cfg)
         mesh, u = dom.mesh, dom.velocity(a.init)
         asm = dom.assembler
     else:
@@ -329,10 +443,17 @@ def run_ours(a) -> None:
     wall1 = time.perf_counter()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     kern_ms = asm.profile_read()
-    if use_graph:  # the graph carries no profile events: time the kernel in plain steps
+    fused = dom is not None and dom.fused
+    if use_graph or fused or not len(kern_ms):
+        # a replayed graph carries no profile events: time the dominant kernel
+        # in plain launches of the same step (with peers attached a plain run
+        # is the whole fused step: every rank runs the same count)
         for _ in range(min(a.steps, 50)):
             flush()
-            asm.run(P, stream=stream, variant=a.variant)
+            if dom is None or fused:
+                asm.run(P, stream=stream, variant=a.variant)
+            else:
+                dom.step(P, stream=stream)
         torch.cuda.synchronize()
         kern_ms = asm.profile_read()
     # nvidia-smi polls the driver every 50 ms: stop it before the wall-clock
@@ -343,9 +464,52 @@ def run_ours(a) -> None:
         t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    units = E * ws * a.steps
+    E_all = E * ws
+    kmean = float(np.mean(kern_ms))
+    step_mean = float(np.mean(step_ms))
+    rate = E / (kmean * 1e-3)  # dominant-kernel elements/s of this GPU
+    bytes_per_elem = (16 * E + 72 * Nn) / E if E else 0.0
+    if dist:  # whole-job elements; slowest rank's kernel, step and kernel rate
+        e = torch.tensor([float(E)], device=f"cuda:{dev}", dtype=torch.float64)
+        t = torch.tensor([kmean, step_mean], device=f"cuda:{dev}", dtype=torch.float64)
+        r = torch.tensor([rate], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(r, op=dist.ReduceOp.MIN)
+        E_all, kmean, step_mean, rate = int(e.item()), float(t[0].item()), float(t[1].item()), \
+            float(r.item())
+    units = E_all * a.steps
     value = units / (total_ms * 1e-3)
 
+    # device-resident in the CALLER's layout: a solver that keeps u and rhs as
+    # (N,3) AoS device arrays in its own node numbering pays the layout
+    # conversion every step: set_velocity_device (k_pack_velocity, renumbered
+    # gather) -> assembly -> get_rhs_device (k_unpack_aos); CUDA events
+    caller_layout = None
+    if dom is None and a.variant == "rsp":
+        u_dev = torch.as_tensor(u, device=f"cuda:{dev}").contiguous()
+        r_dev = torch.empty_like(u_dev)
+        ks = max(min(a.steps, 100), 3)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * ks)]
+        for _ in range(3):
+            asm.set_velocity_device(u_dev.data_ptr(), stream=stream)
+            one_step()
+            asm.get_rhs_device(r_dev.data_ptr(), stream=stream)
+        torch.cuda.synchronize()
+        for i in range(ks):
+            flush()
+            ev[2 * i].record()
+            asm.set_velocity_device(u_dev.data_ptr(), stream=stream)
+            one_step()
+            asm.get_rhs_device(r_dev.data_ptr(), stream=stream)
+            ev[2 * i + 1].record()
+        torch.cuda.synchronize()
+        cl_ms = float(np.mean([ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(ks)]))
+        caller_layout = {"value": E / (cl_ms * 1e-3), "unit": "elem/s", "ms_per_step": cl_ms,
+                         "steps": ks,
+                         "api": "Assembler.set_velocity_device -> step -> get_rhs_device on (N,3) "
+                                "caller-order device arrays, CUDA events, L2 flushed between steps"}
+        del u_dev, r_dev
     # end-to-end through the public host API (pinned host buffers): every step
     # copies that step's u host->device and reads its rhs back device->host.
     #  sync     : Assembler.assemble_into (one field at a time, blocking)
@@ -441,19 +605,11 @@ def run_ours(a) -> None:
     if ws == 1 and not a.no_cpu_baseline:
         from oracle import oracle as O
         O.build()
-        T = O.default_threads()
         rhs_gpu, _ = asm.assemble(u, P, variant=a.variant)
-        O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)  # warm-up
-        ts = []
-        ref = None
-        for _ in range(3):
-            t1 = time.perf_counter()
-            ref = O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=T)
-            ts.append(time.perf_counter() - t1)
-        med = statistics.median(ts)
-        cpu_baseline = {"value": E / med, "unit": "elem/s", "cores": T, "kind": "port",
-                        "sample": f"full {c}^3 mesh ({E} tets), {a.init}; C port of the reference "
-                                  f"numba kernel + private driver, 1 warm-up + median of 3"}
+        # bounded sample of the same workload on all host cores (the reference's
+        # own numba path when importable); the oracle's vector is the checker
+        cpu_baseline = reference_cpu((c, c, c), a.init, 3, 0, budget_s=30.0)
+        ref = O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=O.default_threads())
         if press is not None:
             ref = ref + O.pressure_gradient(mesh.coords, mesh.connectivity, press)
         chk = O.compare(rhs_gpu, ref, mesh.coords, mesh.connectivity, u)
@@ -466,7 +622,7 @@ def run_ours(a) -> None:
         if rank == 0:
             from oracle import oracle as O
             O.build()
-            g = O.box_mesh(c, c, c * ws)
+            g = O.box_mesh(c, c, gz)
             if gperm is not None:  # the permuted global mesh the ranks partitioned
                 gm = tb.permute_nodes(tb.Mesh(coords=g.coords, connectivity=g.connectivity), gperm)
                 g = O.OracleMesh(np.ascontiguousarray(gm.coords), np.ascontiguousarray(gm.connectivity))
@@ -481,10 +637,15 @@ def run_ours(a) -> None:
                       "gathered": f"owned rows of {ws} ranks vs single-domain oracle"}
     asm.profile(False)
 
-    kmean = float(np.mean(kern_ms)) if len(kern_ms) else float("nan")
-    workload = f"{c}^3 Kuhn box{' x%d slabs' % ws if ws > 1 else ''}, {a.init}"
-    tf = FLOP_PER_ELEM * E / (kmean * 1e-3) / 1e12
+    if ws == 1:
+        workload = f"{c}^3 Kuhn box, {a.init}"
+    elif a.scaling == "weak":
+        workload = f"{c}x{c}x{gz} Kuhn box, a {c}^3 slab per rank ({ws} ranks), {a.init}"
+    else:
+        workload = f"{c}^3 Kuhn box cut into {ws} z-slabs, {a.init}"
+    tf = FLOP_PER_ELEM * rate / 1e12  # per GPU (the slowest rank at N>1)
     alg_bytes = 16 * E + 72 * Nn  # int32 conn + coords/u read + rhs write
+    hbm_gbs = bytes_per_elem * rate / 1e9
     hbm_peak, hbm_src = measured_hbm_peak()
     kname = {"private": "k_assemble_private<cfg,ordered=true>",
              "private-atomic": "k_assemble_private<cfg,ordered=false>",
@@ -495,19 +656,23 @@ def run_ours(a) -> None:
         kname = {"b": "k_assemble_baseline", "p": "k_assemble_baseline<fixed>",
                  "rs": "k_assemble_rs"}[a.variant] + \
             ("<colored> (all colours)" if colored else "<atomic>")
-    traffic = ncu_traffic(kname, workload)
+    tr = ncu_traffic(kname, traffic_key(a, workload))
+    traffic = tr.get("dram_bytes_per_launch")
     line = {
         "metric": "assembled elements/s", "value": value, "unit": "elem/s", "n_gpus": ws,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated Kuhn box mesh, seeded velocity)",
-        "config": {"workload": workload, "n_elems": E, "n_nodes": Nn, "scatter": a.scatter,
+        "config": {"workload": workload, "n_elems": E_all, "n_elems_rank0": E, "n_nodes_rank0": Nn,
+                   "box_cells": [c, c, gz], "scatter": a.scatter,
                    "renumber": a.renumber, "element_order": a.element_order,
                    "patches": a.patches, "cta_patches": a.cta_patches, "chunk_nodes": a.chunk_nodes,
                    "permuted": bool(a.permute), "variant": a.variant,
                    "pressure_term": bool(a.pressure), "cuda_graph": bool(use_graph),
                    "l2": "flushed (256 MiB write) before every step, outside the timed events"
                          if flush_buf is not None else "not flushed",
+                   "gpus_shared": torch.cuda.device_count() < ws,
+                   "traffic_key": traffic_key(a, workload),
                    "parallelism": (f"dp{ws} z-slabs" if a.partition == "slab" else f"dp{ws} RCB parts")
                    if ws > 1 else "single GPU",
                    "interface_sum": None if dom is None else (
@@ -523,11 +688,17 @@ def run_ours(a) -> None:
                      "frac_of_nominal": tf / NOMINAL_FP64_TFLOPS,
                      "probe_sm_mhz": fp64_mhz,
                      "flop_per_elem": FLOP_PER_ELEM, "kernel_ms": kmean,
+                     "per": "GPU" if ws == 1 else "GPU (slowest rank's kernel rate)",
+                     "step_ms_mean": step_mean,
+                     "non_kernel_ms_per_step": step_mean - kmean,
                      "traffic": traffic,
-                     "hbm": {"achieved": alg_bytes / (kmean * 1e-3) / 1e9, "peak": hbm_peak,
-                             "unit": "GB/s", "frac": alg_bytes / (kmean * 1e-3) / 1e9 / hbm_peak,
+                     "traffic_source": tr.get("source"),
+                     "l2_sector_bytes": tr.get("l2_sector_bytes_per_launch"),
+                     "hbm": {"achieved": hbm_gbs, "peak": hbm_peak,
+                             "unit": "GB/s", "frac": hbm_gbs / hbm_peak,
                              "alg_bytes_per_launch": alg_bytes, "peak_source": hbm_src}},
         "e2e": e2e,
+        "device_caller_layout": caller_layout,
         "cpu_baseline": cpu_baseline,
         "parity": parity,
         "gpu_launches": launches,
@@ -547,6 +718,9 @@ def run_ours(a) -> None:
 
 def main():
     a = parse()
+    rc = self_launch(a)
+    if rc is not None:
+        sys.exit(rc)
     if a.impl == "reference":
         run_reference(a)
     else:

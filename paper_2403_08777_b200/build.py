@@ -61,7 +61,7 @@ def build(verbose: bool = False, force: bool = False, out: Path = OUT, defines=(
     log = []
     for src in sorted(CSRC.glob("*.cpp")):
         obj = BUILD / (src.stem + tag + ".o")
-        cmd = ["g++", "-O3", "-fPIC", "-std=c++17", "-Wall", *dflags, "-c", str(src), "-o", str(obj)]
+        cmd = ["g++", "-O3", "-fPIC", "-pthread", "-std=c++17", "-Wall", *dflags, "-c", str(src), "-o", str(obj)]
         subprocess.run(cmd, check=True)
         objs.append(obj)
     for src in sorted(CSRC.glob("*.cu")):

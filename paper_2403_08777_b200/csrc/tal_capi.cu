@@ -19,6 +19,7 @@
 #include "tal_kernels.cuh"
 #include "tal_strict.cuh"
 #include "tal_prep.hpp"
+#include "tal_par.hpp"
 #include "tal_shapes.cuh"
 
 using namespace tal;
@@ -754,28 +755,35 @@ void shared_tail_renumber(int64_t n_nodes, HostLayout &L)
             nid[v] = next++;
     const bool had = !L.perm.empty();
     std::vector<int32_t> perm((size_t)n_nodes), iperm((size_t)n_nodes);
-    for (int64_t v = 0; v < n_nodes; ++v) {
-        const int32_t caller = had ? L.perm[v] : (int32_t)v;
-        perm[nid[v]] = caller;
-        iperm[caller] = nid[v];
-    }
+    std::vector<double> xin((size_t)(3 * n_nodes));
+    parallel_for(n_nodes, [&](int64_t v0, int64_t v1, int) {  // nid is a permutation: disjoint writes
+        for (int64_t v = v0; v < v1; ++v) {
+            const int32_t caller = had ? L.perm[v] : (int32_t)v;
+            perm[nid[v]] = caller;
+            iperm[caller] = nid[v];
+            for (int c = 0; c < 3; ++c)
+                xin[3 * (int64_t)nid[v] + c] = L.xin[3 * v + c];
+        }
+    });
     L.perm.swap(perm);
     L.iperm.swap(iperm);
-    std::vector<double> xin((size_t)(3 * n_nodes));
-    for (int64_t v = 0; v < n_nodes; ++v)
-        for (int c = 0; c < 3; ++c)
-            xin[3 * (int64_t)nid[v] + c] = L.xin[3 * v + c];
     L.xin.swap(xin);
-    for (auto &x : L.cord)
-        x = nid[x];
-    for (auto &x : L.patches.nodes)
-        x = nid[x];
-    for (auto &x : L.ch.gather_nodes)
-        x = nid[x];
-    for (auto &x : L.ch.bnd_nodes)
-        x = nid[x];
-    for (auto &x : L.ch.cnodes)
-        x = (int32_t)(((uint32_t)x & 0x80000000u) | (uint32_t)nid[x & 0x7fffffff]);
+    auto remap = [&](std::vector<int32_t> &a) {
+        parallel_for((int64_t)a.size(), [&](int64_t i0, int64_t i1, int) {
+            for (int64_t i = i0; i < i1; ++i)
+                a[i] = nid[a[i]];
+        });
+    };
+    remap(L.cord);
+    remap(L.patches.nodes);
+    remap(L.ch.gather_nodes);
+    remap(L.ch.bnd_nodes);
+    parallel_for((int64_t)L.ch.cnodes.size(), [&](int64_t i0, int64_t i1, int) {
+        for (int64_t i = i0; i < i1; ++i) {
+            const int32_t x = L.ch.cnodes[i];
+            L.ch.cnodes[i] = (int32_t)(((uint32_t)x & 0x80000000u) | (uint32_t)nid[x & 0x7fffffff]);
+        }
+    });
 }
 
 int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
@@ -801,25 +809,34 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
     const bool renum = !L.perm.empty();
     if (renum) {
         L.iperm.resize((size_t)n_nodes);
-        for (int64_t i = 0; i < n_nodes; ++i)
-            L.iperm[L.perm[i]] = (int32_t)i;
+        parallel_for(n_nodes, [&](int64_t i0, int64_t i1, int) {
+            for (int64_t i = i0; i < i1; ++i)
+                L.iperm[L.perm[i]] = (int32_t)i;
+        });
     }
     L.xin.resize((size_t)(3 * n_nodes));  // internal AoS coords
-    for (int64_t i = 0; i < n_nodes; ++i) {
-        const int64_t s = renum ? L.perm[i] : i;
-        for (int c = 0; c < 3; ++c)
-            L.xin[3 * i + c] = coords[3 * s + c];
-    }
+    parallel_for(n_nodes, [&](int64_t i0, int64_t i1, int) {
+        for (int64_t i = i0; i < i1; ++i) {
+            const int64_t s = renum ? L.perm[i] : i;
+            for (int c = 0; c < 3; ++c)
+                L.xin[3 * i + c] = coords[3 * s + c];
+        }
+    });
     std::vector<int32_t> cin((size_t)(4 * n_elems));
-    for (int64_t i = 0; i < 4 * n_elems; ++i)
-        cin[i] = renum ? L.iperm[conn[i]] : (int32_t)conn[i];
+    parallel_for(4 * n_elems, [&](int64_t i0, int64_t i1, int) {
+        for (int64_t i = i0; i < i1; ++i)
+            cin[i] = renum ? L.iperm[conn[i]] : (int32_t)conn[i];
+    });
+    lap("relabel");
     // element order
     element_order(opts.element_order, cin.data(), L.xin.data(), n_nodes, n_elems, L.eperm);
     lap("element order");
     L.cord.resize((size_t)(4 * n_elems));
-    for (int64_t e = 0; e < n_elems; ++e)
-        for (int a = 0; a < 4; ++a)
-            L.cord[4 * e + a] = cin[4 * (int64_t)L.eperm[e] + a];
+    parallel_for(n_elems, [&](int64_t e0, int64_t e1, int) {
+        for (int64_t e = e0; e < e1; ++e)
+            for (int a = 0; a < 4; ++a)
+                L.cord[4 * e + a] = cin[4 * (int64_t)L.eperm[e] + a];
+    });
     // chunks
     std::string err;
     const int cfg = cfg_for(opts.cta_patches);
@@ -829,6 +846,7 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
                                     "], chunk_nodes in [16," + std::to_string(cfg_max_nodes(cfg)) +
                                     "], patch_mode 0|1");
     L.cfg = cfg;
+    lap("reorder");
     build_patches(L.cord.data(), n_nodes, n_elems, opts.patch_mode, L.patches);
     lap("patches");
     std::vector<uint8_t> ext;
@@ -1018,9 +1036,18 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
         opts = *opts_in;
     const auto t0 = std::chrono::steady_clock::now();
     // validation (Mesh.__post_init__, mesh.py:50-75)
-    for (int64_t i = 0; i < 4 * n_elems; ++i)
-        if (conn[i] < 0 || conn[i] >= n_nodes)
+    {
+        std::atomic<bool> bad{false};
+        parallel_for(4 * n_elems, [&](int64_t i0, int64_t i1, int) {
+            for (int64_t i = i0; i < i1; ++i)
+                if (conn[i] < 0 || conn[i] >= n_nodes) {
+                    bad = true;
+                    return;
+                }
+        });
+        if (bad)
             return fail(TAL_EINVAL, "connectivity index out of range [0, n_nodes)");
+    }
     if (opts.validate && n_elems) {
         std::vector<double> vols((size_t)n_elems);
         signed_volumes(coords, conn, n_elems, vols.data());

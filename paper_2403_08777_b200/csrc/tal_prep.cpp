@@ -3,10 +3,16 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <memory>
+#include <chrono>
+#include <cstdio>
+
+#include "tal_par.hpp"
 
 namespace tal {
 
@@ -55,7 +61,8 @@ void box_mesh(int64_t nx, int64_t ny, int64_t nz, double ex, double ey, double e
 
 void signed_volumes(const double *coords, const int64_t *conn, int64_t n_elems, double *vols)
 {
-    for (int64_t e = 0; e < n_elems; ++e) {
+    parallel_for(n_elems, [&](int64_t e0, int64_t e1, int) {
+    for (int64_t e = e0; e < e1; ++e) {
         const double *p0 = coords + 3 * conn[4 * e];
         double d[3][3];
         for (int b = 0; b < 3; ++b) {
@@ -68,6 +75,7 @@ void signed_volumes(const double *coords, const int64_t *conn, int64_t n_elems, 
                            d[0][2] * (d[1][0] * d[2][1] - d[1][1] * d[2][0]);
         vols[e] = det / 6.0;
     }
+    });
 }
 
 int64_t color_elements(const int64_t *conn, int64_t n_nodes, int64_t n_elems, int64_t *colors)
@@ -126,41 +134,84 @@ void node_elements(const int64_t *conn, int64_t n_nodes, int64_t n_elems,
             adj[pos[conn[4 * e + a]]++] = (int32_t)e;
 }
 
-// one BFS from 'start' over unvisited nodes; neighbours of a node are the
-// other nodes of its incident elements; neighbours are appended in order of
-// increasing valence (Cuthill-McKee).  Returns the visit order; 'mark' is set.
-void cm_bfs(int64_t start, const int64_t *conn, const std::vector<int64_t> &off,
-            const std::vector<int32_t> &adj, std::vector<int32_t> &mark, int32_t tag,
-            std::vector<int32_t> &order, int64_t *last_level_begin)
+// Node-node adjacency for Cuthill-McKee: the neighbours of v (the other
+// nodes of its incident elements), each list sorted by (valence, id) with
+// valence = incident element count.  Built in parallel over nodes.
+void cm_neighbours(const int64_t *conn, int64_t n_nodes, const std::vector<int64_t> &off,
+                   const std::vector<int32_t> &adj, std::vector<int64_t> &noff, std::vector<int32_t> &nbr)
+{
+    const int T = prep_threads();
+    std::vector<std::vector<int32_t>> part((size_t)T);
+    std::vector<int64_t> cnt((size_t)n_nodes + 1, 0);
+    std::vector<int64_t> tb((size_t)T + 1, 0);
+    parallel_for(n_nodes, [&](int64_t v0, int64_t v1, int t) {
+        auto &out = part[(size_t)t];
+        std::vector<int32_t> nb;
+        std::vector<int32_t> seen((size_t)n_nodes, -1);  // dedup stamp: last v that saw w
+        for (int64_t v = v0; v < v1; ++v) {
+            nb.clear();
+            seen[v] = (int32_t)v;
+            for (int64_t p = off[v]; p < off[v + 1]; ++p) {
+                const int64_t e = adj[p];
+                for (int a = 0; a < 4; ++a) {
+                    const int64_t w = conn[4 * e + a];
+                    if (seen[w] != (int32_t)v) {
+                        seen[w] = (int32_t)v;
+                        nb.push_back((int32_t)w);
+                    }
+                }
+            }
+            std::sort(nb.begin(), nb.end(), [&](int32_t a, int32_t b) {
+                const int64_t da = off[a + 1] - off[a], db = off[b + 1] - off[b];
+                return da != db ? da < db : a < b;
+            });
+            cnt[v + 1] = (int64_t)nb.size();
+            out.insert(out.end(), nb.begin(), nb.end());
+        }
+    }, 1 << 12);
+    noff.assign((size_t)n_nodes + 1, 0);
+    for (int64_t v = 0; v < n_nodes; ++v)
+        noff[v + 1] = noff[v] + cnt[v + 1];
+    nbr.resize((size_t)noff[n_nodes]);
+    // the blocks of parallel_for are contiguous and in thread order
+    int64_t at = 0;
+    for (auto &pv : part) {
+        std::copy(pv.begin(), pv.end(), nbr.begin() + at);
+        at += (int64_t)pv.size();
+    }
+}
+
+// one BFS from 'start' over unvisited nodes; each node's unvisited
+// neighbours are appended in order of increasing valence (Cuthill-McKee):
+// the presorted list filtered by the mark is exactly that order.  Returns the
+// visit order; 'mark' is set.
+void cm_bfs(int64_t start, const std::vector<int64_t> &noff, const std::vector<int32_t> &nbr,
+            std::vector<uint8_t> &mark, uint8_t tag, std::vector<int32_t> &order, int64_t *last_level_begin)
 {
     order.clear();
     order.push_back((int32_t)start);
     mark[start] = tag;
     size_t head = 0, level_end = 1;
     *last_level_begin = 0;
-    std::vector<int32_t> nb;
     while (head < order.size()) {
         if (head == level_end) {
             *last_level_begin = (int64_t)head;
             level_end = order.size();
         }
+        if (head + 8 < order.size()) {  // the queue is known ahead: hide the list-start miss
+            const int32_t f = order[head + 8];
+            __builtin_prefetch(&noff[f]);
+            if (head + 4 < order.size())
+                __builtin_prefetch(&nbr[noff[order[head + 4]]]);
+        }
         const int32_t v = order[head++];
-        nb.clear();
-        for (int64_t p = off[v]; p < off[v + 1]; ++p) {
-            const int64_t e = adj[p];
-            for (int a = 0; a < 4; ++a) {
-                const int64_t w = conn[4 * e + a];
-                if (mark[w] != tag) {
-                    mark[w] = tag;
-                    nb.push_back((int32_t)w);
-                }
+        for (int64_t p = noff[v]; p < noff[v + 1]; ++p) {
+            const int32_t w = nbr[p];
+            if (mark[w] != tag) {
+                mark[w] = tag;
+                order.push_back(w);
             }
         }
-        std::sort(nb.begin(), nb.end(), [&](int32_t a, int32_t b) {
-            const int64_t da = off[a + 1] - off[a], db = off[b + 1] - off[b];
-            return da != db ? da < db : a < b;
-        });
-        order.insert(order.end(), nb.begin(), nb.end());
     }
 }
 
@@ -182,18 +233,45 @@ uint64_t spread3(uint64_t v)
 // bounding-box code breaks ties; without one, the bounding-box code only.
 inline bool p_ok(double lo, double origin) { return lo >= origin; }
 
+struct Lap {
+    const char *what;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    static bool on() { static const bool b = std::getenv("TAL_PREP_TIMES") != nullptr; return b; }
+    void operator()(const char *sub) {
+        auto t = std::chrono::steady_clock::now();
+        if (on())
+            std::fprintf(stderr, "[tal prep]   %s/%s %.3f s\n", what, sub, std::chrono::duration<double>(t - t0).count());
+        t0 = t;
+    }
+};
+
 template <class GetPoint>
 void morton_order(int64_t n, GetPoint pt, std::vector<int32_t> &perm, const double *cell = nullptr,
                   const double *origin = nullptr)
 {
+    Lap lap{"morton"};
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int64_t i = 0; i < n; ++i) {
-        double p[3];
-        pt(i, p);
-        for (int c = 0; c < 3; ++c) {
-            lo[c] = std::min(lo[c], p[c]);
-            hi[c] = std::max(hi[c], p[c]);
-        }
+    {
+        const int T = prep_threads();
+        std::vector<std::array<double, 6>> box((size_t)T);
+        for (auto &b : box)
+            b = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        parallel_for(n, [&](int64_t i0, int64_t i1, int t) {
+            auto &b = box[(size_t)t];
+            for (int64_t i = i0; i < i1; ++i) {
+                double p[3];
+                pt(i, p);
+                for (int c = 0; c < 3; ++c) {
+                    b[c] = std::min(b[c], p[c]);
+                    b[3 + c] = std::max(b[3 + c], p[c]);
+                }
+            }
+        });
+        for (auto &b : box)  // min / max: exact in any order
+            for (int c = 0; c < 3; ++c) {
+                lo[c] = std::min(lo[c], b[c]);
+                hi[c] = std::max(hi[c], b[3 + c]);
+            }
     }
     double span = 0.0;
     for (int c = 0; c < 3; ++c)
@@ -211,47 +289,77 @@ void morton_order(int64_t n, GetPoint pt, std::vector<int32_t> &perm, const doub
         }
     };
     std::vector<Key> key((size_t)n);
-    for (int64_t i = 0; i < n; ++i) {
-        double p[3];
-        pt(i, p);
-        uint64_t fine = 0, coarse = 0;
-        for (int c = 0; c < 3; ++c) {
-            fine |= spread3((uint64_t)((p[c] - lo[c]) * scale)) << c;
-            if (grid)
-                coarse |= spread3((uint64_t)((p[c] - origin[c]) / cell[c])) << c;
+    parallel_for(n, [&](int64_t i0, int64_t i1, int) {
+        for (int64_t i = i0; i < i1; ++i) {
+            double p[3];
+            pt(i, p);
+            uint64_t fine = 0, coarse = 0;
+            for (int c = 0; c < 3; ++c) {
+                fine |= spread3((uint64_t)((p[c] - lo[c]) * scale)) << c;
+                if (grid)
+                    coarse |= spread3((uint64_t)((p[c] - origin[c]) / cell[c])) << c;
+            }
+            key[i] = {coarse, fine, (int32_t)i};
         }
-        key[i] = {coarse, fine, (int32_t)i};
-    }
-    std::sort(key.begin(), key.end());
+    });
+    lap("bbox+keys");
+    psort(key, [](const Key &a, const Key &b) { return a < b; });  // keys unique (index)
+    lap("sort");
     perm.resize((size_t)n);
-    for (int64_t i = 0; i < n; ++i)
-        perm[i] = key[i].i;
+    parallel_for(n, [&](int64_t i0, int64_t i1, int) {
+        for (int64_t i = i0; i < i1; ++i)
+            perm[i] = key[i].i;
+    });
 }
 
 }  // namespace
 
 void renumber_rcm(const int64_t *conn, int64_t n_nodes, int64_t n_elems, std::vector<int32_t> &perm)
 {
+    Lap lap{"rcm"};
     std::vector<int64_t> off;
     std::vector<int32_t> adj;
     node_elements(conn, n_nodes, n_elems, off, adj);
-    std::vector<int32_t> mark((size_t)n_nodes, 0), done((size_t)n_nodes, 0);
+    lap("node_elements");
+    std::vector<int64_t> noff;
+    std::vector<int32_t> nbr;
+    cm_neighbours(conn, n_nodes, off, adj, noff, nbr);
+    lap("neighbours");
+    // byte marks (a BFS is latency bound on them: 1 B per node keeps them in
+    // cache); tags cycle through 1..255 with a clear on wrap-around
+    std::vector<uint8_t> mark((size_t)n_nodes, 0), done((size_t)n_nodes, 0);
     std::vector<int32_t> order, result;
     result.reserve((size_t)n_nodes);
-    int32_t tag = 0;
+    int tag = 0;
+    auto next_tag = [&]() -> uint8_t {
+        if (++tag == 256) {
+            std::fill(mark.begin(), mark.end(), 0);
+            tag = 1;
+        }
+        return (uint8_t)tag;
+    };
     // components in order of their smallest-valence seed
+    // (= stable sort by valence, as a counting sort)
     std::vector<int32_t> seeds((size_t)n_nodes);
-    std::iota(seeds.begin(), seeds.end(), 0);
-    std::stable_sort(seeds.begin(), seeds.end(), [&](int32_t a, int32_t b) {
-        return off[a + 1] - off[a] < off[b + 1] - off[b];
-    });
+    {
+        int64_t vmax = 0;
+        for (int64_t v = 0; v < n_nodes; ++v)
+            vmax = std::max(vmax, off[v + 1] - off[v]);
+        std::vector<int64_t> at((size_t)vmax + 2, 0);
+        for (int64_t v = 0; v < n_nodes; ++v)
+            at[off[v + 1] - off[v] + 1]++;
+        for (int64_t k = 0; k <= vmax; ++k)
+            at[k + 1] += at[k];
+        for (int64_t v = 0; v < n_nodes; ++v)
+            seeds[at[off[v + 1] - off[v]]++] = (int32_t)v;
+    }
     for (int32_t s : seeds) {
         if (done[s])
             continue;
         // pseudo-peripheral start: two sweeps (George-Liu style)
         int64_t start = s, llb = 0;
         for (int sweep = 0; sweep < 2; ++sweep) {
-            cm_bfs(start, conn, off, adj, mark, ++tag, order, &llb);
+            cm_bfs(start, noff, nbr, mark, next_tag(), order, &llb);
             int64_t best = order[llb];
             for (size_t i = (size_t)llb; i < order.size(); ++i) {
                 const int32_t v = order[i];
@@ -260,13 +368,14 @@ void renumber_rcm(const int64_t *conn, int64_t n_nodes, int64_t n_elems, std::ve
             }
             start = best;
         }
-        cm_bfs(start, conn, off, adj, mark, ++tag, order, &llb);
+        cm_bfs(start, noff, nbr, mark, next_tag(), order, &llb);
         for (int32_t v : order)
             done[v] = 1;
         result.insert(result.end(), order.begin(), order.end());
     }
     std::reverse(result.begin(), result.end());
     perm.swap(result);
+    lap("bfs");
 }
 
 void renumber_sfc(const double *coords, int64_t n_nodes, std::vector<int32_t> &perm)
@@ -287,11 +396,15 @@ void element_order(int method, const int32_t *conn4, const double *coords_int, i
     std::iota(eperm.begin(), eperm.end(), 0);
     if (method == 1) {  // by smallest node id
         std::vector<std::pair<int32_t, int32_t>> key((size_t)n_elems);
-        for (int64_t e = 0; e < n_elems; ++e) {
-            const int32_t *q = conn4 + 4 * e;
-            key[e] = {std::min(std::min(q[0], q[1]), std::min(q[2], q[3])), (int32_t)e};
-        }
-        std::sort(key.begin(), key.end());
+        parallel_for(n_elems, [&](int64_t e0, int64_t e1, int) {
+            for (int64_t e = e0; e < e1; ++e) {
+                const int32_t *q = conn4 + 4 * e;
+                key[e] = {std::min(std::min(q[0], q[1]), std::min(q[2], q[3])), (int32_t)e};
+            }
+        });
+        psort(key, [](const std::pair<int32_t, int32_t> &a, const std::pair<int32_t, int32_t> &b) {
+            return a < b;
+        });
         for (int64_t e = 0; e < n_elems; ++e)
             eperm[e] = key[e].second;
     } else if (method == 2) {  // Morton order of centroids on an element-size grid
@@ -302,26 +415,33 @@ void element_order(int method, const int32_t *conn4, const double *coords_int, i
         for (int64_t v = 0; v < n_nodes; ++v)
             for (int c = 0; c < 3; ++c)
                 lo[c] = std::min(lo[c], coords_int[3 * v + c]);
-        for (int64_t e = 0; e < n_elems; ++e) {
-            const int32_t *q = conn4 + 4 * e;
-            for (int c = 0; c < 3; ++c) {
-                double a = coords_int[3 * q[0] + c], b = a;
-                for (int k = 1; k < 4; ++k) {
-                    a = std::min(a, coords_int[3 * q[k] + c]);
-                    b = std::max(b, coords_int[3 * q[k] + c]);
+        // extents and centroids in one parallel gather; extents summed in
+        // element order (the serial bits)
+        std::unique_ptr<double[]> ext(new double[(size_t)(3 * n_elems)]);  // no zero fill
+        std::unique_ptr<double[]> cen(new double[(size_t)(3 * n_elems)]);
+        parallel_for(n_elems, [&](int64_t e0, int64_t e1, int) {
+            for (int64_t e = e0; e < e1; ++e) {
+                const int32_t *q = conn4 + 4 * e;
+                for (int c = 0; c < 3; ++c) {
+                    const double x0 = coords_int[3 * q[0] + c], x1 = coords_int[3 * q[1] + c];
+                    const double x2 = coords_int[3 * q[2] + c], x3 = coords_int[3 * q[3] + c];
+                    ext[3 * e + c] = std::max(std::max(std::max(x0, x1), x2), x3) -
+                                     std::min(std::min(std::min(x0, x1), x2), x3);
+                    cen[3 * e + c] = 0.25 * (x0 + x1 + x2 + x3);
                 }
-                cell[c] += b - a;
             }
-        }
+        });
+        for (int64_t e = 0; e < n_elems; ++e)
+            for (int c = 0; c < 3; ++c)
+                cell[c] += ext[3 * e + c];
+        ext.reset();
         for (int c = 0; c < 3; ++c)
             cell[c] = n_elems ? cell[c] / (double)n_elems : 0.0;
         morton_order(
             n_elems,
             [&](int64_t e, double p[3]) {
-                const int32_t *q = conn4 + 4 * e;
                 for (int c = 0; c < 3; ++c)
-                    p[c] = 0.25 * (coords_int[3 * q[0] + c] + coords_int[3 * q[1] + c] +
-                                   coords_int[3 * q[2] + c] + coords_int[3 * q[3] + c]);
+                    p[c] = cen[3 * e + c];
             },
             eperm, cell, lo);
     }
@@ -334,33 +454,64 @@ struct Arc {
     bool closed = false;
 };
 
-// ring of unassigned tets around edge (p,q) that contains tet t
-void ring_arc(int32_t t, int32_t p, int32_t q, const int32_t *conn4, const std::vector<int64_t> &off,
-              const std::vector<int32_t> &adj, const std::vector<uint8_t> &assigned, Arc &arc)
-{
-    // candidate tets: unassigned, contain p and q; their ring edge (c,d)
-    struct Cand {
-        int32_t tet, c, d;
-        bool used;
-    };
+// ring candidates of one edge (p,q) of the current tet: the unassigned tets
+// containing p and q (in adj[p] order, at most 64) with their two other
+// corners (c,d)
+struct Cand {
+    int32_t tet, c, d;
+    bool used;
+};
+struct EdgeCands {
     Cand cand[64];
-    int nc = 0;
-    for (int64_t k = off[p]; k < off[p + 1] && nc < 64; ++k) {
-        const int32_t s = adj[k];
-        if (assigned[s])
-            continue;
-        const int32_t *v = conn4 + 4 * (int64_t)s;
-        bool hq = false;
-        int32_t o[2], no = 0;
-        for (int a = 0; a < 4; ++a) {
-            if (v[a] == q)
-                hq = true;
-            else if (v[a] != p && no < 2)
-                o[no++] = v[a];
+    int n = 0;
+};
+
+// one pass over the unassigned tets at each corner i < 3 of tet t fills the
+// candidate lists of the edges (v[i], v[j]), j > i -- the same lists, in the
+// same order, as scanning adj[v[i]] once per edge
+template <class Assigned>
+void edge_candidates(int64_t t, const int32_t *conn4, const std::vector<int64_t> &off,
+                     const std::vector<int32_t> &adj, const Assigned &assigned, EdgeCands ec[6])
+{
+    static const int EIDX[3][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}};
+    const int32_t *v = conn4 + 4 * t;
+    for (int e = 0; e < 6; ++e)
+        ec[e].n = 0;
+    for (int i = 0; i < 3; ++i) {
+        const int32_t p = v[i];
+        for (int64_t k = off[p]; k < off[p + 1]; ++k) {
+            const int32_t s = adj[k];
+            if (assigned(s))
+                continue;
+            const int32_t *w = conn4 + 4 * (int64_t)s;
+            unsigned m = 0;  // which of v[j], j > i, tet s contains
+            for (int j = i + 1; j < 4; ++j)
+                m |= (unsigned)((w[0] == v[j]) | (w[1] == v[j]) | (w[2] == v[j]) | (w[3] == v[j])) << j;
+            while (m) {
+                const int j = __builtin_ctz(m);
+                m &= m - 1;
+                EdgeCands &E = ec[EIDX[i][j]];
+                if (E.n >= 64)
+                    continue;
+                const int32_t q = v[j];
+                int32_t o[2], no = 0;
+                for (int a = 0; a < 4; ++a)
+                    if (w[a] != q && w[a] != p && no < 2)
+                        o[no++] = w[a];
+                if (no == 2)
+                    E.cand[E.n++] = {s, o[0], o[1], s == (int32_t)t};
+            }
         }
-        if (hq && no == 2)
-            cand[nc++] = {s, o[0], o[1], s == t};
     }
+}
+
+// ring of unassigned tets around edge (p,q) that contains tet t, from the
+// edge's candidate list
+void ring_arc(int32_t t, int32_t p, int32_t q, const int32_t *conn4, const EdgeCands &E, Arc &arc)
+{
+    Cand cand[64];
+    const int nc = E.n;
+    std::copy(E.cand, E.cand + nc, cand);
     int it = -1;
     for (int i = 0; i < nc; ++i)
         if (cand[i].tet == t)
@@ -375,11 +526,19 @@ void ring_arc(int32_t t, int32_t p, int32_t q, const int32_t *conn4, const std::
                 arc.ring.push_back(v[a]);
         return;
     }
-    std::vector<int32_t> fwd{cand[it].d}, bwd{cand[it].c};
-    std::vector<int32_t> tf, tb;
+    // fixed-size walks (this runs 6x per patch: no heap traffic)
+    struct Seq {
+        int32_t v[PATCH_MAX_RING + 2];
+        int n = 0;
+        void push(int32_t x) { v[n++] = x; }
+        int32_t back() const { return v[n - 1]; }
+    };
+    Seq fwd, bwd, tf, tb;
+    fwd.push(cand[it].d);
+    bwd.push(cand[it].c);
     const int max_tets = PATCH_MAX_RING - 1;
-    auto walk = [&](std::vector<int32_t> &seq, std::vector<int32_t> &ts, int budget) {
-        while ((int)ts.size() < budget) {
+    auto walk = [&](Seq &seq, Seq &ts, const Seq &other, int budget) {
+        while (ts.n < budget) {
             const int32_t cur = seq.back();
             int found = -1;
             for (int i = 0; i < nc; ++i)
@@ -391,27 +550,27 @@ void ring_arc(int32_t t, int32_t p, int32_t q, const int32_t *conn4, const std::
                 return false;
             cand[found].used = true;
             const int32_t nxt = cand[found].c == cur ? cand[found].d : cand[found].c;
-            ts.push_back(cand[found].tet);
-            if (nxt == (&seq == &fwd ? bwd.front() : fwd.front()))
+            ts.push(cand[found].tet);
+            if (nxt == other.v[0])
                 return true;  // closed the ring
-            seq.push_back(nxt);
+            seq.push(nxt);
         }
         return false;
     };
-    const bool closed = walk(fwd, tf, max_tets - 1);
+    const bool closed = walk(fwd, tf, bwd, max_tets - 1);
     if (!closed)
-        walk(bwd, tb, max_tets - 1 - (int)tf.size());
+        walk(bwd, tb, fwd, max_tets - 1 - tf.n);
     arc.ring.clear();
-    for (auto i = bwd.rbegin(); i != bwd.rend(); ++i)
-        arc.ring.push_back(*i);
-    for (int32_t v : fwd)
-        arc.ring.push_back(v);
+    for (int i = bwd.n - 1; i >= 0; --i)
+        arc.ring.push_back(bwd.v[i]);
+    for (int i = 0; i < fwd.n; ++i)
+        arc.ring.push_back(fwd.v[i]);
     arc.tets.clear();
-    for (auto i = tb.rbegin(); i != tb.rend(); ++i)
-        arc.tets.push_back(*i);
+    for (int i = tb.n - 1; i >= 0; --i)
+        arc.tets.push_back(tb.v[i]);
     arc.tets.push_back(t);
-    for (int32_t s : tf)
-        arc.tets.push_back(s);
+    for (int i = 0; i < tf.n; ++i)
+        arc.tets.push_back(tf.v[i]);
     arc.closed = closed;
 }
 
@@ -434,6 +593,7 @@ void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int m
         return;
     }
     // node -> tets
+    Lap lap{"patches"};
     std::vector<int64_t> off((size_t)n_nodes + 1, 0);
     for (int64_t i = 0; i < 4 * n_elems; ++i)
         off[conn4[i] + 1]++;
@@ -446,42 +606,117 @@ void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int m
             for (int a = 0; a < 4; ++a)
                 adj[pos[conn4[4 * e + a]]++] = (int32_t)e;
     }
-    std::vector<uint8_t> assigned((size_t)n_elems, 0);
-    static const int EDGES[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-    Arc best, cur;
-    int32_t best_p = 0, best_q = 0;
-    for (int64_t t = 0; t < n_elems; ++t) {
-        if (assigned[t])
-            continue;
-        const int32_t *v = conn4 + 4 * t;
-        size_t best_n = 0;
-        int64_t best_span = 0;
-        for (auto &ed : EDGES) {
-            const int32_t p = v[ed[0]], q = v[ed[1]];
-            ring_arc((int32_t)t, p, q, conn4, off, adj, assigned, cur);
-            int64_t lo = cur.tets[0], hi = cur.tets[0];
-            for (int32_t s : cur.tets) {
-                lo = std::min<int64_t>(lo, s);
-                hi = std::max<int64_t>(hi, s);
-            }
-            const int64_t span = hi - lo;
-            if (cur.tets.size() > best_n || (cur.tets.size() == best_n && span < best_span)) {
-                best_n = cur.tets.size();
-                best_span = span;
-                std::swap(best, cur);
-                best_p = p;
-                best_q = q;
-            }
+    lap("adjacency");
+    // The greedy is sequential in tet order; it runs on contiguous blocks of
+    // the order in parallel, speculatively.  When the serial walk reaches a
+    // block's first tet, every earlier tet is assigned, so a block's outcome
+    // depends only on which of ITS OWN or later tets earlier blocks' patches
+    // took ("spill"): each block assumes none, records its own spills, and a
+    // serial fix-up re-runs every block whose actual inflow was not empty
+    // with that inflow -- the result is exactly the serial greedy's.
+    std::vector<uint8_t> shared((size_t)n_elems, 0);  // block k owns [b_k, e_k)
+    struct Block {
+        int64_t b = 0, e = 0;
+        std::vector<int32_t> ends, nodes, spill;  // patch end offsets (block-relative nodes)
+        std::vector<uint8_t> closed;
+    };
+    auto greedy = [&](Block &B, const std::vector<int32_t> &inflow) {
+        const int64_t b = B.b, e = B.e;
+        std::fill(shared.begin() + b, shared.begin() + e, 0);
+        std::vector<int32_t> ext;  // assigned tets >= e, sorted
+        for (int32_t x : inflow) {
+            if (x < e)
+                shared[x] = 1;
+            else
+                ext.push_back(x);
         }
-        for (int32_t s : best.tets)
-            assigned[s] = 1;
-        out.nodes.push_back(best_p);
-        out.nodes.push_back(best_q);
-        for (int32_t r : best.ring)
-            out.nodes.push_back(r);
-        out.off.push_back((int32_t)out.nodes.size());
-        out.closed.push_back(best.closed ? 1 : 0);
+        std::sort(ext.begin(), ext.end());
+        B.ends.clear(), B.nodes.clear(), B.spill.clear(), B.closed.clear();
+        auto assigned = [&](int64_t x) {
+            return x < b || (x < e ? shared[x] != 0 : std::binary_search(ext.begin(), ext.end(), (int32_t)x));
+        };
+        static const int EDGES[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+        Arc best, cur;
+        EdgeCands ec[6];
+        int32_t best_p = 0, best_q = 0;
+        for (int64_t t = b; t < e; ++t) {
+            if (assigned(t))
+                continue;
+            const int32_t *v = conn4 + 4 * t;
+            size_t best_n = 0;
+            int64_t best_span = 0;
+            edge_candidates(t, conn4, off, adj, assigned, ec);
+            for (int k = 0; k < 6; ++k) {
+                const auto &ed = EDGES[k];
+                const int32_t p = v[ed[0]], q = v[ed[1]];
+                ring_arc((int32_t)t, p, q, conn4, ec[k], cur);
+                int64_t lo = cur.tets[0], hi = cur.tets[0];
+                for (int32_t x : cur.tets) {
+                    lo = std::min<int64_t>(lo, x);
+                    hi = std::max<int64_t>(hi, x);
+                }
+                const int64_t span = hi - lo;
+                if (cur.tets.size() > best_n || (cur.tets.size() == best_n && span < best_span)) {
+                    best_n = cur.tets.size();
+                    best_span = span;
+                    std::swap(best, cur);
+                    best_p = p;
+                    best_q = q;
+                }
+            }
+            for (int32_t x : best.tets) {
+                if (x < e) {
+                    shared[x] = 1;
+                } else {
+                    ext.insert(std::lower_bound(ext.begin(), ext.end(), x), x);
+                    B.spill.push_back(x);
+                }
+            }
+            B.nodes.push_back(best_p);
+            B.nodes.push_back(best_q);
+            for (int32_t r : best.ring)
+                B.nodes.push_back(r);
+            B.ends.push_back((int32_t)B.nodes.size());
+            B.closed.push_back(best.closed ? 1 : 0);
+        }
+    };
+    const int K = (int)std::max<int64_t>(1, std::min<int64_t>(prep_threads(), n_elems / 4096));
+    std::vector<Block> blocks((size_t)K);
+    for (int k = 0; k < K; ++k)
+        blocks[k].b = n_elems * k / K, blocks[k].e = n_elems * (k + 1) / K;
+    const std::vector<int32_t> none;
+    parallel_items(K, [&](int64_t k, int) { greedy(blocks[k], none); }, 1);
+    lap("greedy (speculative)");
+    std::vector<int32_t> carry;  // tets >= b_k taken by the final patches of blocks < k
+    int reruns = 0;
+    for (int k = 0; k < K; ++k) {
+        std::vector<int32_t> inflow;
+        for (int32_t x : carry)
+            if (x >= blocks[k].b)
+                inflow.push_back(x);
+        if (!inflow.empty()) {
+            greedy(blocks[k], inflow);
+            ++reruns;
+        }
+        inflow.insert(inflow.end(), blocks[k].spill.begin(), blocks[k].spill.end());
+        carry.swap(inflow);
     }
+    if (Lap::on())
+        std::fprintf(stderr, "[tal prep]   patches: %d blocks, %d re-run\n", K, reruns);
+    size_t nn = 0, np = 0;
+    for (auto &B : blocks)
+        nn += B.nodes.size(), np += B.ends.size();
+    out.nodes.reserve(nn);
+    out.off.reserve(np + 1);
+    out.closed.reserve(np);
+    for (auto &B : blocks) {
+        const int32_t base = (int32_t)out.nodes.size();
+        out.nodes.insert(out.nodes.end(), B.nodes.begin(), B.nodes.end());
+        for (int32_t x : B.ends)
+            out.off.push_back(base + x);
+        out.closed.insert(out.closed.end(), B.closed.begin(), B.closed.end());
+    }
+    lap("fix-up + concat");
 }
 
 // ---------------------------------------------------------------------------
@@ -512,7 +747,7 @@ int bank_place_mode()
 }
 
 void bank_place(const Patches &P, int64_t p0, int64_t p1, std::vector<int32_t> &nodes,
-                std::vector<int32_t> &idx)
+                int32_t *idx, BankStats &stats)
 {
     const int nn = (int)nodes.size();
     for (int i = 0; i < nn; ++i)
@@ -637,9 +872,9 @@ void bank_place(const Patches &P, int64_t p0, int64_t p1, std::vector<int32_t> &
         if (!any)
             break;
     }
-    g_bank.groups += groups;
-    g_bank.wave_before += before;
-    g_bank.wave_after += waves();
+    stats.groups += groups;
+    stats.wave_before += before;
+    stats.wave_after += waves();
     // slot j = c + 8 r: class c's members in ascending node id
     std::vector<int32_t> out((size_t)nn);
     for (int c = 0; c < 8; ++c) {
@@ -684,9 +919,9 @@ int pos_place_mode()
     return mode;
 }
 
-void pos_place(const Patches &P, int64_t p0, int64_t p1, const std::vector<int32_t> &local,
+void pos_place(const Patches &P, int64_t p0, int64_t p1, const int32_t *local,
                const std::vector<int32_t> &ncnt, std::vector<int32_t> &order, std::vector<int32_t> &rank,
-               const uint16_t *lev, std::vector<int32_t> &lvl)
+               const uint16_t *lev, std::vector<int32_t> &lvl, BankStats &stats)
 {
     constexpr int NI = PATCH_MAX_RING + 3;  // loop stores, then ring end, a, b
     const int nn = (int)rank.size();
@@ -787,9 +1022,9 @@ void pos_place(const Patches &P, int64_t p0, int64_t p1, const std::vector<int32
             break;
     }
     const auto after = waves();
-    g_pos.groups += before.second;
-    g_pos.wave_before += before.first;
-    g_pos.wave_after += after.first;
+    stats.groups += before.second;
+    stats.wave_before += before.first;
+    stats.wave_after += after.first;
 }
 }  // namespace
 
@@ -813,21 +1048,101 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
     const int64_t np = P.n_patches();
     out.pids.assign((size_t)np * PATCH_SLOTS, 0);
     out.ppos.assign((size_t)np * PATCH_SLOTS, 0);
-    std::vector<int32_t> stamp((size_t)n_nodes, -1), local((size_t)n_nodes, 0), cnt((size_t)n_nodes, 0);
-    std::vector<int32_t> cnt_chunks((size_t)n_nodes, 0);
-    std::vector<int32_t> nodes, order, rank, fill, lvl, ncnt;
-    int32_t chunk = 0;
-    int64_t p_begin = 0, contrib = 0;
 
-    auto close_chunk = [&](int64_t p_end) {
-        std::vector<int32_t> sorted(nodes);
+    Lap lap{"chunks"};
+    // pass 1 (serial, cheap): greedy chunk boundaries in patch order
+    struct Span {
+        int64_t p0, p1;
+        int32_t nn, contrib;
+    };
+    std::vector<Span> spans;
+    {
+        std::vector<int32_t> stamp((size_t)n_nodes, -1), cnt((size_t)n_nodes, 0), nodes;
+        int32_t chunk = 0;
+        int64_t p_begin = 0, contrib = 0;
+        auto close = [&](int64_t p_end) {
+            spans.push_back({p_begin, p_end, (int32_t)nodes.size(), (int32_t)contrib});
+            for (int32_t v : nodes)
+                cnt[v] = 0;
+            nodes.clear();
+            ++chunk;
+            p_begin = p_end;
+            contrib = 0;
+        };
+        for (int64_t g = 0; g < np; ++g) {
+            const int32_t n = P.off[g + 1] - P.off[g];
+            if (n - 2 > PATCH_MAX_RING || n < 4) {
+                err = "patch ring size out of range";
+                return false;
+            }
+            int fresh = 0;
+            bool full_level = false;
+            for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
+                const int32_t v = P.nodes[k];
+                if (stamp[v] != chunk)
+                    ++fresh;
+                else if (cnt[v] + 1 > CHUNK_LEVELS)
+                    full_level = true;
+            }
+            if (g > p_begin && ((g - p_begin) + 1 > max_patches || (int64_t)nodes.size() + fresh > max_nodes ||
+                                contrib + n > max_contrib || full_level))
+                close(g);
+            for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
+                const int32_t v = P.nodes[k];
+                if (stamp[v] != chunk) {
+                    stamp[v] = chunk;
+                    nodes.push_back(v);
+                }
+                cnt[v]++;
+            }
+            contrib += n;
+        }
+        if (np > p_begin)
+            close(np);
+    }
+    lap("pass1");
+    const int64_t n_chunks = (int64_t)spans.size();
+    std::vector<int64_t> nbeg((size_t)n_chunks + 1, 0);
+    for (int64_t c = 0; c < n_chunks; ++c)
+        nbeg[c + 1] = nbeg[c] + spans[c].nn;
+    const int64_t total = nbeg[n_chunks];
+    out.chunks.resize((size_t)(5 * n_chunks));
+    out.gather_nodes.resize((size_t)total);
+    out.cnodes.resize((size_t)total);
+    out.runs.resize((size_t)total);
+    out.levels.resize((size_t)(CHUNK_LEVELS * n_chunks));
+
+    // pass 2 (parallel over chunks): slot placement, ranks, jagged levels,
+    // contribution positions -- each chunk's outputs are disjoint
+    struct Scratch {
+        std::vector<int32_t> local, cnt, nodes, order, rank, fill, lvl, ncnt;
+        BankStats bank, pos;
+    };
+    std::vector<Scratch> scr((size_t)prep_threads());
+    parallel_items(n_chunks, [&](int64_t c, int t) {
+        Scratch &S = scr[(size_t)t];
+        if (S.local.empty()) {  // node-indexed scratch: written before read, cnt reset after use
+            S.local.resize((size_t)std::max<int64_t>(n_nodes, 1));
+            S.cnt.assign((size_t)std::max<int64_t>(n_nodes, 1), 0);
+        }
+        int32_t *local = S.local.data(), *cnt = S.cnt.data();
+        const int64_t p_begin = spans[c].p0, p_end = spans[c].p1;
+        std::vector<int32_t> &sorted = S.nodes;
+        sorted.clear();
+        for (int64_t g = p_begin; g < p_end; ++g)
+            for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
+                const int32_t v = P.nodes[k];
+                if (cnt[v]++ == 0)
+                    sorted.push_back(v);
+            }
         std::sort(sorted.begin(), sorted.end());  // local ids: ascending node id (gather order)
         if (bank_place_mode())                    // or bank-aware slots (above)
-            bank_place(P, p_begin, p_end, sorted, local);
+            bank_place(P, p_begin, p_end, sorted, local, S.bank);
         const int32_t nn = (int32_t)sorted.size();
         for (int32_t j = 0; j < nn; ++j)
             local[sorted[j]] = j;
         // rank: by contribution count descending, then local id
+        std::vector<int32_t> &order = S.order, &rank = S.rank;
         order.resize(nn);
         for (int32_t j = 0; j < nn; ++j)
             order[j] = j;
@@ -836,7 +1151,8 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
         rank.assign(nn, 0);
         for (int32_t q = 0; q < nn; ++q)
             rank[order[q]] = q;
-        uint16_t lev[CHUNK_LEVELS] = {0};
+        uint16_t *lev = out.levels.data() + (size_t)CHUNK_LEVELS * c;
+        lev[0] = 0;
         for (int s = 1; s < CHUNK_LEVELS; ++s) {
             int32_t alive = 0;  // nodes with more than s-1 contributions
             for (int32_t q = 0; q < nn; ++q)
@@ -844,29 +1160,27 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
             lev[s] = (uint16_t)(lev[s - 1] + alive);
         }
         // levels of the patch-order contributions (fill order), then the
-        // bank-aware choice of levels / equal-count ranks (above)
+        // bank-aware choice of levels (above)
+        std::vector<int32_t> &fill = S.fill, &lvl = S.lvl;
         fill.assign(nn, 0);
         lvl.clear();
         for (int64_t g = p_begin; g < p_end; ++g)
             for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k)
                 lvl.push_back(fill[local[P.nodes[k]]]++);
         if (pos_place_mode()) {
-            ncnt.resize(nn);
+            S.ncnt.resize(nn);
             for (int32_t j = 0; j < nn; ++j)
-                ncnt[j] = cnt[sorted[j]];
-            pos_place(P, p_begin, p_end, local, ncnt, order, rank, lev, lvl);
+                S.ncnt[j] = cnt[sorted[j]];
+            pos_place(P, p_begin, p_end, local, S.ncnt, order, rank, lev, lvl, S.pos);
         }
-        const size_t node_begin = out.cnodes.size();
+        const int64_t node_begin = nbeg[c];
         for (int32_t j = 0; j < nn; ++j)
-            out.gather_nodes.push_back(sorted[j]);
+            out.gather_nodes[node_begin + j] = sorted[j];
         for (int32_t q = 0; q < nn; ++q) {
             const int32_t v = sorted[order[q]];
-            out.cnodes.push_back(v);
-            out.runs.push_back((uint8_t)cnt[v]);
-            cnt_chunks[v]++;
+            out.cnodes[node_begin + q] = v;
+            out.runs[node_begin + q] = (uint8_t)cnt[v];
         }
-        for (int s = 0; s < CHUNK_LEVELS; ++s)
-            out.levels.push_back(lev[s]);
         size_t ci = 0;  // contribution index in patch order (lvl)
         for (int64_t g = p_begin; g < p_end; ++g) {
             uint16_t *ids = out.pids.data() + PATCH_SLOTS * g, *pos = out.ppos.data() + PATCH_SLOTS * g;
@@ -880,50 +1194,25 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
         }
         for (int32_t v : sorted)
             cnt[v] = 0;
-        out.chunks.push_back((int32_t)p_begin);
-        out.chunks.push_back((int32_t)(p_end - p_begin));
-        out.chunks.push_back((int32_t)node_begin);
-        out.chunks.push_back(nn);
-        out.chunks.push_back((int32_t)contrib);
-        nodes.clear();
-        ++chunk;
-        p_begin = p_end;
-        contrib = 0;
-    };
-
-    for (int64_t g = 0; g < np; ++g) {
-        const int32_t n = P.off[g + 1] - P.off[g];
-        if (n - 2 > PATCH_MAX_RING || n < 4) {
-            err = "patch ring size out of range";
-            return false;
-        }
-        int fresh = 0;
-        bool full_level = false;
-        for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
-            const int32_t v = P.nodes[k];
-            if (stamp[v] != chunk)
-                ++fresh;
-            else if (cnt[v] + 1 > CHUNK_LEVELS)
-                full_level = true;
-        }
-        if (g > p_begin && ((g - p_begin) + 1 > max_patches || (int64_t)nodes.size() + fresh > max_nodes ||
-                            contrib + n > max_contrib || full_level))
-            close_chunk(g);
-        for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
-            const int32_t v = P.nodes[k];
-            if (stamp[v] != chunk) {
-                stamp[v] = chunk;
-                nodes.push_back(v);
-            }
-            cnt[v]++;
-        }
-        contrib += n;
+        int32_t *ch = out.chunks.data() + 5 * c;
+        ch[0] = (int32_t)p_begin;
+        ch[1] = (int32_t)(p_end - p_begin);
+        ch[2] = (int32_t)node_begin;
+        ch[3] = nn;
+        ch[4] = spans[c].contrib;
+    }, 4);
+    for (auto &S : scr) {  // integer sums: the serial totals
+        g_bank.groups += S.bank.groups, g_bank.wave_before += S.bank.wave_before;
+        g_bank.wave_after += S.bank.wave_after;
+        g_pos.groups += S.pos.groups, g_pos.wave_before += S.pos.wave_before;
+        g_pos.wave_after += S.pos.wave_after;
     }
-    if (np > p_begin)
-        close_chunk(np);
 
+    lap("pass2");
     // interior flag + shared/isolated node lists for the ordered merge
-    const int64_t total = (int64_t)out.cnodes.size();
+    std::vector<int32_t> cnt_chunks((size_t)n_nodes, 0);
+    for (int32_t v : out.cnodes)
+        cnt_chunks[v]++;
     auto interior = [&](int64_t v) { return cnt_chunks[v] == 1 && !(external && external[v]); };
     for (int64_t q = 0; q < total; ++q) {
         const int32_t v = out.cnodes[q];
@@ -950,6 +1239,7 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
             continue;
         out.bnd_pos[bfill[bidx[raw]]++] = (int32_t)q;
     }
+    lap("tail");
     return true;
 }
 
@@ -967,7 +1257,7 @@ void pack_blobs(const Chunking &ch, int T, std::vector<uint8_t> &blobs, std::vec
         blob_off[c + 1] = (int32_t)(total / 16);
     }
     blobs.assign((size_t)total, 0);
-    for (int64_t c = 0; c < n_chunks; ++c) {
+    parallel_items(n_chunks, [&](int64_t c, int) {
         const int32_t p0 = ch.chunks[5 * c], npch = ch.chunks[5 * c + 1];
         const int32_t n0 = ch.chunks[5 * c + 2], nn = ch.chunks[5 * c + 3];
         uint8_t *b = blobs.data() + (int64_t)blob_off[c] * 16;
@@ -988,7 +1278,7 @@ void pack_blobs(const Chunking &ch, int T, std::vector<uint8_t> &blobs, std::vec
         std::memcpy(q, ch.cnodes.data() + n0, 4 * (size_t)nn);
         q += pad(4 * nn);
         std::memcpy(q, ch.runs.data() + n0, (size_t)nn);
-    }
+    }, 64);
 }
 
 }  // namespace tal

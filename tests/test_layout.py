@@ -159,3 +159,27 @@ def test_shared_tail_numbering(layout):
     assert interior == list(range(len(interior)))  # contiguous, in chunk / slot order
     assert min(shared) >= len(interior)
     assert len(interior) + len(shared) == mesh.n_nodes  # no isolated nodes in a box
+
+
+def test_parallel_prep_reproduces_serial_layouts():
+    """The multithreaded host preprocessing (tal_par.hpp: parallel RCM
+    neighbour lists, parallel Morton sort, speculative block-parallel patch
+    greedy with serial fix-up, per-chunk parallel placement) yields the
+    serial code's layouts bit for bit: SHA-256 of blobs / offsets / node
+    permutation over 29 (mesh x option) cases, recorded by the serial
+    round-1 code (tools/layout_digest.py)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root / "tools"))
+    import layout_digest as LD
+    want = json.loads((root / "tests" / "golden" / "layout_digests.json").read_text())
+    got = LD.compute()
+    assert got == want
+    # and independent of the thread count
+    env = {**__import__("os").environ, "TAL_PREP_THREADS": "3"}
+    r = subprocess.run([sys.executable, str(root / "tools" / "layout_digest.py")], env=env,
+                       capture_output=True, text=True, check=True)
+    assert "mismatch: none" in r.stdout

@@ -64,6 +64,10 @@ for r in rows[2:]:
         "shared_wavefronts": f("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
         "shared_bank_conflicts": f("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
         "l2_hit_pct": f("lts__t_sector_hit_rate.pct"),
+        "l2_sectors": f("lts__t_sectors.sum"),
+        "l2_throughput_pct": f("lts__t_sectors.avg.pct_of_peak_sustained_elapsed"),
+        "dram_throughput_pct": f("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+        "l1_hit_pct": f("l1tex__t_sector_hit_rate.pct"),
         "red_sectors": f("l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum"),
         "stalls_per_issue": dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:10]),
     }
