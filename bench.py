@@ -600,6 +600,36 @@ def run_ours(a) -> None:
                       + " (pinned), wall clock, max over ranks"}
         for p_ in pu + pr:
             p_.free()
+    # the numba seam swapped inside the reference's OWN driver:
+    # tet_assembly_lab.variants.assemble_rsp with _rsp_kernels.assemble_elements
+    # -> paper_2403_08777_b200.assemble_elements (tal_seam_*), timed by the
+    # reference's own wall_time (variants.py:572, :616); one-thread driver (one
+    # call with ids = all elements) and the threaded private driver (one call
+    # per vector_dim-aligned slab, numpy merge of the per-thread buffers)
+    seam = None
+    R = import_reference() if (dom is None and a.variant == "rsp" and not a.no_e2e
+                               and a.scatter in ("private", "private-atomic")) else None
+    if R is not None:
+        ref, variants, _ = R
+        from tet_assembly_lab import _rsp_kernels
+        orig = _rsp_kernels.assemble_elements
+        _rsp_kernels.assemble_elements = tb.assemble_elements
+        try:
+            seam = {"unit": "elem/s", "api": "reference variants.assemble_rsp (scatter='private') with "
+                    "_rsp_kernels.assemble_elements swapped for paper_2403_08777_b200.assemble_elements; "
+                    "the reference's own wall_time, median of 5 after 2 warm-ups",
+                    "h2d_bytes_per_step": 24 * Nn, "d2h_bytes_per_step": 24 * Nn}
+            for T in (1, host_threads()):
+                cfgr = variants.RunConfig(n_threads=T, scatter="private")
+                for _ in range(2):
+                    variants.assemble_rsp(mesh, u, ref.PhysParams(), cfgr)
+                ws_ = [variants.assemble_rsp(mesh, u, ref.PhysParams(), cfgr).wall_time for _ in range(5)]
+                seam[f"threads_{T}"] = {"value": E / statistics.median(ws_),
+                                        "ms_per_step": 1e3 * statistics.median(ws_)}
+            seam["value"] = seam["threads_1"]["value"]
+        finally:
+            _rsp_kernels.assemble_elements = orig
+            tb.clear_cache()
     # parity + CPU baseline (rank 0, N=1): the oracle as checker / baseline only.
     # Runs after the e2e leg, so its 16-thread host load cannot disturb it.
     if ws == 1 and not a.no_cpu_baseline:
@@ -699,6 +729,7 @@ def run_ours(a) -> None:
                              "alg_bytes_per_launch": alg_bytes, "peak_source": hbm_src}},
         "e2e": e2e,
         "device_caller_layout": caller_layout,
+        "seam_in_reference_driver": seam,
         "cpu_baseline": cpu_baseline,
         "parity": parity,
         "gpu_launches": launches,

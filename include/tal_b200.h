@@ -233,8 +233,11 @@ int tal_synchronize(tal_handle *h, void *stream);
 
 /* Element-subset seam, signature-for-signature the numba kernel
  * _rsp_kernels.assemble_elements (_rsp_kernels.py:20-21): assembles elements
- * ids[0..k) and ADDS (+=) into the host rhs, as the numba loop does.  Runs
- * on 'device' with a transient upload (no renumbering). */
+ * ids[0..k) and ADDS (+=) into the host rhs, as the numba loop does.  The
+ * mesh stays resident between calls in a small internal cache keyed by the
+ * arrays' addresses, sizes and a content hash (a changed array is
+ * re-uploaded, never served stale); ids = the whole mesh runs the edge-star
+ * kernel, any other subset the per-element kernel. */
 int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
                           int64_t n_nodes, int64_t n_elems, const double *u,
                           double rho, double mu, double cvre,
@@ -251,6 +254,17 @@ int tal_assemble_elements_strict(int device, const double *coords, const int64_t
                                  double rho, double mu, double cvre,
                                  const double *pmat, const int64_t *ids, int64_t k,
                                  double *rhs);
+
+/* The same seam with an explicit per-mesh context (no per-call content
+ * hash): open once per (coords, conn), call tal_seam_assemble with the numba
+ * kernel's remaining arguments, close.  Calls on one context are serialised
+ * (thread-safe); u and rhs are caller-order (N,3) host arrays, rhs += result. */
+typedef struct tal_seam tal_seam;
+int tal_seam_open(int device, const double *coords, const int64_t *conn, int64_t n_nodes,
+                  int64_t n_elems, tal_seam **out);
+int tal_seam_assemble(tal_seam *ctx, const double *u, double rho, double mu, double cvre,
+                      const double *pmat, const int64_t *ids, int64_t k, double *rhs);
+int tal_seam_close(tal_seam *ctx);
 
 /* ---- multi-GPU interface (domain decomposition) ----------------------------- */
 /* Gather rhs of internal node ids list[0..n) into a packed buffer d_out

@@ -103,6 +103,9 @@ SIGNATURES = [
     ("tal_synchronize", _I, [_P, _P]),
     ("tal_assemble_elements", _I, [_I, _P, _P, _I64, _I64, _P, _D, _D, _D, _P, _P, _I64, _P]),
     ("tal_assemble_elements_strict", _I, [_I, _P, _P, _I64, _I64, _P, _D, _D, _D, _P, _P, _I64, _P]),
+    ("tal_seam_open", _I, [_I, _P, _P, _I64, _I64, ctypes.POINTER(_P)]),
+    ("tal_seam_assemble", _I, [_P, _P, _D, _D, _D, _P, _P, _I64, _P]),
+    ("tal_seam_close", _I, [_P]),
     ("tal_halo_pack", _I, [_P, _P, _I64, _P, _P]),
     ("tal_halo_accumulate", _I, [_P, _P, _I64, _P, _P]),
     ("tal_map_nodes", _I, [_P, _P, _I64, _P]),

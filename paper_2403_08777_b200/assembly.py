@@ -591,6 +591,9 @@ def clear_cache() -> None:
     while _CACHE:
         _, (asm, *_) = _CACHE.popitem()
         asm.close()
+    while _SEAMS:
+        _, (seam, *_) = _SEAMS.popitem()
+        seam.close()
 
 
 def _assemble_variant(variant: VariantId, mesh, u, params: PhysParams,
@@ -654,13 +657,79 @@ def assemble(variant: VariantId, mesh, u, params, cfg=None) -> AssemblyResult:
     return ASSEMBLERS[variant](mesh, u, params, cfg)
 
 
+class _Seam:
+    """A tal_seam context (resident mesh + pinned staging) for one (coords, conn)."""
+
+    def __init__(self, coords, conn, device):
+        h = ctypes.c_void_p()
+        N.check(N.lib().tal_seam_open(device, N.ptr(coords), N.ptr(conn), coords.shape[0],
+                                      conn.shape[0], ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            N.lib().tal_seam_close(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_SEAMS: "OrderedDict[tuple, tuple]" = OrderedDict()
+
+
+def _seam_for(coords, conn, device) -> "_Seam":
+    """Seam context cache with the resident-mesh cache's rules (_cached_assembler)."""
+    key = (id(coords), id(conn), coords.shape, conn.shape, device)
+    hit = _SEAMS.get(key)
+    if hit is not None:
+        seam, held, snaps = hit
+        if all(s is None or np.array_equal(a, s) for a, s in zip(held, snaps)):
+            _SEAMS.move_to_end(key)
+            return seam
+        del _SEAMS[key]
+        seam.close()
+    seam = _Seam(coords, conn, device)
+    snaps = tuple(None if _frozen(a) else np.array(a, copy=True) for a in (coords, conn))
+    _SEAMS[key] = (seam, (coords, conn), snaps)
+    while len(_SEAMS) > 2:
+        _, (old, *_) = _SEAMS.popitem(last=False)
+        old.close()
+    return seam
+
+
 def assemble_elements(coords, conn, u, rho, mu, cvre, pmat, ids, rhs, device: int = 0,
                       strict: bool = False) -> None:
     """The numba seam ``_rsp_kernels.assemble_elements`` on the GPU: assemble
     elements ``ids`` and ADD into ``rhs`` (in place, like the numba loop).
+
+    Fast path (``tal_seam_*``): the mesh stays resident per (coords, conn)
+    between calls -- the reference's drivers call the seam once per assembly
+    (one thread, ``ids`` = all elements: the edge-star kernel) or once per
+    thread slab (a contiguous ``ids`` range: the per-element kernel).
     ``strict=True`` (``tal_assemble_elements_strict``) is bitwise the numba
     loop: each node continues from its incoming ``rhs`` through its elements in
     ``ids`` order with the reference's operation order (tal_strict.cuh)."""
+    if not strict and isinstance(coords, np.ndarray) and isinstance(conn, np.ndarray) \
+            and coords.dtype == np.float64 and conn.dtype == np.int64 \
+            and coords.flags.c_contiguous and conn.flags.c_contiguous \
+            and coords.ndim == 2 and coords.shape[1:] == (3,) and conn.ndim == 2 and conn.shape[1:] == (4,):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        pm = np.ascontiguousarray(pmat, dtype=np.float64)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        if not (isinstance(rhs, np.ndarray) and rhs.flags.c_contiguous and rhs.dtype == np.float64):
+            raise ValueError("rhs must be a C-contiguous float64 array (accumulated in place)")
+        if u.shape != coords.shape or rhs.shape != coords.shape or pm.shape != (4, 4):
+            raise ValueError("bad array shapes")
+        if coords.shape[0] == 0 or ids.shape[0] == 0:
+            return
+        seam = _seam_for(coords, conn, device)
+        N.check(N.lib().tal_seam_assemble(seam.h, N.ptr(u), float(rho), float(mu), float(cvre),
+                                          N.ptr(pm), N.ptr(ids), ids.shape[0], N.ptr(rhs)))
+        return
     coords = np.ascontiguousarray(coords, dtype=np.float64)
     conn = np.ascontiguousarray(conn, dtype=np.int64)
     u = np.ascontiguousarray(u, dtype=np.float64)

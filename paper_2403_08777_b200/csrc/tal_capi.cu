@@ -18,6 +18,9 @@
 #include "../../include/tal_b200.h"
 #include "tal_kernels.cuh"
 #include "tal_strict.cuh"
+#include <mutex>
+#include <memory>
+#include <atomic>
 #include "tal_prep.hpp"
 #include "tal_par.hpp"
 #include "tal_shapes.cuh"
@@ -1656,14 +1659,13 @@ int tal_assemble_variant(tal_handle *h, const double *u, const tal_params *p, do
 }
 
 namespace {
-// the numba seam (_rsp_kernels.py:20-164): elements ids[0..k) ADDED into rhs.
-// strict=false: one thread per element, FP64 REDs into a zeroed buffer, added
-// to rhs on the host (parity to tolerance).  strict=true: tal_strict.cuh --
-// each node continues from its incoming rhs value through its elements in
-// ids order with the reference's operation order: bitwise the numba loop.
+// the strict numba seam (_rsp_kernels.py:20-164), tal_strict.cuh: each node
+// continues from its incoming rhs value through its elements in ids order
+// with the reference's operation order -- bitwise the numba loop.  Transient
+// upload (a parity/debug path; the fast seam is tal_seam_* below).
 int seam_impl(int device, const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
               const double *u, double rho, double mu, double cvre, const double *pmat, const int64_t *ids,
-              int64_t k, double *rhs, bool strict)
+              int64_t k, double *rhs)
 {
     if (n_nodes < 0 || n_elems < 0 || k < 0)
         return fail(TAL_EINVAL, "negative sizes");
@@ -1712,7 +1714,7 @@ int seam_impl(int device, const double *coords, const int64_t *conn, int64_t n_n
     std::vector<double> rin, dlt;
     std::vector<int64_t> off;
     std::vector<int32_t> ent;
-    if (strict) {
+    {
         if (4 * k > INT32_MAX)
             return fail(TAL_EINVAL, "strict seam supports up to 2^29 element ids per call");
         rin.resize((size_t)(3 * n_nodes));
@@ -1744,14 +1746,13 @@ int seam_impl(int device, const double *coords, const int64_t *conn, int64_t n_n
         if ((e = cudaMalloc((void **)&dconn, sizeof(int4) * k)) != cudaSuccess ||
             (e = cudaMemcpy(buf, soa.data(), sizeof(double) * 6 * n_nodes, cudaMemcpyHostToDevice)) !=
                 cudaSuccess ||
-            (e = strict ? cudaMemcpy(buf + 6 * n_nodes, rin.data(), sizeof(double) * 3 * n_nodes,
-                                     cudaMemcpyHostToDevice)
-                        : cudaMemset(buf + 6 * n_nodes, 0, sizeof(double) * 3 * n_nodes)) != cudaSuccess ||
+            (e = cudaMemcpy(buf + 6 * n_nodes, rin.data(), sizeof(double) * 3 * n_nodes,
+                            cudaMemcpyHostToDevice)) != cudaSuccess ||
             (e = cudaMemcpy(dconn, sub.data(), sizeof(int4) * k, cudaMemcpyHostToDevice)) != cudaSuccess) {
             rc = fail(TAL_ECUDA, std::string("assemble_elements upload: ") + cudaGetErrorString(e));
             break;
         }
-        if (strict && ((e = cudaMalloc((void **)&doff, sizeof(int64_t) * off.size())) != cudaSuccess ||
+        if (((e = cudaMalloc((void **)&doff, sizeof(int64_t) * off.size())) != cudaSuccess ||
                        (e = cudaMalloc((void **)&dent, sizeof(int32_t) * ent.size())) != cudaSuccess ||
                        (e = cudaMalloc((void **)&ddlt, sizeof(double) * dlt.size())) != cudaSuccess ||
                        (e = cudaMemcpy(doff, off.data(), sizeof(int64_t) * off.size(),
@@ -1765,13 +1766,8 @@ int seam_impl(int device, const double *coords, const int64_t *conn, int64_t n_n
         }
         const double *nodes = buf;
         RhsSoA r{buf + 6 * n_nodes, buf + 7 * n_nodes, buf + 8 * n_nodes};
-        if (strict)
-            k_assemble_sequential<<<grid_for(n_nodes, 128), 128>>>(doff, dent, n_nodes, dconn, nodes, ddlt,
-                                                                   r.rx, r.ry, r.rz, kc, true);
-        else if (sym)
-            k_assemble_atomic<true><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc, nullptr);
-        else
-            k_assemble_atomic<false><<<grid_for(k, 256), 256>>>(dconn, 0, k, nodes, r, kc, nullptr);
+        k_assemble_sequential<<<grid_for(n_nodes, 128), 128>>>(doff, dent, n_nodes, dconn, nodes, ddlt,
+                                                               r.rx, r.ry, r.rz, kc, true);
         if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
             rc = fail(TAL_ECUDA, std::string("assemble_elements kernel: ") + cudaGetErrorString(e));
             break;
@@ -1782,12 +1778,8 @@ int seam_impl(int device, const double *coords, const int64_t *conn, int64_t n_n
             break;
         }
         for (int64_t i = 0; i < n_nodes; ++i)
-            for (int c = 0; c < 3; ++c) {
-                if (strict)
-                    rhs[3 * i + c] = soa[c * n_nodes + i];  // accumulated on the device
-                else
-                    rhs[3 * i + c] += soa[c * n_nodes + i];
-            }
+            for (int c = 0; c < 3; ++c)
+                rhs[3 * i + c] = soa[c * n_nodes + i];  // accumulated on the device
     } while (0);
     void *tmp[] = {buf, dconn, doff, dent, ddlt};
     for (void *q : tmp)
@@ -1797,12 +1789,288 @@ int seam_impl(int device, const double *coords, const int64_t *conn, int64_t n_n
 }
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// The fast numba seam: a per-mesh context (resident mesh + caller-order
+// connectivity on the device, pinned staging) so a call costs the velocity
+// H2D, one kernel and the RHS D2H.  'ids' = the whole mesh in order (the
+// reference's one-thread driver, variants.py:573-576): the private edge-star
+// kernel; a contiguous range (its threaded slabs, :578-596): the per-element
+// kernel over that conn range; any other list: the per-element kernel over an
+// uploaded id list.  Calls on one context are serialised (the reference
+// calls the seam from a thread pool).
+// ---------------------------------------------------------------------------
+struct tal_seam {
+    tal_handle *h = nullptr;
+    int4 *conn_caller = nullptr;  // caller element order, internal node ids
+    int32_t *d_ids = nullptr;
+    int64_t ids_cap = 0;
+    double *pin_u = nullptr, *pin_r = nullptr;
+    int64_t N = 0, E = 0;
+    std::mutex mu;
+};
+
+namespace {
+void seam_free(tal_seam *c)
+{
+    if (!c)
+        return;
+    if (c->h) {
+        DeviceGuard g(c->h->device);
+        if (c->conn_caller)
+            cudaFree(c->conn_caller);
+        if (c->d_ids)
+            cudaFree(c->d_ids);
+        if (c->pin_u)
+            cudaFreeHost(c->pin_u);
+        if (c->pin_r)
+            cudaFreeHost(c->pin_r);
+        tal_destroy(c->h);
+    }
+    delete c;
+}
+
+int seam_open_impl(int device, const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
+                   tal_seam **out)
+{
+    *out = nullptr;
+    if (n_nodes < 0 || n_elems < 0 || (n_nodes && !coords) || (n_elems && !conn))
+        return fail(TAL_EINVAL, "bad mesh arguments");
+    std::unique_ptr<tal_seam, void (*)(tal_seam *)> c(new tal_seam(), seam_free);
+    c->N = n_nodes, c->E = n_elems;
+    if (int rc = tal_create(device, &c->h))
+        return rc;
+    tal_mesh_opts o;
+    tal_default_mesh_opts(&o);
+    o.validate = 0;  // the numba seam takes any mesh (no orientation check)
+    if (int rc = tal_upload_mesh_ex(c->h, coords, conn, n_nodes, n_elems, nullptr, &o, nullptr, 0))
+        return rc;
+    DeviceGuard g(device);
+    const size_t nb = sizeof(double) * 3 * (size_t)std::max<int64_t>(n_nodes, 1);
+    TAL_CK(cudaMallocHost((void **)&c->pin_u, nb));
+    TAL_CK(cudaMallocHost((void **)&c->pin_r, nb));
+    if (n_elems) {
+        std::vector<int4> cc((size_t)n_elems);
+        parallel_for(n_elems, [&](int64_t e0, int64_t e1, int) {
+            for (int64_t e = e0; e < e1; ++e)
+                cc[e] = make_int4((int)conn[4 * e], (int)conn[4 * e + 1], (int)conn[4 * e + 2],
+                                  (int)conn[4 * e + 3]);
+        });
+        TAL_CK(cudaMalloc((void **)&c->conn_caller, sizeof(int4) * n_elems));
+        TAL_CK(cudaMemcpy(c->conn_caller, cc.data(), sizeof(int4) * n_elems, cudaMemcpyHostToDevice));
+        if (c->h->iperm) {
+            k_remap_conn<<<grid_for(n_elems, 256), 256, 0, c->h->stream>>>(c->conn_caller, n_elems, c->h->iperm);
+            TAL_CK_LAUNCH();
+            TAL_CK(cudaStreamSynchronize(c->h->stream));
+        }
+    }
+    *out = c.release();
+    return TAL_OK;
+}
+
+int seam_assemble_impl(tal_seam *c, const double *u, double rho, double mu, double cvre, const double *pmat,
+                       const int64_t *ids, int64_t k, double *rhs)
+{
+    if (!c || !c->h)
+        return fail(TAL_EINVAL, "seam context is NULL");
+    if (k < 0)
+        return fail(TAL_EINVAL, "negative sizes");
+    if (k == 0 || c->N == 0)
+        return TAL_OK;
+    if (!u || !pmat || !ids || !rhs)
+        return fail(TAL_EINVAL, "NULL arrays");
+    const int64_t E = c->E, a0 = ids[0];
+    std::atomic<bool> bad{false}, seq{true};
+    parallel_for(k, [&](int64_t t0, int64_t t1, int) {
+        for (int64_t t = t0; t < t1; ++t) {
+            if (ids[t] < 0 || ids[t] >= E) {
+                bad = true;
+                return;
+            }
+            if (ids[t] != a0 + t)
+                seq = false;
+        }
+    });
+    if (bad)
+        return fail(TAL_EINVAL, "element id out of range");
+    tal_params p;
+    p.rho = rho, p.mu = mu, p.c_vreman = cvre;
+    std::memcpy(p.pmat, pmat, sizeof p.pmat);
+    if (int rc = check_params(&p))
+        return rc;
+    ElemConsts kc;
+    bool sym;
+    make_consts(&p, kc, sym);
+    std::lock_guard<std::mutex> lk(c->mu);
+    tal_handle *h = c->h;
+    DeviceGuard g(h->device);
+    cudaStream_t s = h->stream;
+    const int64_t n3 = 3 * c->N;
+    parallel_for(n3, [&](int64_t i0, int64_t i1, int) { std::memcpy(c->pin_u + i0, u + i0, sizeof(double) * (i1 - i0)); });
+    if (int rc = tal_set_velocity_host(h, c->pin_u, s))
+        return rc;
+    int64_t nl = 0;
+    if (seq && a0 == 0 && k == E) {  // the whole mesh: the resident edge-star kernel
+        if (int rc = launch_run(h, &p, TAL_SCATTER_PRIVATE_ATOMIC, s, &nl))
+            return rc;
+    } else {
+        TAL_CK(zero_rhs(h, s));
+        RhsSoA r{h->RX(), h->RY(), h->RZ()};
+        if (seq) {
+            if (sym)
+                k_assemble_atomic<true><<<grid_for(k, 256), 256, 0, s>>>(c->conn_caller, a0, a0 + k, h->REC(), r, kc, nullptr);
+            else
+                k_assemble_atomic<false><<<grid_for(k, 256), 256, 0, s>>>(c->conn_caller, a0, a0 + k, h->REC(), r, kc, nullptr);
+        } else {
+            if (k > c->ids_cap) {
+                if (c->d_ids)
+                    cudaFree(c->d_ids);
+                c->d_ids = nullptr;
+                c->ids_cap = 0;
+                TAL_CK(cudaMalloc((void **)&c->d_ids, sizeof(int32_t) * k));
+                c->ids_cap = k;
+            }
+            std::vector<int32_t> i32((size_t)k);
+            parallel_for(k, [&](int64_t t0, int64_t t1, int) {
+                for (int64_t t = t0; t < t1; ++t)
+                    i32[t] = (int32_t)ids[t];
+            });
+            TAL_CK(cudaMemcpyAsync(c->d_ids, i32.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
+            if (sym)
+                k_assemble_atomic_ids<true><<<grid_for(k, 256), 256, 0, s>>>(c->conn_caller, c->d_ids, k, h->REC(), r, kc);
+            else
+                k_assemble_atomic_ids<false><<<grid_for(k, 256), 256, 0, s>>>(c->conn_caller, c->d_ids, k, h->REC(), r, kc);
+        }
+        TAL_CK_LAUNCH();
+    }
+    if (int rc = tal_get_rhs_host(h, c->pin_r, s))  // blocking
+        return rc;
+    parallel_for(n3, [&](int64_t i0, int64_t i1, int) {
+        for (int64_t i = i0; i < i1; ++i)
+            rhs[i] += c->pin_r[i];
+    });
+    return TAL_OK;
+}
+
+// stateless entry: a small cache of contexts keyed by the mesh arrays'
+// addresses, sizes and a content hash (parallel, order-fixed 64-bit mix), so
+// repeated calls on one mesh reuse the device copy and a changed array is
+// never served stale
+uint64_t content_hash(const void *p, size_t bytes)
+{
+    const size_t B = 1 << 16, nb = (bytes + B - 1) / B;
+    std::vector<uint64_t> hb(nb);
+    parallel_items((int64_t)nb, [&](int64_t b, int) {
+        const uint8_t *q = (const uint8_t *)p + b * B;
+        const size_t n = std::min(B, bytes - b * B);
+        uint64_t x = 0x9e3779b97f4a7c15ull ^ (uint64_t)b;
+        size_t i = 0;
+        for (; i + 8 <= n; i += 8) {
+            uint64_t w;
+            std::memcpy(&w, q + i, 8);
+            x = (x ^ w) * 0xff51afd7ed558ccdull;
+            x ^= x >> 29;
+        }
+        for (; i < n; ++i)
+            x = (x ^ q[i]) * 0xc4ceb9fe1a85ec53ull;
+        hb[b] = x;
+    }, 16);
+    uint64_t h = bytes;
+    for (uint64_t x : hb)
+        h = (h ^ x) * 0x100000001b3ull + 0x9e3779b97f4a7c15ull;
+    return h;
+}
+
+struct SeamKey {
+    int device;
+    const void *coords, *conn;
+    int64_t N, E;
+    uint64_t hash;
+    bool operator==(const SeamKey &o) const
+    {
+        return device == o.device && coords == o.coords && conn == o.conn && N == o.N && E == o.E &&
+               hash == o.hash;
+    }
+};
+std::mutex g_seam_mu;
+std::vector<std::pair<SeamKey, tal_seam *>> g_seams;  // most recent last, at most 2
+}  // namespace
+
+int tal_seam_open(int device, const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
+                  tal_seam **out)
+{
+    TAL_GUARD_BEGIN
+    if (!out)
+        return fail(TAL_EINVAL, "out is NULL");
+    return seam_open_impl(device, coords, conn, n_nodes, n_elems, out);
+    TAL_GUARD_END
+}
+
+int tal_seam_assemble(tal_seam *ctx, const double *u, double rho, double mu, double cvre, const double *pmat,
+                      const int64_t *ids, int64_t k, double *rhs)
+{
+    TAL_GUARD_BEGIN
+    return seam_assemble_impl(ctx, u, rho, mu, cvre, pmat, ids, k, rhs);
+    TAL_GUARD_END
+}
+
+int tal_seam_close(tal_seam *ctx)
+{
+    TAL_GUARD_BEGIN
+    seam_free(ctx);
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
 int tal_assemble_elements(int device, const double *coords, const int64_t *conn, int64_t n_nodes,
                           int64_t n_elems, const double *u, double rho, double mu, double cvre,
                           const double *pmat, const int64_t *ids, int64_t k, double *rhs)
 {
     TAL_GUARD_BEGIN
-    return seam_impl(device, coords, conn, n_nodes, n_elems, u, rho, mu, cvre, pmat, ids, k, rhs, false);
+    if (n_nodes < 0 || n_elems < 0 || k < 0)
+        return fail(TAL_EINVAL, "negative sizes");
+    if (k == 0 || n_nodes == 0)
+        return TAL_OK;
+    if (!coords || !conn || !u || !pmat || !ids || !rhs)
+        return fail(TAL_EINVAL, "NULL arrays");
+    if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
+        return fail(TAL_EINVAL, "too many nodes / elements");
+    {
+        std::atomic<bool> bad{false};
+        parallel_for(4 * n_elems, [&](int64_t i0, int64_t i1, int) {
+            for (int64_t i = i0; i < i1; ++i)
+                if (conn[i] < 0 || conn[i] >= n_nodes) {
+                    bad = true;
+                    return;
+                }
+        });
+        if (bad)
+            return fail(TAL_EINVAL, "connectivity index out of range [0, n_nodes)");
+    }
+    const SeamKey key{device, coords, conn, n_nodes, n_elems,
+                      content_hash(coords, sizeof(double) * 3 * n_nodes) * 31 +
+                          content_hash(conn, sizeof(int64_t) * 4 * n_elems)};
+    tal_seam *ctx = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_seam_mu);
+        for (size_t i = 0; i < g_seams.size(); ++i)
+            if (g_seams[i].first == key) {
+                ctx = g_seams[i].second;
+                std::rotate(g_seams.begin() + i, g_seams.begin() + i + 1, g_seams.end());
+                break;
+            }
+        if (!ctx) {
+            if (int rc = seam_open_impl(device, coords, conn, n_nodes, n_elems, &ctx))
+                return rc;
+            g_seams.push_back({key, ctx});
+            if (g_seams.size() > 2) {
+                seam_free(g_seams.front().second);
+                g_seams.erase(g_seams.begin());
+            }
+        }
+        // calls on one context serialise on its own mutex; the cache lock
+        // is held through the call so an eviction cannot free it underneath
+        return seam_assemble_impl(ctx, u, rho, mu, cvre, pmat, ids, k, rhs);
+    }
     TAL_GUARD_END
 }
 
@@ -1811,7 +2079,7 @@ int tal_assemble_elements_strict(int device, const double *coords, const int64_t
                                  const double *pmat, const int64_t *ids, int64_t k, double *rhs)
 {
     TAL_GUARD_BEGIN
-    return seam_impl(device, coords, conn, n_nodes, n_elems, u, rho, mu, cvre, pmat, ids, k, rhs, true);
+    return seam_impl(device, coords, conn, n_nodes, n_elems, u, rho, mu, cvre, pmat, ids, k, rhs);
     TAL_GUARD_END
 }
 

@@ -134,6 +134,43 @@ __global__ void __launch_bounds__(256) k_assemble_atomic(const int4 *__restrict_
     }
 }
 
+// the same over an element id list (the numba seam with a non-contiguous
+// 'ids' subset): conn rows ids[t]
+template <bool SYM>
+__global__ void __launch_bounds__(256) k_assemble_atomic_ids(const int4 *__restrict__ conn,
+                                                             const int32_t *__restrict__ ids, int64_t k,
+                                                             const double *__restrict__ nrec, RhsSoA rhs,
+                                                             ElemConsts kc)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= k)
+        return;
+    const int4 q = __ldg(conn + __ldg(ids + t));
+    const int n[4] = {q.x, q.y, q.z, q.w};
+    double X[4][3], U[4][3], R[4][3];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+        load_record_g(nrec, n[a], X[a], U[a]);
+    element_rhs<SYM>(X, U, nullptr, kc, R);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        atomicAdd(rhs.rx + n[a], R[a][0]);
+        atomicAdd(rhs.ry + n[a], R[a][1]);
+        atomicAdd(rhs.rz + n[a], R[a][2]);
+    }
+}
+
+// caller connectivity (int4, caller node ids) -> internal node ids, in place
+__global__ void k_remap_conn(int4 *c, int64_t k, const int32_t *__restrict__ iperm)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= k)
+        return;
+    int4 q = c[t];
+    q.x = iperm[q.x], q.y = iperm[q.y], q.z = iperm[q.z], q.w = iperm[q.w];
+    c[t] = q;
+}
+
 // ---------------------------------------------------------------------------
 // (2) one colour class per launch, plain read-modify-write (scatter = colored)
 // ---------------------------------------------------------------------------

@@ -118,20 +118,75 @@ bool check_coloring(const int64_t *conn, const int64_t *colors, int64_t n_nodes,
 
 namespace {
 
-// node -> element incidence (CSR)
-void node_elements(const int64_t *conn, int64_t n_nodes, int64_t n_elems,
-                   std::vector<int64_t> &off, std::vector<int32_t> &adj)
+// node -> element incidence (CSR), each list in ascending element id.
+// Parallel without atomics: thread t counts its contiguous element block into
+// its own count row, the rows become per-(thread, node) write cursors
+// (ascending thread order inside each node's list), then every thread fills
+// its block -- the serial lists exactly.  Threads are limited so the T x N
+// cursor table stays under ~2 GB.
+template <class Idx>
+void node_elements(const Idx *conn, int64_t n_nodes, int64_t n_elems, std::vector<int64_t> &off,
+                   std::vector<int32_t> &adj)
 {
     off.assign((size_t)n_nodes + 1, 0);
-    for (int64_t i = 0; i < 4 * n_elems; ++i)
-        off[conn[i] + 1]++;
+    adj.resize((size_t)(4 * n_elems));
+    int T = prep_threads();
+    while (T > 1 && (int64_t)T * n_nodes * 8 > ((int64_t)2 << 30))
+        --T;
+    if (T <= 1 || n_elems < (1 << 16)) {
+        for (int64_t i = 0; i < 4 * n_elems; ++i)
+            off[conn[i] + 1]++;
+        for (int64_t v = 0; v < n_nodes; ++v)
+            off[v + 1] += off[v];
+        std::vector<int64_t> pos(off.begin(), off.end() - 1);
+        for (int64_t e = 0; e < n_elems; ++e)
+            for (int a = 0; a < 4; ++a)
+                adj[pos[conn[4 * e + a]]++] = (int32_t)e;
+        return;
+    }
+    std::vector<std::unique_ptr<int64_t[]>> cur((size_t)T);
+    std::vector<std::thread> th;
+    auto run = [&](auto f) {
+        th.clear();
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&, t] { f(t); });
+        for (auto &x : th)
+            x.join();
+    };
+    auto eb = [&](int t) { return n_elems * t / T; };
+    run([&](int t) {
+        cur[t].reset(new int64_t[(size_t)n_nodes]());
+        int64_t *c = cur[t].get();
+        for (int64_t i = 4 * eb(t); i < 4 * eb(t + 1); ++i)
+            c[conn[i]]++;
+    });
+    // node totals, prefix sum, then per-(thread, node) cursors
+    run([&](int t) {
+        for (int64_t v = n_nodes * t / T; v < n_nodes * (t + 1) / T; ++v) {
+            int64_t sum = 0;
+            for (int r = 0; r < T; ++r)
+                sum += cur[r][v];
+            off[v + 1] = sum;
+        }
+    });
     for (int64_t v = 0; v < n_nodes; ++v)
         off[v + 1] += off[v];
-    adj.resize((size_t)(4 * n_elems));
-    std::vector<int64_t> pos(off.begin(), off.end() - 1);
-    for (int64_t e = 0; e < n_elems; ++e)
-        for (int a = 0; a < 4; ++a)
-            adj[pos[conn[4 * e + a]]++] = (int32_t)e;
+    run([&](int t) {
+        for (int64_t v = n_nodes * t / T; v < n_nodes * (t + 1) / T; ++v) {
+            int64_t at = off[v];
+            for (int r = 0; r < T; ++r) {
+                const int64_t c = cur[r][v];
+                cur[r][v] = at;
+                at += c;
+            }
+        }
+    });
+    run([&](int t) {
+        int64_t *c = cur[t].get();
+        for (int64_t e = eb(t); e < eb(t + 1); ++e)
+            for (int a = 0; a < 4; ++a)
+                adj[c[conn[4 * e + a]]++] = (int32_t)e;
+    });
 }
 
 // Node-node adjacency for Cuthill-McKee: the neighbours of v (the other
@@ -594,18 +649,9 @@ void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int m
     }
     // node -> tets
     Lap lap{"patches"};
-    std::vector<int64_t> off((size_t)n_nodes + 1, 0);
-    for (int64_t i = 0; i < 4 * n_elems; ++i)
-        off[conn4[i] + 1]++;
-    for (int64_t v = 0; v < n_nodes; ++v)
-        off[v + 1] += off[v];
-    std::vector<int32_t> adj((size_t)(4 * n_elems));
-    {
-        std::vector<int64_t> pos(off.begin(), off.end() - 1);
-        for (int64_t e = 0; e < n_elems; ++e)
-            for (int a = 0; a < 4; ++a)
-                adj[pos[conn4[4 * e + a]]++] = (int32_t)e;
-    }
+    std::vector<int64_t> off;
+    std::vector<int32_t> adj;
+    node_elements(conn4, n_nodes, n_elems, off, adj);
     lap("adjacency");
     // The greedy is sequential in tet order; it runs on contiguous blocks of
     // the order in parallel, speculatively.  When the serial walk reaches a

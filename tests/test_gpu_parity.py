@@ -530,3 +530,58 @@ def test_bad_colour_ids_are_rejected():
         mc = tb.Mesh(coords=m.coords, connectivity=m.connectivity, colors=cols)
         with pytest.raises(ValueError, match="colour ids"):
             tb.Assembler(mc, tb.RunConfig(scatter="colored"))
+
+
+@pytest.mark.parametrize("which", ["all", "range", "slabs", "scattered", "repeated"])
+@pytest.mark.parametrize("general", [False, True])
+def test_fast_seam_paths(oracle, which, general):
+    """tal_seam_*: the whole mesh (edge-star kernel), a contiguous range and
+    thread slabs (per-element kernel over the resident conn), an arbitrary
+    and a repeated id list (uploaded ids) -- each accumulating into rhs like
+    the numba loop, for the symmetric and a general pmat."""
+    m = tb.generate_box_mesh(7, 6, 5)
+    u = tb.make_velocity(m, "random:12")
+    pm = np.random.default_rng(4).uniform(0.0, 0.5, (4, 4)) if general else tb.interpolation_table()
+    E = m.n_elems
+    groups = {"all": [np.arange(E)], "range": [np.arange(17, 433)],
+              "slabs": [np.arange(lo, min(lo + 160, E)) for lo in range(0, E, 160)],
+              "scattered": [np.random.default_rng(2).permutation(E)[: E // 3]],
+              "repeated": [np.array([5, 5, 9, 0, 5, E - 1])]}[which]
+    start = np.random.default_rng(1).uniform(-1, 1, (m.n_nodes, 3))
+    ref, got = start.copy(), start.copy()
+    for ids in groups:
+        ids = ids.astype(np.int64)
+        oracle.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, ref)
+        tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, got)
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_stateless_seam_entry_sees_changed_arrays(oracle):
+    """tal_assemble_elements (the plain C entry) caches the resident mesh by
+    address + content hash: an in-place change of coords is re-uploaded."""
+    import ctypes
+    from paper_2403_08777_b200 import _native as N
+    m = tb.generate_box_mesh(5, 4, 4)
+    coords = np.array(m.coords)
+    conn = np.array(m.connectivity)
+    u = tb.make_velocity(m, "random:3")
+    pm = tb.interpolation_table()
+    ids = np.arange(m.n_elems, dtype=np.int64)
+
+    def call():
+        out = np.zeros((m.n_nodes, 3))
+        N.check(N.lib().tal_assemble_elements(0, N.ptr(coords), N.ptr(conn), coords.shape[0],
+                                              conn.shape[0], N.ptr(u), 1.0, 1e-3, 0.07, N.ptr(pm),
+                                              N.ptr(ids), ids.shape[0], N.ptr(out)))
+        ref = np.zeros_like(out)
+        oracle.assemble_elements(coords, conn, u, 1.0, 1e-3, 0.07, pm, ids, ref)
+        assert np.abs(out - ref).max() <= 1e-13 * np.abs(ref).max()
+        return out
+
+    a = call()
+    b = call()  # cached context
+    assert np.array_equal(a, b) or np.abs(a - b).max() <= 1e-15 * np.abs(a).max()
+    coords *= 1.5  # same address, new content
+    c = call()
+    assert not np.allclose(a, c)
+    del ctypes
