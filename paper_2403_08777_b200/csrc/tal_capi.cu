@@ -1905,8 +1905,18 @@ int seam_assemble_impl(tal_seam *c, const double *u, double rho, double mu, doub
     DeviceGuard g(h->device);
     cudaStream_t s = h->stream;
     const int64_t n3 = 3 * c->N;
-    parallel_for(n3, [&](int64_t i0, int64_t i1, int) { std::memcpy(c->pin_u + i0, u + i0, sizeof(double) * (i1 - i0)); });
-    if (int rc = tal_set_velocity_host(h, c->pin_u, s))
+    // pageable u -> pinned -> device in 4 MB pieces: the host copy of piece
+    // i+1 overlaps the DMA of piece i
+    constexpr int64_t PIECE = 1 << 19;  // doubles
+    for (int64_t i0 = 0; i0 < n3; i0 += PIECE) {
+        const int64_t i1 = std::min(n3, i0 + PIECE);
+        parallel_for(i1 - i0, [&](int64_t a, int64_t b, int) {
+            std::memcpy(c->pin_u + i0 + a, u + i0 + a, sizeof(double) * (b - a));
+        }, 1 << 15);
+        TAL_CK(cudaMemcpyAsync(h->staging + i0, c->pin_u + i0, sizeof(double) * (i1 - i0),
+                               cudaMemcpyHostToDevice, s));
+    }
+    if (int rc = tal_set_velocity_device(h, h->staging, s))
         return rc;
     int64_t nl = 0;
     if (seq && a0 == 0 && k == E) {  // the whole mesh: the resident edge-star kernel
@@ -1942,13 +1952,38 @@ int seam_assemble_impl(tal_seam *c, const double *u, double rho, double mu, doub
         }
         TAL_CK_LAUNCH();
     }
-    if (int rc = tal_get_rhs_host(h, c->pin_r, s))  // blocking
+    // device -> pinned in pieces; piece i is added into rhs while piece i+1 copies
+    if (int rc = tal_get_rhs_device(h, h->staging, s))
         return rc;
-    parallel_for(n3, [&](int64_t i0, int64_t i1, int) {
-        for (int64_t i = i0; i < i1; ++i)
-            rhs[i] += c->pin_r[i];
-    });
-    return TAL_OK;
+    const int64_t np_ = (n3 + PIECE - 1) / PIECE;
+    std::vector<cudaEvent_t> ev((size_t)np_);
+    for (auto &e : ev)
+        TAL_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int rc = TAL_OK;
+    for (int64_t p = 0; p < np_; ++p) {
+        const int64_t i0 = p * PIECE, i1 = std::min(n3, i0 + PIECE);
+        if (cudaMemcpyAsync(c->pin_r + i0, h->staging + i0, sizeof(double) * (i1 - i0), cudaMemcpyDeviceToHost,
+                            s) != cudaSuccess ||
+            cudaEventRecord(ev[p], s) != cudaSuccess) {
+            rc = fail(TAL_ECUDA, "seam D2H");
+            break;
+        }
+    }
+    for (int64_t p = 0; p < np_ && rc == TAL_OK; ++p) {
+        if (cudaEventSynchronize(ev[p]) != cudaSuccess) {
+            rc = fail(TAL_ECUDA, "seam D2H sync");
+            break;
+        }
+        const int64_t i0 = p * PIECE, i1 = std::min(n3, i0 + PIECE);
+        parallel_for(i1 - i0, [&](int64_t a, int64_t b, int) {
+            for (int64_t i = i0 + a; i < i0 + b; ++i)
+                rhs[i] += c->pin_r[i];
+        }, 1 << 15);
+    }
+    cudaStreamSynchronize(s);
+    for (auto &e : ev)
+        cudaEventDestroy(e);
+    return rc;
 }
 
 // stateless entry: a small cache of contexts keyed by the mesh arrays'

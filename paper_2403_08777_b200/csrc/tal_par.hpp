@@ -8,7 +8,10 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
+#include <mutex>
 #include <cstdlib>
 #include <sched.h>
 #include <thread>
@@ -30,6 +33,105 @@ inline int prep_threads()
     return n;
 }
 
+// Persistent worker pool: run(T, f) calls f(t) for t in [0, T), t = 0 on the
+// caller, the rest on parked workers (no thread creation per call -- the
+// seam's pipelined copies issue dozens of small parallel steps per call).
+// Nested or concurrent use (a worker calling run, or two host threads at
+// once) degrades to a serial loop in the caller, so it can never deadlock.
+class WorkerPool {
+  public:
+    static WorkerPool &get()
+    {
+        static WorkerPool pool(prep_threads());
+        return pool;
+    }
+    template <class F>
+    void run(int T, F &&f)
+    {
+        T = std::min(T, n_);
+        if (T <= 1 || in_worker()) {
+            for (int t = 0; t < T; ++t)
+                f(t);
+            return;
+        }
+        std::unique_lock<std::mutex> busy(busy_, std::try_to_lock);
+        if (!busy.owns_lock()) {
+            for (int t = 0; t < T; ++t)
+                f(t);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            job_ = [&f](int t) { f(t); };
+            want_ = T;
+            next_ = 1;
+            left_ = T - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        in_worker() = true;  // a nested run() from f(0) goes serial
+        f(0);
+        in_worker() = false;
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [&] { return left_ == 0; });
+        job_ = nullptr;
+    }
+    ~WorkerPool()
+    {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto &t : th_)
+            t.join();
+    }
+
+  private:
+    explicit WorkerPool(int n) : n_(std::max(1, n))
+    {
+        for (int i = 1; i < n_; ++i)
+            th_.emplace_back([this] { loop(); });
+    }
+    static bool &in_worker()
+    {
+        thread_local bool w = false;
+        return w;
+    }
+    void loop()
+    {
+        in_worker() = true;
+        uint64_t seen = 0;
+        for (;;) {
+            std::function<void(int)> job;
+            int t = -1;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < want_); });
+                if (stop_)
+                    return;
+                t = next_++;
+                if (next_ >= want_)
+                    seen = gen_;
+                job = job_;
+            }
+            job(t);
+            std::lock_guard<std::mutex> lk(m_);
+            if (--left_ == 0)
+                done_.notify_all();
+        }
+    }
+    int n_;
+    std::vector<std::thread> th_;
+    std::mutex m_, busy_;
+    std::condition_variable cv_, done_;
+    std::function<void(int)> job_;
+    uint64_t gen_ = 0;
+    int want_ = 0, next_ = 0, left_ = 0;
+    bool stop_ = false;
+};
+
 // f(begin, end, thread) over [0, n) in contiguous blocks, one per thread;
 // serial below 'grain' items.
 template <class F>
@@ -41,14 +143,7 @@ void parallel_for(int64_t n, F f, int64_t grain = 1 << 14)
             f((int64_t)0, n, 0);
         return;
     }
-    std::vector<std::thread> th;
-    th.reserve((size_t)T);
-    for (int t = 0; t < T; ++t) {
-        const int64_t b = n * t / T, e = n * (t + 1) / T;
-        th.emplace_back([=, &f] { f(b, e, t); });
-    }
-    for (auto &x : th)
-        x.join();
+    WorkerPool::get().run(T, [&](int t) { f(n * t / T, n * (t + 1) / T, t); });
 }
 
 // dynamic scheduling over [0, n) for uneven items: f(i, thread)
@@ -62,19 +157,15 @@ void parallel_items(int64_t n, F f, int64_t block = 16)
         return;
     }
     std::atomic<int64_t> next{0};
-    std::vector<std::thread> th;
-    for (int t = 0; t < T; ++t)
-        th.emplace_back([&, t] {
-            for (;;) {
-                const int64_t b = next.fetch_add(block);
-                if (b >= n)
-                    return;
-                for (int64_t i = b, e = std::min(n, b + block); i < e; ++i)
-                    f(i, t);
-            }
-        });
-    for (auto &x : th)
-        x.join();
+    WorkerPool::get().run(T, [&](int t) {
+        for (;;) {
+            const int64_t b = next.fetch_add(block);
+            if (b >= n)
+                return;
+            for (int64_t i = b, e = std::min(n, b + block); i < e; ++i)
+                f(i, t);
+        }
+    });
 }
 
 // sort of unique keys: per-thread std::sort runs, then a parallel multiway
