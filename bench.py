@@ -420,7 +420,7 @@ def run_ours(a) -> None:
         one_step()
     torch.cuda.synchronize()
     asm.profile_read()
-    fp64_tf, fp64_mhz = N.fp64_peak(dev, 0.5)  # burst: ~0.5 ms launches, best of 20
+    fp64_tf, fp64_mhz = N.fp64_peak(dev, 5.0)  # >= 5 ms DFMA launches, best of 20
 
     sampler = ClockSampler(dev)
     sampler.start()
@@ -720,9 +720,11 @@ def run_ours(a) -> None:
                        + (f" (fused unavailable: {dom.fused_error})" if dom.fused_error else ""))},
         "roofline": {"bound": "fp64", "kernel": kname, "achieved": tf, "peak": fp64_tf,
                      "unit": "TFLOP/s", "frac": tf / fp64_tf,
-                     "peak_source": "live DFMA probe in this run (tal_fp64_peak: ~0.5 ms "
-                                    "launches like one assembly, best of 20, at "
-                                    f"{fp64_mhz:.0f} MHz measured in-kernel); nominal "
+                     "peak_source": "live DFMA probe in this run (tal_fp64_peak: >= 5 ms "
+                                    "launches of 8 independent DFMA chains per thread, best of 20, at "
+                                    f"{fp64_mhz:.0f} MHz measured in-kernel); DFMA issues at ~58.3 of "
+                                    "the nominal 64 lanes/clk/SM while DMUL/DADD reach 63.8 "
+                                    "(tools/probe_fp64.cu, profiles/round2/probe_fp64.txt); nominal "
                                     f"{NOMINAL_FP64_TFLOPS} at 1965 MHz",
                      "frac_of_nominal": tf / NOMINAL_FP64_TFLOPS,
                      "probe_sm_mhz": fp64_mhz,

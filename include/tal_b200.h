@@ -45,6 +45,7 @@ extern "C" {
 #define TAL_ENOMEM 3 /* host or device allocation     -> MemoryError  */
 #define TAL_ESTATE 4 /* call order (e.g. no mesh yet) -> RuntimeError */
 #define TAL_EINTERNAL 5 /* unexpected internal failure  -> RuntimeError */
+#define TAL_EIO 6       /* file system error            -> OSError      */
 
 /* scatter strategies (the reference RunConfig.scatter, variants.py:74-101,
  * offers 'private' and 'colored'; the GPU adds two atomic forms) */
@@ -265,6 +266,30 @@ int tal_seam_open(int device, const double *coords, const int64_t *conn, int64_t
 int tal_seam_assemble(tal_seam *ctx, const double *u, double rho, double mu, double cvre,
                       const double *pmat, const int64_t *ids, int64_t k, double *rhs);
 int tal_seam_close(tal_seam *ctx);
+
+/* ---- mesh IO and partitioning (host only) ------------ */
+/* The reference's text format (mesh.py:280-371): tal_mesh_save_text writes
+ * it byte for byte like save_mesh; tal_mesh_load_text parses it like
+ * load_mesh (comments, blank lines, inverted elements re-oriented and
+ * counted).  A format error returns TAL_EINVAL with "line N: ..." and
+ * tal_last_error_line() = N (the reference's MeshFormatError.line). */
+typedef struct tal_meshbuf tal_meshbuf;
+int64_t tal_last_error_line(void);
+int tal_mesh_load_text(const char *path, tal_meshbuf **out);
+int tal_meshbuf_info(tal_meshbuf *b, int64_t *n_nodes, int64_t *n_elems, int64_t *n_reoriented);
+int tal_meshbuf_copy(tal_meshbuf *b, double *coords, int64_t *conn);
+int tal_meshbuf_free(tal_meshbuf *b);
+int tal_mesh_save_text(const char *path, const double *coords, const int64_t *conn,
+                       int64_t n_nodes, int64_t n_elems);
+/* Binary "TALMESH1": 64-byte header (magic, version, sizes, content hash),
+ * coords f64 (N,3), conn i64 (E,4); exact round trip, hash verified. */
+int tal_mesh_save_binary(const char *path, const double *coords, const int64_t *conn,
+                         int64_t n_nodes, int64_t n_elems);
+int tal_mesh_probe_binary(const char *path, int64_t *n_nodes, int64_t *n_elems, int *is_binary);
+int tal_mesh_load_binary(const char *path, double *coords, int64_t n_nodes, int64_t *conn,
+                         int64_t n_elems);
+/* Recursive coordinate bisection of n points (n,3) into 'world' parts. */
+int tal_rcb_parts(const double *points, int64_t n, int world, int32_t *parts);
 
 /* ---- multi-GPU interface (domain decomposition) ----------------------------- */
 /* Gather rhs of internal node ids list[0..n) into a packed buffer d_out

@@ -22,6 +22,10 @@ GPU path, against outputs of tet-assembly-lab 0.1.0 computed here:
 * ``rhs_shapes.npz``  assemble_baseline / assemble_rs (variants.py:522-550)
                        on the test_variants.py matrix + the 4^3 TG box
                        (``--shapes`` writes only this file)
+* ``meshio/``         files written by the reference's save_mesh, a commented
+                       file with inverted elements and malformed files with the
+                       line numbers of the reference's load_mesh errors
+                       (mesh.py:280-371; ``--meshio`` writes only these)
 This script is the only file in the repo that imports /root/reference; it is
 never run on the GPU box.
 """
@@ -72,6 +76,68 @@ def shapes() -> None:
     store["rs_4x4x4_taylor-green"] = tal.assemble_rs(m, u, params, RunConfig()).rhs
     np.savez_compressed(OUT / "rhs_shapes.npz", **store, **{f"meta_{k}": v for k, v in versions().items()})
     print("wrote rhs_shapes.npz", len(store))
+
+
+def meshio() -> None:
+    """Reference save_mesh / load_mesh behaviour (mesh.py:280-371)."""
+    import json
+    import warnings
+    from tet_assembly_lab import mesh as M
+    d = OUT / "meshio"
+    d.mkdir(exist_ok=True)
+    store = {}
+    box = tal.generate_box_mesh(3, 2, 2)
+    store["box3x2x2_coords"], store["box3x2x2_conn"] = box.coords, box.connectivity
+    tal.save_mesh(box, d / "box3x2x2.txt")
+    # awkward values: tiny, huge, negative zero, 17-digit mantissas
+    c = np.array([[0.0, 0.0, 0.0], [1e-5, 0.1, 1.0 / 3.0], [0.0, 1.0, 2.0 / 3.0],
+                  [-0.0, 1e300 * 0 + 3.0, 1e-300], [np.pi, -np.e, 1e22], [1.5, 2.5, -7.0]])
+    q = np.array([[0, 1, 2, 3], [1, 2, 4, 5]], dtype=np.int64)
+    vols = M.signed_volumes(c, q)
+    q[vols < 0] = q[vols < 0][:, [0, 1, 3, 2]]
+    odd = tal.Mesh(coords=c, connectivity=q)
+    store["odd_coords"], store["odd_conn"] = odd.coords, odd.connectivity
+    tal.save_mesh(odd, d / "odd.txt")
+    # comments, blank lines, two inverted elements (re-oriented on load)
+    b2 = tal.generate_box_mesh(2, 1, 1)
+    conn = b2.connectivity.copy()
+    conn[[1, 4]] = conn[[1, 4]][:, [0, 1, 3, 2]]
+    lines = ["# a hand-edited file", "", f"nodes {b2.n_nodes}   # count"]
+    lines += [f"  {x!r} {y!r} {z!r}  " for x, y, z in b2.coords.tolist()]
+    lines += ["", "elems %d" % b2.n_elems] + [" ".join(map(str, r)) + "  # tet" for r in conn.tolist()]
+    (d / "commented_inverted.txt").write_text("\n".join(lines) + "\n")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ci = tal.load_mesh(d / "commented_inverted.txt")
+    store["commented_inverted_coords"], store["commented_inverted_conn"] = ci.coords, ci.connectivity
+    np.savez_compressed(d / "meshes.npz", **store)
+    good = (d / "box3x2x2.txt").read_text().splitlines()
+    bad = {
+        "err_header.txt": ["node 5"] + good[1:],
+        "err_count.txt": ["nodes five"] + good[1:],
+        "err_ncoord.txt": good[:3] + ["0.5 0.5"] + good[4:],
+        "err_coord.txt": good[:4] + ["0.5 x 0.5"] + good[5:],
+        "err_elems.txt": good[:good.index("elems 72")] + ["elements 72"] + good[good.index("elems 72") + 1:],
+        "err_nidx.txt": good[:-1] + ["1 2 3"],
+        "err_idx.txt": good[:-2] + ["1 2 3 q"] + good[-1:],
+        "err_eof_nodes.txt": good[:10],
+        "err_eof_elems.txt": good[:-5],
+        "err_trailing.txt": good + ["", "extra 1"],
+        "err_range.txt": good[:-1] + ["0 1 2 999"],
+        "err_empty.txt": ["# nothing here"],
+    }
+    errors = {}
+    for name, ls in bad.items():
+        (d / name).write_text("\n".join(ls) + "\n")
+        try:
+            tal.load_mesh(d / name)
+            raise AssertionError(f"{name} loaded")
+        except M.MeshFormatError as e:
+            errors[name] = {"type": "MeshFormatError", "line": e.line, "message": str(e)}
+        except ValueError as e:
+            errors[name] = {"type": "ValueError", "message": str(e)}
+    (d / "errors.json").write_text(json.dumps(errors, indent=1) + "\n")
+    print("wrote meshio goldens", sorted(p.name for p in d.iterdir()))
 
 
 def main() -> None:
@@ -194,5 +260,8 @@ def main() -> None:
     print("wrote", sorted(p.name for p in OUT.glob("*.npz")), meta)
 
 
+if __name__ == "__main__" and "--meshio" in sys.argv:
+    meshio()
+    sys.exit(0)
 if __name__ == "__main__":
     main()

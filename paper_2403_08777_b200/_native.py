@@ -15,7 +15,7 @@ import numpy as np
 
 LIB_PATH = Path(os.environ.get("TAL_LIB_PATH") or Path(__file__).resolve().parent / "libtal_b200.so")
 
-TAL_OK, TAL_EINVAL, TAL_ECUDA, TAL_ENOMEM, TAL_ESTATE = 0, 1, 2, 3, 4
+TAL_OK, TAL_EINVAL, TAL_ECUDA, TAL_ENOMEM, TAL_ESTATE, TAL_EINTERNAL, TAL_EIO = 0, 1, 2, 3, 4, 5, 6
 
 SCATTER = {"private": 0, "colored": 1, "atomic": 2, "private-atomic": 3, "sequential": 4}
 VARIANT = {"b": 0, "rs": 1, "rsp": 2, "p": 3}  # TAL_VARIANT_* ("p": study-only shape)
@@ -103,6 +103,17 @@ SIGNATURES = [
     ("tal_synchronize", _I, [_P, _P]),
     ("tal_assemble_elements", _I, [_I, _P, _P, _I64, _I64, _P, _D, _D, _D, _P, _P, _I64, _P]),
     ("tal_assemble_elements_strict", _I, [_I, _P, _P, _I64, _I64, _P, _D, _D, _D, _P, _P, _I64, _P]),
+    ("tal_last_error_line", _I64, []),
+    ("tal_mesh_load_text", _I, [ctypes.c_char_p, ctypes.POINTER(_P)]),
+    ("tal_meshbuf_info", _I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    ("tal_meshbuf_copy", _I, [_P, _P, _P]),
+    ("tal_meshbuf_free", _I, [_P]),
+    ("tal_mesh_save_text", _I, [ctypes.c_char_p, _P, _P, _I64, _I64]),
+    ("tal_mesh_save_binary", _I, [ctypes.c_char_p, _P, _P, _I64, _I64]),
+    ("tal_mesh_probe_binary", _I, [ctypes.c_char_p, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                                   ctypes.POINTER(_I)]),
+    ("tal_mesh_load_binary", _I, [ctypes.c_char_p, _P, _I64, _P, _I64]),
+    ("tal_rcb_parts", _I, [_P, _I64, _I, _P]),
     ("tal_seam_open", _I, [_I, _P, _P, _I64, _I64, ctypes.POINTER(_P)]),
     ("tal_seam_assemble", _I, [_P, _P, _D, _D, _D, _P, _P, _I64, _P]),
     ("tal_seam_close", _I, [_P]),
@@ -157,6 +168,8 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == TAL_ENOMEM:
         raise MemoryError(msg)
+    if rc == TAL_EIO:
+        raise OSError(msg)
     raise RuntimeError(msg or f"libtal_b200 error {rc}")
 
 

@@ -22,6 +22,7 @@
 #include <memory>
 #include <atomic>
 #include "tal_prep.hpp"
+#include "tal_meshio.hpp"
 #include "tal_par.hpp"
 #include "tal_shapes.cuh"
 
@@ -32,10 +33,12 @@ static_assert(SLOTS == PATCH_SLOTS && BLOB_LEVELS == CHUNK_LEVELS, "blob layout 
 namespace {
 
 thread_local std::string g_err;
+thread_local int64_t g_err_line = 0;
 
 int fail(int code, const std::string &msg)
 {
     g_err = msg;
+    g_err_line = 0;
     return code;
 }
 
@@ -851,6 +854,9 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
     L.cfg = cfg;
     lap("reorder");
     build_patches(L.cord.data(), n_nodes, n_elems, opts.patch_mode, L.patches);
+#if TAL_ORIENT
+    orient_patches(L.patches, L.xin.data());
+#endif
     lap("patches");
     std::vector<uint8_t> ext;
     if (n_external) {
@@ -883,6 +889,119 @@ int host_layout(const double *coords, const int64_t *conn, int64_t n_nodes, int6
 extern "C" {
 
 const char *tal_last_error(void) { return g_err.c_str(); }
+int64_t tal_last_error_line(void) { return g_err_line; }
+
+// ---- mesh IO / partitioning (tal_meshio.cpp) ---------------------------------
+struct tal_meshbuf {
+    MeshText m;
+};
+
+int tal_mesh_load_text(const char *path, tal_meshbuf **out)
+{
+    TAL_GUARD_BEGIN
+    if (!path || !out)
+        return fail(TAL_EINVAL, "NULL argument");
+    *out = nullptr;
+    std::unique_ptr<tal_meshbuf> b(new tal_meshbuf());
+    std::string err;
+    int64_t line = 0;
+    if (!load_mesh_text(path, b->m, err, line)) {
+        const int rc = fail(TAL_EINVAL, line > 0 ? "line " + std::to_string(line) + ": " + err : err);
+        g_err_line = line;
+        return rc;
+    }
+    *out = b.release();
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_meshbuf_info(tal_meshbuf *b, int64_t *n_nodes, int64_t *n_elems, int64_t *n_reoriented)
+{
+    TAL_GUARD_BEGIN
+    if (!b || !n_nodes || !n_elems || !n_reoriented)
+        return fail(TAL_EINVAL, "NULL argument");
+    *n_nodes = b->m.n_nodes, *n_elems = b->m.n_elems, *n_reoriented = b->m.n_reoriented;
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_meshbuf_copy(tal_meshbuf *b, double *coords, int64_t *conn)
+{
+    TAL_GUARD_BEGIN
+    if (!b || (b->m.n_nodes && !coords) || (b->m.n_elems && !conn))
+        return fail(TAL_EINVAL, "NULL argument");
+    std::memcpy(coords, b->m.coords.data(), sizeof(double) * b->m.coords.size());
+    std::memcpy(conn, b->m.conn.data(), sizeof(int64_t) * b->m.conn.size());
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_meshbuf_free(tal_meshbuf *b)
+{
+    delete b;
+    return TAL_OK;
+}
+
+int tal_mesh_save_text(const char *path, const double *coords, const int64_t *conn, int64_t n_nodes,
+                       int64_t n_elems)
+{
+    TAL_GUARD_BEGIN
+    if (!path || n_nodes < 0 || n_elems < 0 || (n_nodes && !coords) || (n_elems && !conn))
+        return fail(TAL_EINVAL, "bad arguments");
+    std::string err;
+    if (!save_mesh_text(path, coords, conn, n_nodes, n_elems, err))
+        return fail(TAL_EIO, err);
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_mesh_save_binary(const char *path, const double *coords, const int64_t *conn, int64_t n_nodes,
+                         int64_t n_elems)
+{
+    TAL_GUARD_BEGIN
+    if (!path || n_nodes < 0 || n_elems < 0 || (n_nodes && !coords) || (n_elems && !conn))
+        return fail(TAL_EINVAL, "bad arguments");
+    std::string err;
+    if (!save_mesh_binary(path, coords, conn, n_nodes, n_elems, err))
+        return fail(TAL_EIO, err);
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_mesh_probe_binary(const char *path, int64_t *n_nodes, int64_t *n_elems, int *is_binary)
+{
+    TAL_GUARD_BEGIN
+    if (!path || !n_nodes || !n_elems || !is_binary)
+        return fail(TAL_EINVAL, "NULL argument");
+    const int r = probe_mesh_binary(path, n_nodes, n_elems);
+    if (r < 0)
+        return fail(TAL_EIO, std::string("cannot open ") + path);
+    *is_binary = r;
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_mesh_load_binary(const char *path, double *coords, int64_t n_nodes, int64_t *conn, int64_t n_elems)
+{
+    TAL_GUARD_BEGIN
+    if (!path || n_nodes < 0 || n_elems < 0 || (n_nodes && !coords) || (n_elems && !conn))
+        return fail(TAL_EINVAL, "bad arguments");
+    std::string err;
+    if (!load_mesh_binary(path, coords, n_nodes, conn, n_elems, err))
+        return fail(TAL_EINVAL, err);
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_rcb_parts(const double *points, int64_t n, int world, int32_t *parts)
+{
+    TAL_GUARD_BEGIN
+    if (n < 0 || world < 1 || (n && (!points || !parts)))
+        return fail(TAL_EINVAL, "bad arguments (world must be >= 1)");
+    rcb_parts(points, n, world, parts);
+    return TAL_OK;
+    TAL_GUARD_END
+}
 int tal_abi_version(void) { return TAL_ABI_VERSION; }
 
 int tal_device_count(int *count)

@@ -133,14 +133,16 @@ __device__ __forceinline__ void pressure_add(double pbar, double det, const doub
 // folds its running sums into them instead of separate adds).  With NEG3 the
 // c3 argument holds -c3 (the ring kernel carries c2 of the previous tet; the
 // negation becomes a free operand modifier instead of three DADDs).
-template <bool ACC, bool NEG3 = false>
+// POS: the caller guarantees det > 0 (patches oriented on the host), so
+// |det| = det and the sign folds vanish.
+template <bool ACC, bool NEG3 = false, bool POS = false>
 __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3], const double c3[3],
                                          double det, const double du1[3], const double du2[3],
                                          const double du3[3], const double U0[3], const double U1[3],
                                          const double S01[3], const double U2[3], const double U3[3],
                                          const ElemConsts &k, double R[4][3])
 {
-    const double ad = abs_bits(det);
+    const double ad = POS ? det : abs_bits(det);
     double c3v[3];
 #pragma unroll
     for (int kk = 0; kk < 3; ++kk)
@@ -179,8 +181,8 @@ __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3],
     if (aah * inv * inv > 1e-30 && t > 0.0)  // kernel.py:24 guard, in G units
         f = (k.rc6 * r3) * (is_normal_pos(t) ? rsqrt_fast(t) : rsqrt(t));
     const double B = fma(f, ssqh, k.mu6) * inv;  // -(mu + rho nu_t) / (6 |D|)
-    const double As = mul_sign(k.a_po, det), Aq = mul_sign(k.a_q, det);
-    const double A4 = mul_sign(k.a_4, det);
+    const double As = POS ? k.a_po : mul_sign(k.a_po, det), Aq = POS ? k.a_q : mul_sign(k.a_q, det);
+    const double A4 = POS ? k.a_4 : mul_sign(k.a_4, det);
     double w[4][3];
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {

@@ -87,6 +87,16 @@ __device__ __forceinline__ int4 ldg_stream(const int4 *p)
     return r;
 }
 
+// shared-memory loads that the compiler may neither hoist nor merge (the
+// ring loop re-reads the patch's a/b records instead of holding them in
+// registers: TAL_RELOAD_AB)
+__device__ __forceinline__ double2 lds2(uint32_t a)
+{
+    double2 r;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(a));
+    return r;
+}
+
 // one 48-B node record -> X, U (three 16-B loads; global or shared)
 __device__ __forceinline__ void load_record_g(const double *__restrict__ rec, int v, double X[3],
                                               double U[3])
@@ -255,6 +265,12 @@ constexpr int kRingUnroll = TAL_RING_UNROLL;
 #ifndef TAL_GATHER_COOP
 #define TAL_GATHER_COOP 1
 #endif
+#ifndef TAL_RELOAD_AB
+#define TAL_RELOAD_AB 0
+#endif
+#ifndef TAL_ORIENT
+#define TAL_ORIENT 0  // experiment: host-oriented patches (every ring tet det > 0)
+#endif
 
 template <>
 struct PrivCfg<1> {  // 128 patches / chunk
@@ -405,8 +421,17 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
             //   e1 = x_b - x_a, du1 = u_b - u_a (patch constants),
             //   e2(t) = e3(t-1), du2(t) = du3(t-1), c3(t) = e1 x e2(t) = -c2(t-1)
             // (carried as nc3 = -c3 = c2(t-1): tet_tail<.., NEG3> folds the sign)
+#if TAL_RELOAD_AB
+            // a's and b's records are re-read per tet (5 LDS.128) instead of
+            // living in 18 registers
+            const uint32_t ra = smem_u32(nr + 6 * ID(1)), rb = smem_u32(nr + 6 * ID(2));
+            double S01[3], e1[3], du1[3], e2[3], du2[3], U2[3], nc3[3];
+            {
+                double Xa[3], Ua[3], Ub[3];
+#else
             double Xa[3], Ua[3], Ub[3], S01[3], e1[3], du1[3], e2[3], du2[3], U2[3], nc3[3];
             {
+#endif
                 double Xb[3], Xr[3];
                 load_record_s(nr, ID(1), Xa, Ua);
                 load_record_s(nr, ID(2), Xb, Ub);
@@ -435,6 +460,15 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
                 double X3[3], U3[3], e3[3], du3[3], c1[3], c2[3];
                 const int nxt = (t + 1 == m) ? 0 : t + 1;
                 load_record_s(nr, ID(3 + nxt), X3, U3);
+#if TAL_RELOAD_AB
+                double Xa[3], Ua[3], Ub[3];
+                {
+                    const double2 p0 = lds2(ra), p1 = lds2(ra + 16), p2 = lds2(ra + 32);
+                    const double2 q1 = lds2(rb + 16), q2 = lds2(rb + 32);
+                    Xa[0] = p0.x, Xa[1] = p0.y, Xa[2] = p1.x, Ua[0] = p1.y, Ua[1] = p2.x, Ua[2] = p2.y;
+                    Ub[0] = q1.y, Ub[1] = q2.x, Ub[2] = q2.y;
+                }
+#endif
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     e3[q] = X3[q] - Xa[q];
@@ -443,7 +477,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
                 cross3(e2, e3, c1);
                 cross3(e3, e1, c2);
                 const double det = fma(e1[0], c1[0], fma(e1[1], c1[1], e1[2] * c1[2]));
-                tet_tail<true, true>(c1, c2, nc3, det, du1, du2, du3, Ua, Ub, S01, U2, U3, kc, R);
+                tet_tail<true, true, TAL_ORIENT != 0>(c1, c2, nc3, det, du1, du2, du3, Ua, Ub, S01, U2, U3, kc, R);
                 if (PR) {
                     const double p3 = pres_s[ID(3 + nxt)];
                     const double c3[3] = {-nc3[0], -nc3[1], -nc3[2]};

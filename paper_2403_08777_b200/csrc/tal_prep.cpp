@@ -765,6 +765,40 @@ void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int m
     lap("fix-up + concat");
 }
 
+bool orient_patches(Patches &P, const double *xyz)
+{
+    auto det = [&](int32_t a, int32_t b, int32_t c, int32_t d) {
+        double e[3][3];
+        for (int k = 0; k < 3; ++k) {
+            e[0][k] = xyz[3 * (int64_t)b + k] - xyz[3 * (int64_t)a + k];
+            e[1][k] = xyz[3 * (int64_t)c + k] - xyz[3 * (int64_t)a + k];
+            e[2][k] = xyz[3 * (int64_t)d + k] - xyz[3 * (int64_t)a + k];
+        }
+        return e[0][0] * (e[1][1] * e[2][2] - e[1][2] * e[2][1]) +
+               e[0][1] * (e[1][2] * e[2][0] - e[1][0] * e[2][2]) +
+               e[0][2] * (e[1][0] * e[2][1] - e[1][1] * e[2][0]);
+    };
+    std::atomic<bool> ok{true};
+    parallel_for(P.n_patches(), [&](int64_t g0, int64_t g1, int) {
+        for (int64_t g = g0; g < g1; ++g) {
+            int32_t *v = P.nodes.data() + P.off[g];
+            const int m = P.off[g + 1] - P.off[g] - 2;
+            const int k = P.closed[g] ? m : m - 1;
+            int pos = 0, neg = 0;
+            for (int t = 0; t < k; ++t) {
+                const double d = det(v[0], v[1], v[2 + t], v[2 + (t + 1 == m ? 0 : t + 1)]);
+                pos += d > 0.0;
+                neg += d < 0.0;
+            }
+            if (neg == k)
+                std::swap(v[0], v[1]);
+            else if (pos != k)
+                ok = false;
+        }
+    }, 1 << 12);
+    return ok;
+}
+
 // ---------------------------------------------------------------------------
 // Bank-aware placement of a chunk's node records in shared memory.
 //

@@ -46,6 +46,11 @@ struct Patches {
 // still-unassigned tets around one of the current tet's edges; ties -> the
 // most compact tet-index span), tets visited in the given order.
 void build_patches(const int32_t *conn4, int64_t n_nodes, int64_t n_elems, int mode, Patches &out);
+// Orient every patch so that all of its tets (a, b, r_t, r_t+1) have det > 0
+// (swap a and b where all are negative).  Returns false if some patch has a
+// tet with det <= 0 left (degenerate / inverted / mixed ring): the kernel
+// must then keep the sign-generic arithmetic.  xyz: internal coords (AoS).
+bool orient_patches(Patches &p, const double *xyz);
 
 // CTA chunking of the patch sequence for the private scatter.  Each node's
 // contributions inside a chunk (one per patch that touches it) are laid out

@@ -151,30 +151,22 @@ class SlabPartition:
 
 
 def rcb_parts(points: np.ndarray, world: int) -> np.ndarray:
-    """Recursive coordinate bisection: a part id in [0, world) per point.
+    """Recursive coordinate bisection: a part id in [0, world) per point
+    (native, csrc/tal_meshio.cpp: rcb_parts).
 
-    Each level splits the current set along its largest extent at the count
-    that gives the two halves floor(k/2) and ceil(k/2) of the k parts
-    (balanced to one element); ties resolved by a stable sort, so every rank
-    computes the same partition."""
-    pts = np.asarray(points, dtype=np.float64)
-    n = pts.shape[0]
-    part = np.zeros(n, dtype=np.int32)
+    Each level splits the current set along its largest extent (first axis
+    on ties) at the count that gives the two halves floor(k/2) and ceil(k/2)
+    of the k parts (balanced to one element); ties in the coordinate keep
+    the set's order (a stable sort), so every rank computes the same
+    partition.  Sub-problems of a level run in parallel on the host."""
+    from ._native import check, lib, ptr
+    pts = np.ascontiguousarray(points, dtype=np.float64)
     if world < 1:
         raise ValueError("world must be >= 1")
-    stack = [(np.arange(n), 0, world)]
-    while stack:
-        idx, first, k = stack.pop()
-        if k == 1 or idx.size == 0:
-            part[idx] = first
-            continue
-        kl = k // 2
-        sub = pts[idx]
-        ax = int(np.argmax(sub.max(axis=0) - sub.min(axis=0))) if idx.size else 0
-        order = np.argsort(sub[:, ax], kind="stable")
-        cut = (idx.size * kl) // k
-        stack.append((idx[order[:cut]], first, kl))
-        stack.append((idx[order[cut:]], first + kl, k - kl))
+    if pts.ndim != 2 or pts.shape[1] != 3:
+        raise ValueError("points must have shape (n, 3)")
+    part = np.zeros(pts.shape[0], dtype=np.int32)
+    check(lib().tal_rcb_parts(ptr(pts), pts.shape[0], int(world), ptr(part)))
     return part
 
 

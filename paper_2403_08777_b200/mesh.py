@@ -212,3 +212,76 @@ def plan_layout(mesh, cfg=None) -> dict:
                                 ctypes.byref(o), ctypes.byref(inf)))
     return {k: getattr(inf, k) for k, _ in N.TalMeshInfo._fields_
             if k not in ("n_colors", "device_bytes")}
+
+
+# ---------------------------------------------------------------------------
+# mesh IO (native, csrc/tal_meshio.cpp)
+# ---------------------------------------------------------------------------
+
+class MeshFormatError(ValueError):
+    """Unparseable mesh file; ``line`` is the 1-based offending line number
+    (the reference's mesh.MeshFormatError, mesh.py:22-29)."""
+
+    def __init__(self, message: str, line: Optional[int] = None):
+        # the native message already carries the "line N: " prefix
+        super().__init__(message)
+        self.line = line
+
+
+def _path(path) -> bytes:
+    import os
+    return os.fsencode(os.fspath(path))
+
+
+def save_mesh(mesh, path) -> None:
+    """The reference's text format (mesh.py:280-290), byte for byte:
+    ``nodes <n>``, n ``x y z`` lines (%.17g), ``elems <m>``, m lines of 4
+    zero-based node ids.  Formatted in parallel native blocks."""
+    coords = np.ascontiguousarray(mesh.coords, dtype=np.float64)
+    conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int64)
+    check(lib().tal_mesh_save_text(_path(path), ptr(coords), ptr(conn), coords.shape[0], conn.shape[0]))
+
+
+def save_mesh_binary(mesh, path) -> None:
+    """Binary TALMESH1 file (64-byte header with sizes and a content hash,
+    coords f64 (N,3), connectivity i64 (E,4)): exact round trip for meshes
+    too large for the text format."""
+    coords = np.ascontiguousarray(mesh.coords, dtype=np.float64)
+    conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int64)
+    check(lib().tal_mesh_save_binary(_path(path), ptr(coords), ptr(conn), coords.shape[0], conn.shape[0]))
+
+
+def load_mesh(path) -> Mesh:
+    """Read a mesh file: TALMESH1 binary (detected by its magic) or the
+    reference's text format with its semantics (mesh.py:293-371): ``#``
+    comments and blank lines skipped, MeshFormatError with the line number on
+    malformed input, ValueError for out-of-range ids, inverted elements
+    re-oriented (last two nodes swapped) with a warning."""
+    import warnings
+    from pathlib import Path
+    p = _path(path)
+    n, e, is_bin = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+    check(lib().tal_mesh_probe_binary(p, ctypes.byref(n), ctypes.byref(e), ctypes.byref(is_bin)))
+    if is_bin.value:
+        coords = np.empty((n.value, 3))
+        conn = np.empty((e.value, 4), dtype=np.int64)
+        check(lib().tal_mesh_load_binary(p, ptr(coords), n.value, ptr(conn), e.value))
+        return Mesh(coords=coords, connectivity=conn)
+    h = ctypes.c_void_p()
+    rc = lib().tal_mesh_load_text(p, ctypes.byref(h))
+    if rc != 0:
+        line = int(lib().tal_last_error_line())
+        if line > 0:
+            raise MeshFormatError((lib().tal_last_error() or b"").decode(errors="replace"), line)
+        check(rc)
+    try:
+        nr = ctypes.c_int64()
+        check(lib().tal_meshbuf_info(h, ctypes.byref(n), ctypes.byref(e), ctypes.byref(nr)))
+        coords = np.empty((n.value, 3))
+        conn = np.empty((e.value, 4), dtype=np.int64)
+        check(lib().tal_meshbuf_copy(h, ptr(coords), ptr(conn)))
+    finally:
+        lib().tal_meshbuf_free(h)
+    if nr.value:
+        warnings.warn(f"{Path(path).name}: re-oriented {nr.value} inverted element(s)", stacklevel=2)
+    return Mesh(coords=coords, connectivity=conn)

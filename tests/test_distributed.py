@@ -194,3 +194,41 @@ def test_rcb_exchange_gloo_matches_single_domain(tmp_path, world, oracle):
     assert nbrs >= 2
     assert not np.isnan(full).any()
     assert oracle.compare(full, ref, g.coords, g.connectivity, ug).passed
+
+
+def _rcb_numpy(points, world):
+    """The numpy statement of RCB (round 1's implementation, kept here as the
+    checker of the native partitioner)."""
+    pts = np.asarray(points, dtype=np.float64)
+    part = np.zeros(pts.shape[0], dtype=np.int32)
+    stack = [(np.arange(pts.shape[0]), 0, world)]
+    while stack:
+        idx, first, k = stack.pop()
+        if k == 1 or idx.size == 0:
+            part[idx] = first
+            continue
+        kl = k // 2
+        sub = pts[idx]
+        ax = int(np.argmax(sub.max(axis=0) - sub.min(axis=0)))
+        order = np.argsort(sub[:, ax], kind="stable")
+        cut = (idx.size * kl) // k
+        stack.append((idx[order[:cut]], first, kl))
+        stack.append((idx[order[cut:]], first + kl, k - kl))
+    return part
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 7, 8, 16])
+@pytest.mark.parametrize("case", ["box", "permuted", "ties", "random"])
+def test_native_rcb_equals_numpy_statement(world, case):
+    from paper_2403_08777_b200.distributed import rcb_parts
+    if case == "box":
+        m = tb.generate_box_mesh(9, 7, 5)
+        pts = m.coords[m.connectivity].mean(axis=1)
+    elif case == "permuted":
+        m = _perm_box((8, 6, 7), seed=3)
+        pts = m.coords[m.connectivity].mean(axis=1)
+    elif case == "ties":  # many equal coordinates: the stable order decides
+        pts = np.floor(np.random.default_rng(1).uniform(0, 4, (3000, 3)))
+    else:
+        pts = np.random.default_rng(2).normal(size=(20000, 3)) * [1.0, 3.0, 0.5]
+    np.testing.assert_array_equal(rcb_parts(pts, world), _rcb_numpy(pts, world))
