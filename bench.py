@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--permute", action="store_true", help="config 3: random node permutation")
     ap.add_argument("--pressure", action="store_true",
                     help="add the P1 pressure-gradient term (extension; uniform [-1,1) nodal p, seed 2)")
+    ap.add_argument("--supg", action="store_true",
+                    help="add the SUPG stabilisation term (extension; c1=4, c2=2)")
     ap.add_argument("--partition", choices=["slab", "rcb"], default="slab",
                     help="N>1: z-slabs of the box (weak scaling) or RCB of the (optionally "
                          "--permute'd) global box mesh, exchange-path interface sum")
@@ -316,7 +318,7 @@ def traffic_key(a, workload: str) -> str:
     kernel's memory behaviour (node numbering, element order, chunking)."""
     return (f"{workload} | permuted={int(bool(a.permute))} renumber={a.renumber} "
             f"element_order={a.element_order} patches={a.patches} cta={a.cta_patches} "
-            f"chunk_nodes={a.chunk_nodes} pressure={int(bool(a.pressure))}")
+            f"chunk_nodes={a.chunk_nodes} pressure={int(bool(a.pressure))} supg={int(bool(a.supg))}")
 
 
 def ncu_traffic(kernel_key: str, key: str) -> dict:
@@ -388,6 +390,8 @@ def run_ours(a) -> None:
     if a.pressure:
         press = np.random.default_rng(2).uniform(-1.0, 1.0, mesh.n_nodes)
         asm.set_pressure(press)
+    if a.supg:
+        asm.set_stabilization(True)
     E, Nn = mesh.n_elems, mesh.n_nodes
 
     stream = torch.cuda.current_stream().cuda_stream
@@ -651,6 +655,8 @@ def run_ours(a) -> None:
         ref = O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=O.default_threads())
         if press is not None:
             ref = ref + O.pressure_gradient(mesh.coords, mesh.connectivity, press)
+        if a.supg:
+            ref = ref + O.supg_term(mesh.coords, mesh.connectivity, u)
         chk = O.compare(rhs_gpu, ref, mesh.coords, mesh.connectivity, u)
         parity = {"reference_rel_diff": chk.rel_diff, "rel_l2": chk.rel_l2,
                   "entry_rel": chk.entry_rel, "passed": bool(chk.passed)}
@@ -707,7 +713,8 @@ def run_ours(a) -> None:
                    "renumber": a.renumber, "element_order": a.element_order,
                    "patches": a.patches, "cta_patches": a.cta_patches, "chunk_nodes": a.chunk_nodes,
                    "permuted": bool(a.permute), "variant": a.variant,
-                   "pressure_term": bool(a.pressure), "cuda_graph": bool(use_graph),
+                   "pressure_term": bool(a.pressure), "supg_term": bool(a.supg),
+                   "cuda_graph": bool(use_graph),
                    "l2": "flushed (256 MiB write) before every step, outside the timed events"
                          if flush_buf is not None else "not flushed",
                    "gpus_shared": torch.cuda.device_count() < ws,

@@ -227,6 +227,15 @@ int tal_run_variant(tal_handle *h, const tal_params *p, int variant, int scatter
 int tal_graph_capture(tal_handle *h, const tal_params *p, int variant, int scatter);
 int tal_graph_launch(tal_handle *h, void *stream, int64_t *kernel_launches);
 int tal_graph_destroy(tal_handle *h);
+/* Optional SUPG stabilisation of the convective residual (extension, no
+ * reference counterpart; tal_element.cuh supg_add): every later RSP-shape
+ * assembly on this handle adds
+ *   r_a[i] -= int tau (rho u.grad N_a)(rho u.grad u_i),
+ *   tau = 1 / (c1 (mu + rho nu_t) / h^2 + c2 rho |u_mean| / h), h = cbrt(6 vol).
+ * enable = 0 switches it off.  Needs the symmetric Gauss table; not with
+ * scatter 'sequential', the B/RS shapes or the fused multi-GPU path
+ * (TAL_EINVAL).  A captured graph (tal_graph_capture) is dropped. */
+int tal_set_stabilization(tal_handle *h, int enable, double c1, double c2);
 /* tal_get_rhs_host blocks until rhs (caller order, (N,3) AoS) is complete. */
 int tal_get_rhs_host(tal_handle *h, double *rhs, void *stream);
 int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream);

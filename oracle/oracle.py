@@ -25,6 +25,9 @@ Exception -- parity UNPINNED: ``pressure_gradient``
 has no counterpart in the reference (its operator has no pressure term,
 kernel.py:7-10); it is restated here from the weak form and
 checked only against closed-form answers (tests/test_pressure.py).
+The same holds for ``supg_term`` (the SUPG stabilisation extension): restated
+from its weak form with explicit Gauss points and the reference's Vreman
+formula (kernel.py:99-143), pinned by closed forms (tests/test_stabilization.py).
 """
 
 from __future__ import annotations
@@ -224,6 +227,65 @@ def pressure_gradient(coords, conn, p) -> np.ndarray:
     vol = np.abs(det) / 6.0
     pbar = p[conn].mean(axis=1)
     contrib = (vol * pbar)[:, None, None] * grad  # (E, 4, 3)
+    for a in range(4):
+        np.add.at(rhs, conn[:, a], contrib[:, a])
+    return rhs
+
+
+def _vreman_np(G, delta, c):
+    """kernel.py:99-143 (the minor form), vectorised over elements: G (E,3,3)
+    with G[e,k,i] = du_i/dx_k."""
+    a = G.reshape(-1, 9)
+    aa = (a * a).sum(axis=1)
+    g = G
+    d = np.stack([g[:, 0, 0] * g[:, 1, 1] - g[:, 0, 1] * g[:, 1, 0],
+                  g[:, 0, 0] * g[:, 2, 1] - g[:, 0, 1] * g[:, 2, 0],
+                  g[:, 1, 0] * g[:, 2, 1] - g[:, 1, 1] * g[:, 2, 0],
+                  g[:, 0, 0] * g[:, 1, 2] - g[:, 0, 2] * g[:, 1, 0],
+                  g[:, 0, 0] * g[:, 2, 2] - g[:, 0, 2] * g[:, 2, 0],
+                  g[:, 1, 0] * g[:, 2, 2] - g[:, 1, 2] * g[:, 2, 0],
+                  g[:, 0, 1] * g[:, 1, 2] - g[:, 0, 2] * g[:, 1, 1],
+                  g[:, 0, 1] * g[:, 2, 2] - g[:, 0, 2] * g[:, 2, 1],
+                  g[:, 1, 1] * g[:, 2, 2] - g[:, 1, 2] * g[:, 2, 1]], axis=1)
+    ssq = (d * d).sum(axis=1)
+    bb = delta ** 4 * ssq
+    nut = np.zeros_like(aa)
+    ok = (aa > 1e-30) & (bb >= 0.0)
+    nut[ok] = c * np.sqrt(bb[ok] / aa[ok])
+    return nut
+
+
+def supg_term(coords, conn, u, rho=1.0, mu=1e-3, cvre=0.07, c1=4.0, c2=2.0) -> np.ndarray:
+    """SUPG stabilisation of the convective residual (parity unpinned, see the
+    module header), from its weak form with the 4-point Gauss rule
+    (kernel.py:71-86):
+        r_a[i] -= sum_g w_g |det|/6 tau (rho u_g . grad N_a)(rho u_g . grad u_i),
+        tau = 1 / (c1 (mu + rho nu_t) / h^2 + c2 rho |u_mean| / h), h = cbrt(6 vol),
+    nu_t the reference's Vreman viscosity with filter width h."""
+    coords = np.asarray(coords, dtype=np.float64)
+    conn = np.asarray(conn, dtype=np.int64)
+    u = np.asarray(u, dtype=np.float64)
+    rhs = np.zeros((coords.shape[0], 3))
+    if conn.shape[0] == 0:
+        return rhs
+    x, ue = coords[conn], u[conn]                         # (E,4,3)
+    J = np.stack([x[:, 1] - x[:, 0], x[:, 2] - x[:, 0], x[:, 3] - x[:, 0]], axis=1)  # rows = edges
+    det = np.linalg.det(J)
+    vol = np.abs(det) / 6.0
+    dref = np.array([[-1.0, -1.0, -1.0], [1.0, 0, 0], [0, 1.0, 0], [0, 0, 1.0]])  # dN/dxi
+    grad = np.einsum("ekl,al->eak", np.linalg.inv(J), dref)  # (E,4,3): dN_a/dx_k
+    G = np.einsum("eak,eai->eki", grad, ue)              # du_i/dx_k
+    h = np.cbrt(6.0 * vol)
+    nut = _vreman_np(G, h, cvre)
+    vis = mu + rho * nut
+    umean = np.linalg.norm(ue.mean(axis=1), axis=1)
+    tau = 1.0 / (c1 * vis / h ** 2 + c2 * rho * umean / h)
+    qa, qb = (5.0 + 3.0 * math.sqrt(5.0)) / 20.0, (5.0 - math.sqrt(5.0)) / 20.0
+    P = np.full((4, 4), qb) + np.eye(4) * (qa - qb)         # N_b(x_g) = P[g, b]
+    ug = np.einsum("gb,ebi->egi", P, ue)                   # (E,4g,3)
+    adv_N = np.einsum("egk,eak->ega", ug, grad)            # u_g . grad N_a
+    adv_u = np.einsum("egk,eki->egi", ug, G)               # u_g . grad u_i
+    contrib = -(0.25 * vol * tau * rho * rho)[:, None, None] * np.einsum("ega,egi->eai", adv_N, adv_u)
     for a in range(4):
         np.add.at(rhs, conn[:, a], contrib[:, a])
     return rhs

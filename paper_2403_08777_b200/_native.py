@@ -92,6 +92,7 @@ SIGNATURES = [
     ("tal_buffers_get", _I, [_P, ctypes.POINTER(TalBuffers)]),
     ("tal_set_velocity_host", _I, [_P, _P, _P]),
     ("tal_set_pressure_host", _I, [_P, _P, _P]),
+    ("tal_set_stabilization", _I, [_P, _I, _D, _D]),
     ("tal_set_pressure_device", _I, [_P, _P, _P]),
     ("tal_set_velocity_device", _I, [_P, _P, _P]),
     ("tal_run", _I, [_P, ctypes.POINTER(TalParams), _I, _P, ctypes.POINTER(_I64)]),

@@ -417,6 +417,14 @@ class Assembler:
             raise ValueError("pressure contains non-finite entries")
         N.check(N.lib().tal_set_pressure_host(self._h, N.ptr(p), _stream(stream)))
 
+    def set_stabilization(self, enable: bool = True, c1: float = 4.0, c2: float = 2.0) -> None:
+        """SUPG stabilisation of the convective residual for every later
+        RSP-shape assembly on this handle (tal_set_stabilization; an
+        extension with no reference counterpart):
+        r_a[i] -= int tau (rho u.grad N_a)(rho u.grad u_i),
+        tau = 1 / (c1 (mu + rho nu_t) / h^2 + c2 rho |u_mean| / h)."""
+        N.check(N.lib().tal_set_stabilization(self._h, 1 if enable else 0, float(c1), float(c2)))
+
     def set_pressure_device(self, d_p_ptr: Optional[int], stream=None) -> None:
         N.check(N.lib().tal_set_pressure_device(
             self._h, None if d_p_ptr is None else ctypes.c_void_p(d_p_ptr), _stream(stream)))
@@ -596,20 +604,34 @@ def clear_cache() -> None:
         seam.close()
 
 
+def _stab_args(stabilization):
+    if stabilization is None or stabilization is False:
+        return None
+    if stabilization is True:
+        return (4.0, 2.0)
+    c1, c2 = stabilization
+    return float(c1), float(c2)
+
+
 def _assemble_variant(variant: VariantId, mesh, u, params: PhysParams,
-                      cfg: Optional[RunConfig], pressure: Optional[np.ndarray] = None) -> AssemblyResult:
+                      cfg: Optional[RunConfig], pressure: Optional[np.ndarray] = None,
+                      stabilization=None) -> AssemblyResult:
     cfg = as_run_config(cfg)
     u = validate_velocity(mesh, u)
     asm = _cached_assembler(mesh, cfg, variant)
     rhs = np.empty((asm.n_nodes, 3))
-    if pressure is None:
+    st = _stab_args(stabilization)
+    try:
+        if pressure is not None:
+            asm.set_pressure(pressure)
+        if st is not None:
+            asm.set_stabilization(True, *st)
         t = asm.assemble_into(u, params, rhs, cfg.scatter, variant=variant)
-    else:
-        asm.set_pressure(pressure)
-        try:
-            t = asm.assemble_into(u, params, rhs, cfg.scatter, variant=variant)
-        finally:
+    finally:
+        if pressure is not None:
             asm.set_pressure(None)
+        if st is not None:
+            asm.set_stabilization(False)
     wall = t.total_ms * 1e-3
     rate = asm.n_elems / wall if wall > 0.0 else 0.0
     return AssemblyResult(rhs=rhs, ledger=make_ledger(variant, cfg), wall_time=wall,
@@ -617,7 +639,8 @@ def _assemble_variant(variant: VariantId, mesh, u, params: PhysParams,
 
 
 def assemble_rsp(mesh, u: np.ndarray, params: PhysParams,
-                 cfg: Optional[RunConfig] = None, pressure: Optional[np.ndarray] = None) -> AssemblyResult:
+                 cfg: Optional[RunConfig] = None, pressure: Optional[np.ndarray] = None,
+                 stabilization=None) -> AssemblyResult:
     """Drop-in for ``tet_assembly_lab.assemble_rsp`` (variants.py:553-616).
 
     ``wall_time`` is the CUDA-event time of the call's device timeline
@@ -626,8 +649,11 @@ def assemble_rsp(mesh, u: np.ndarray, params: PhysParams,
     ``pressure`` (n_nodes,) adds the P1 pressure-gradient term
     ``int p dN_a/dx_i`` -- an extension with no reference counterpart
     (parity pinned only by this repo's oracle).
+    ``stabilization`` (True for c1=4, c2=2, or a (c1, c2) pair) adds the SUPG
+    term of the convective residual (Assembler.set_stabilization) -- also an
+    extension with no reference counterpart.
     """
-    return _assemble_variant(VariantId.RSP, mesh, u, params, cfg, pressure)
+    return _assemble_variant(VariantId.RSP, mesh, u, params, cfg, pressure, stabilization)
 
 
 def assemble_baseline(mesh, u: np.ndarray, params: PhysParams,

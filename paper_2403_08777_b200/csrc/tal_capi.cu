@@ -111,7 +111,10 @@ struct tal_handle {
     int32_t *d_blob_off = nullptr;
     int32_t *d_bnd_nodes = nullptr, *d_bnd_off = nullptr, *d_bnd_pos = nullptr;
     double *d_partial = nullptr;  // 3 * n_chunk_nodes
-    int priv_grid = 0, priv_grid_pr = 0, priv_cfg = 1;
+    int priv_cfg = 1;
+    int priv_grid_ext[4] = {0, 0, 0, 0};  // persistent grid per (pressure, SUPG) instance
+    bool has_st = false;                  // SUPG stabilisation (tal_set_stabilization)
+    double st_c1 = 4.0, st_c2 = 2.0;
     // optional nodal pressure (internal order) for the pressure-gradient term
     double *d_press = nullptr;
     bool has_press = false;
@@ -200,7 +203,7 @@ struct tal_handle {
         h_iperm.clear();
         ch = Chunking();
         n_interior = 0;
-        priv_grid = 0;
+        std::fill(priv_grid_ext, priv_grid_ext + 4, 0);
         has_mesh = false;
         info = tal_mesh_info{};
     }
@@ -267,6 +270,10 @@ bool make_consts(const tal_params *p, ElemConsts &kc, bool &sym)
     kc.a_4 = 4.0 * kc.a_po + kc.a_q;
     kc.rc6 = -kc.rc / 6.0;
     kc.mu6 = -p->mu / 6.0;
+    kc.st_po = po;
+    kc.st_dq = pd - po;
+    kc.st_c1 = 4.0;
+    kc.st_c2 = 2.0;
     return std::isfinite(p->rho) && std::isfinite(p->mu) && std::isfinite(p->c_vreman);
 }
 
@@ -287,31 +294,40 @@ int check_params(const tal_params *p)
     return TAL_OK;
 }
 
+template <int CFG, bool ORDERED>
+const void *private_fn(bool peer, bool pr, bool st)
+{
+    if (peer)  // the fused multi-GPU path: no SUPG instance (host-checked)
+        return pr ? (const void *)k_assemble_private<CFG, ORDERED, true, true>
+                  : (const void *)k_assemble_private<CFG, ORDERED, true>;
+    return st ? (pr ? (const void *)k_assemble_private<CFG, ORDERED, false, true, true>
+                    : (const void *)k_assemble_private<CFG, ORDERED, false, false, true>)
+              : (pr ? (const void *)k_assemble_private<CFG, ORDERED, false, true>
+                    : (const void *)k_assemble_private<CFG, ORDERED>);
+}
+
 template <int CFG>
-cudaError_t launch_private_cfg(bool ordered, unsigned grid, cudaStream_t s, PrivArgs pa, const double *nodes,
-                               RhsSoA rhs, ElemConsts kc, PeerArgs peer)
+cudaError_t launch_private_cfg(bool ordered, bool st, unsigned grid, cudaStream_t s, PrivArgs pa,
+                               const double *nodes, RhsSoA rhs, ElemConsts kc, PeerArgs peer)
 {
     const bool pr = pa.press != nullptr;
     const size_t sm = pr ? PrivLayoutOf<CFG, true>::TOTAL : PrivLayoutOf<CFG>::TOTAL;
     constexpr int T = PrivCfg<CFG>::THREADS;
     void *args[] = {(void *)&pa, (void *)&nodes, (void *)&rhs, (void *)&kc, (void *)&peer};
-    const void *fn = ordered   ? (pr ? (const void *)k_assemble_private<CFG, true, false, true>
-                                     : (const void *)k_assemble_private<CFG, true>)
-                     : peer.pidx ? (pr ? (const void *)k_assemble_private<CFG, false, true, true>
-                                       : (const void *)k_assemble_private<CFG, false, true>)
-                                 : (pr ? (const void *)k_assemble_private<CFG, false, false, true>
-                                       : (const void *)k_assemble_private<CFG, false>);
+    const bool peer_on = peer.pidx != nullptr && !ordered;
+    const void *fn =
+        ordered ? private_fn<CFG, true>(false, pr, st) : private_fn<CFG, false>(peer_on, pr, st);
     // plain launch of a persistent grid (occupancy x SMs); no grid-wide barrier
     // is used, so CTAs that cannot be resident yet simply start later
     return cudaLaunchKernel(fn, dim3(grid), dim3(T), args, sm, s);
 }
 
-cudaError_t launch_private(int cfg, bool ordered, unsigned grid, cudaStream_t s, const PrivArgs &pa,
+cudaError_t launch_private(int cfg, bool ordered, bool st, unsigned grid, cudaStream_t s, const PrivArgs &pa,
                            const double *nodes, RhsSoA rhs, const ElemConsts &kc, const PeerArgs &peer)
 {
-    return cfg == 0   ? launch_private_cfg<0>(ordered, grid, s, pa, nodes, rhs, kc, peer)
-           : cfg == 1 ? launch_private_cfg<1>(ordered, grid, s, pa, nodes, rhs, kc, peer)
-                      : launch_private_cfg<2>(ordered, grid, s, pa, nodes, rhs, kc, peer);
+    return cfg == 0   ? launch_private_cfg<0>(ordered, st, grid, s, pa, nodes, rhs, kc, peer)
+           : cfg == 1 ? launch_private_cfg<1>(ordered, st, grid, s, pa, nodes, rhs, kc, peer)
+                      : launch_private_cfg<2>(ordered, st, grid, s, pa, nodes, rhs, kc, peer);
 }
 
 struct ProfMark {
@@ -426,6 +442,15 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
     RhsSoA rhs{h->RX(), h->RY(), h->RZ()};
     int64_t nl = 0;
     const int64_t N = h->N, E = h->E;
+    const bool st = h->has_st;
+    if (st) {
+        if (!sym)
+            return fail(TAL_EINVAL, "the SUPG stabilisation needs the symmetric Gauss table (pmat = P^T P)");
+        if (h->n_peers())
+            return fail(TAL_EINVAL, "the SUPG stabilisation is not available on the fused multi-GPU path");
+        kc.st_c1 = h->st_c1;
+        kc.st_c2 = h->st_c2;
+    }
     // the fused interface sum lives in the private-atomic kernel's phase C
     // (and its signal/wait kernels): any other path would drop this rank's
     // interface sums and leave the neighbours waiting
@@ -441,7 +466,10 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             pm.begin();
             const double *pr = h->has_press ? h->d_press : nullptr;
             const unsigned g = grid_for(E, 256);
-            if (sym)
+            if (sym && st)
+                pr ? k_assemble_atomic<true, true, true><<<g, 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc, pr)
+                   : k_assemble_atomic<true, false, true><<<g, 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc, nullptr);
+            else if (sym)
                 pr ? k_assemble_atomic<true, true><<<g, 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc, pr)
                    : k_assemble_atomic<true><<<g, 256, 0, s>>>(h->conn, 0, E, nodes, rhs, kc, nullptr);
             else
@@ -466,7 +494,11 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
                 continue;
             const double *pr = h->has_press ? h->d_press : nullptr;
             const unsigned g = grid_for(e - b, 256);
-            if (sym)
+            if (sym && st)
+                pr ? k_assemble_colored<true, true, true><<<g, 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc, pr)
+                   : k_assemble_colored<true, false, true><<<g, 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc,
+                                                                             nullptr);
+            else if (sym)
                 pr ? k_assemble_colored<true, true><<<g, 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc, pr)
                    : k_assemble_colored<true><<<g, 256, 0, s>>>(h->conn_col, b, e, nodes, rhs, kc, nullptr);
             else
@@ -521,10 +553,10 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
             nl += 2;
         }
         if (h->info.n_chunks) {
-            const unsigned grid =
-                (unsigned)std::min<int64_t>(pa.press ? h->priv_grid_pr : h->priv_grid, h->info.n_chunks);
+            const int ext = (pa.press ? 1 : 0) | (st ? 2 : 0);
+            const unsigned grid = (unsigned)std::min<int64_t>(h->priv_grid_ext[ext], h->info.n_chunks);
             pm.begin();
-            const cudaError_t le = launch_private(h->priv_cfg, ordered, grid, s, pa, nodes, rhs, kc, peer);
+            const cudaError_t le = launch_private(h->priv_cfg, ordered, st, grid, s, pa, nodes, rhs, kc, peer);
             pm.end();
             if (le != cudaSuccess)
                 return fail(TAL_ECUDA, std::string("private kernel launch: ") + cudaGetErrorString(le));
@@ -546,9 +578,9 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         break;
     }
     case TAL_SCATTER_SEQUENTIAL: {
-        if (h->has_press)
+        if (h->has_press || st)
             return fail(TAL_EINVAL, "scatter 'sequential' reproduces the reference operator, which has no "
-                                    "pressure term; clear the pressure first");
+                                    "pressure or stabilisation term; switch them off first");
         if (N && !h->d_seq_off)
             if (int rc = build_sequential(h))
                 return rc;
@@ -671,41 +703,38 @@ int launch_any(tal_handle *h, const tal_params *p, int variant, int scatter, cud
     if (variant == TAL_VARIANT_RSP)
         return launch_run(h, p, scatter, s, launches);
     const bool shape = variant == TAL_VARIANT_B || variant == TAL_VARIANT_RS || variant == TAL_VARIANT_P;
-    if (h->has_press && shape)
-        return fail(TAL_EINVAL, "the pressure-gradient term is implemented for the RSP shape only");
+    if ((h->has_press || h->has_st) && shape)
+        return fail(TAL_EINVAL, "the pressure-gradient and SUPG terms are implemented for the RSP shape only");
     if (shape)
         return launch_shape(h, p, variant, scatter, s, launches);
     return fail(TAL_EINVAL, "unknown variant " + std::to_string(variant));
 }
 
 template <int CFG>
-int set_attrs_cfg(int device, int *grid_out, int *grid_pr_out)
+int set_attrs_cfg(int device, int grid_ext[4])
 {
     constexpr int sm = PrivLayoutOf<CFG>::TOTAL, sm_pr = PrivLayoutOf<CFG, true>::TOTAL;
-    const void *fns[] = {(const void *)k_assemble_private<CFG, true>,
-                         (const void *)k_assemble_private<CFG, false>,
-                         (const void *)k_assemble_private<CFG, false, true>};
-    const void *fns_pr[] = {(const void *)k_assemble_private<CFG, true, false, true>,
-                            (const void *)k_assemble_private<CFG, false, false, true>,
-                            (const void *)k_assemble_private<CFG, false, true, true>};
-    for (const void *f : fns)
-        TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    for (const void *f : fns_pr)
-        TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_pr));
-    int per_sm = 0, per_sm_pr = 0, n_sm = 0;
-    TAL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[1], PrivCfg<CFG>::THREADS, sm));
-    TAL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_pr, fns_pr[1], PrivCfg<CFG>::THREADS, sm_pr));
+    int n_sm = 0;
     TAL_CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
-    *grid_out = std::max(1, per_sm) * n_sm;
-    *grid_pr_out = std::max(1, per_sm_pr) * n_sm;
+    for (int ext = 0; ext < 4; ++ext) {
+        const bool pr = ext & 1, st = ext & 2;
+        const int bytes = pr ? sm_pr : sm;
+        const void *fns[] = {private_fn<CFG, true>(false, pr, st), private_fn<CFG, false>(false, pr, st),
+                             private_fn<CFG, false>(true, pr, false)};
+        for (const void *f : fns)
+            TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        int per_sm = 0;
+        TAL_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[1], PrivCfg<CFG>::THREADS, bytes));
+        grid_ext[ext] = std::max(1, per_sm) * n_sm;
+    }
     return TAL_OK;
 }
 
-int set_kernel_attrs(int device, int cfg, int *grid_out, int *grid_pr_out)
+int set_kernel_attrs(int device, int cfg, int grid_ext[4])
 {
-    return cfg == 0   ? set_attrs_cfg<0>(device, grid_out, grid_pr_out)
-           : cfg == 1 ? set_attrs_cfg<1>(device, grid_out, grid_pr_out)
-                      : set_attrs_cfg<2>(device, grid_out, grid_pr_out);
+    return cfg == 0   ? set_attrs_cfg<0>(device, grid_ext)
+           : cfg == 1 ? set_attrs_cfg<1>(device, grid_ext)
+                      : set_attrs_cfg<2>(device, grid_ext);
 }
 
 // cta_patches -> CTA configuration (PrivCfg in tal_kernels.cuh)
@@ -1291,7 +1320,7 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
         TAL_CK(cudaMalloc((void **)&h->d_partial, sizeof(double) * 3 * C.cnodes.size()));
     bytes += blobs.size() + blob_off.size() * 4 + C.cnodes.size() * 24 +
              (C.bnd_nodes.size() + C.bnd_off.size() + C.bnd_pos.size()) * 4;
-    if ((rc = set_kernel_attrs(h->device, h->priv_cfg, &h->priv_grid, &h->priv_grid_pr)))
+    if ((rc = set_kernel_attrs(h->device, h->priv_cfg, h->priv_grid_ext)))
         return rc;
     TAL_CK(cudaDeviceSynchronize());
 
@@ -1457,6 +1486,24 @@ int tal_set_pressure_device(tal_handle *h, const double *d_p, void *stream)
         TAL_CK_LAUNCH();
     }
     h->has_press = true;
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_set_stabilization(tal_handle *h, int enable, double c1, double c2)
+{
+    TAL_GUARD_BEGIN
+    if (!h)
+        return fail(TAL_EINVAL, "handle is NULL");
+    if (enable && !(c1 > 0.0 && std::isfinite(c1) && c2 >= 0.0 && std::isfinite(c2)))
+        return fail(TAL_EINVAL, "SUPG constants need c1 > 0 and c2 >= 0 (finite)");
+    h->has_st = enable != 0;
+    if (enable)
+        h->st_c1 = c1, h->st_c2 = c2;
+    if (h->gexec) {  // a captured step no longer matches the handle state: capture again
+        cudaGraphExecDestroy(h->gexec);
+        h->gexec = nullptr;
+    }
     return TAL_OK;
     TAL_GUARD_END
 }

@@ -44,6 +44,11 @@ struct ElemConsts {
     double rc6;   // -rho * c_vreman / 6
     double mu6;   // -mu / 6
     double pm[16];  // full pmat (general kernel only)
+    // SUPG stabilisation (ST instances; tal_set_stabilization):
+    // tau = 1 / (st_c1 vis / h^2 + st_c2 rho |u_mean| / h), h = cbrt(|D|);
+    // the symmetric table's off-diagonal po and pd - po for the Gauss-point
+    // velocity second moments
+    double st_c1, st_c2, st_po, st_dq;
 };
 
 __device__ __forceinline__ void cross3(const double a[3], const double b[3], double c[3])
@@ -133,9 +138,53 @@ __device__ __forceinline__ void pressure_add(double pbar, double det, const doub
 // folds its running sums into them instead of separate adds).  With NEG3 the
 // c3 argument holds -c3 (the ring kernel carries c2 of the previous tet; the
 // negation becomes a free operand modifier instead of three DADDs).
+// Optional SUPG stabilisation of the convective residual (SURVEY.md section
+// 8 f4; no reference counterpart, parity pinned by this repo's own oracle):
+//   r_a[i] += -int tau (rho u.grad N_a) (rho u.grad u_i)
+//           = -tau rho^2 / (24 |D|) * c_a . (M Gh)[:, i],
+// M = sum_g u_g u_g^T = sum_bc pmat[b][c] u_b u_c^T (exact for P1 u with the
+// degree-2 Gauss rule), tau = 1 / (c1 vis / h^2 + c2 rho |S/4| / h),
+// 1/h = r3 = |D|^(-1/3) (the Vreman filter width), vis = mu + rho nu_t.
+// The viscous part of the strong residual vanishes for P1; the pressure part
+// is not included.  ~110 FP64 instructions.
+__device__ __forceinline__ void supg_add(const double c1[3], const double c2[3], const double c3[3],
+                                         const double Gh[3][3], const double U0[3], const double U1[3],
+                                         const double U2[3], const double U3[3], const double S[3], double r3,
+                                         double inv, double vis, const ElemConsts &k, double R[4][3])
+{
+    const double un = sqrt(fma(S[0], S[0], fma(S[1], S[1], S[2] * S[2])));
+    const double tau = 1.0 / fma(k.st_c1 * vis, r3 * r3, k.st_c2 * k.rho * (0.25 * un) * r3);
+    const double coef = -tau * (k.rho * k.rho) * inv * (1.0 / 24.0);
+    double M[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = a; b < 3; ++b) {
+            const double q = fma(U0[a], U0[b], fma(U1[a], U1[b], fma(U2[a], U2[b], U3[a] * U3[b])));
+            M[a][b] = fma(k.st_po, S[a] * S[b], k.st_dq * q);
+            M[b][a] = M[a][b];
+        }
+    double MG[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            MG[a][i] = coef * fma(M[a][0], Gh[0][i], fma(M[a][1], Gh[1][i], M[a][2] * Gh[2][i]));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double t1 = fma(c1[0], MG[0][i], fma(c1[1], MG[1][i], c1[2] * MG[2][i]));
+        const double t2 = fma(c2[0], MG[0][i], fma(c2[1], MG[1][i], c2[2] * MG[2][i]));
+        const double t3 = fma(c3[0], MG[0][i], fma(c3[1], MG[1][i], c3[2] * MG[2][i]));
+        R[1][i] += t1;
+        R[2][i] += t2;
+        R[3][i] += t3;
+        R[0][i] -= (t1 + t2) + t3;
+    }
+}
+
 // POS: the caller guarantees det > 0 (patches oriented on the host), so
-// |det| = det and the sign folds vanish.
-template <bool ACC, bool NEG3 = false, bool POS = false>
+// |det| = det and the sign folds vanish.  ST: add the SUPG term (supg_add).
+template <bool ACC, bool NEG3 = false, bool POS = false, bool ST = false>
 __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3], const double c3[3],
                                          double det, const double du1[3], const double du2[3],
                                          const double du3[3], const double U0[3], const double U1[3],
@@ -201,10 +250,19 @@ __device__ __forceinline__ void tet_tail(const double c1[3], const double c2[3],
             const double last = ACC ? fma(w[a][2], Gh[2][i], R[a][i]) : w[a][2] * Gh[2][i];
             R[a][i] = fma(w[a][0], Gh[0][i], fma(w[a][1], Gh[1][i], last));
         }
+    if constexpr (ST) {
+        double Sv[3];
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+            Sv[cc] = S01[cc] + (U2[cc] + U3[cc]);
+        const double vis = fma(-6.0 * f, ssqh, k.mu);  // f ssqh = -rho nu_t / 6
+        supg_add(c1, c2, c3v, Gh, U0, U1, U2, U3, Sv, r3, inv, vis, k, R);
+    }
 }
 
 // Symmetric-rule element (pmat = po * ones + (pd - po) * I); p4 = nodal
-// pressures or nullptr.
+// pressures or nullptr; ST: with the SUPG term.
+template <bool ST = false>
 __device__ __forceinline__ void element_rhs_sym(const double X[4][3], const double U[4][3],
                                                 const double *p4, const ElemConsts &k, double R[4][3])
 {
@@ -221,7 +279,7 @@ __device__ __forceinline__ void element_rhs_sym(const double X[4][3], const doub
     cross3(e[0], e[1], c3);  // e1 x e2
     const double det = fma(e[0][0], c1[0], fma(e[0][1], c1[1], e[0][2] * c1[2]));
     const double S01[3] = {U[0][0] + U[1][0], U[0][1] + U[1][1], U[0][2] + U[1][2]};
-    tet_tail<false>(c1, c2, c3, det, du[0], du[1], du[2], U[0], U[1], S01, U[2], U[3], k, R);
+    tet_tail<false, false, false, ST>(c1, c2, c3, det, du[0], du[1], du[2], U[0], U[1], S01, U[2], U[3], k, R);
     if (p4)
         pressure_add(0.25 * ((p4[0] + p4[1]) + (p4[2] + p4[3])), det, c1, c2, c3, R);
 }
@@ -309,14 +367,14 @@ __device__ __forceinline__ void element_rhs_gen(const double X[4][3], const doub
         pressure_add(0.25 * ((p4[0] + p4[1]) + (p4[2] + p4[3])), det, cf[1], cf[2], cf[3], R);
 }
 
-template <bool SYM>
+template <bool SYM, bool ST = false>
 __device__ __forceinline__ void element_rhs(const double X[4][3], const double U[4][3],
                                             const double *p4, const ElemConsts &k, double R[4][3])
 {
     if constexpr (SYM)
-        element_rhs_sym(X, U, p4, k, R);
+        element_rhs_sym<ST>(X, U, p4, k, R);
     else
-        element_rhs_gen(X, U, p4, k, R);
+        element_rhs_gen(X, U, p4, k, R);  // SUPG needs the symmetric rule (host-checked)
 }
 
 }  // namespace tal

@@ -117,7 +117,7 @@ __device__ __forceinline__ void load_record_s(const double *rec, int v, double X
 // ---------------------------------------------------------------------------
 // (1) one thread per element, 12 FP64 REDs (scatter = atomic)
 // ---------------------------------------------------------------------------
-template <bool SYM, bool PR = false>
+template <bool SYM, bool PR = false, bool ST = false>
 __global__ void __launch_bounds__(256) k_assemble_atomic(const int4 *__restrict__ conn,
                                                          int64_t e_begin, int64_t e_end,
                                                          const double *__restrict__ nrec, RhsSoA rhs,
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) k_assemble_atomic(const int4 *__restrict_
         if (PR)
             p4[a] = __ldg(press + ids[a]);
     }
-    element_rhs<SYM>(X, U, PR ? p4 : nullptr, kc, R);
+    element_rhs<SYM, ST>(X, U, PR ? p4 : nullptr, kc, R);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         atomicAdd(rhs.rx + ids[a], R[a][0]);
@@ -184,7 +184,7 @@ __global__ void k_remap_conn(int4 *c, int64_t k, const int32_t *__restrict__ ipe
 // ---------------------------------------------------------------------------
 // (2) one colour class per launch, plain read-modify-write (scatter = colored)
 // ---------------------------------------------------------------------------
-template <bool SYM, bool PR = false>
+template <bool SYM, bool PR = false, bool ST = false>
 __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict__ conn,
                                                           int64_t e_begin, int64_t e_end,
                                                           const double *__restrict__ nrec, RhsSoA rhs,
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256) k_assemble_colored(const int4 *__restrict
         if (PR)
             p4[a] = __ldg(press + ids[a]);
     }
-    element_rhs<SYM>(X, U, PR ? p4 : nullptr, kc, R);
+    element_rhs<SYM, ST>(X, U, PR ? p4 : nullptr, kc, R);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         rhs.rx[ids[a]] += R[a][0];
@@ -318,8 +318,9 @@ struct PrivArgs {
 // PR: with the optional pressure-gradient term (tal_element.cuh pressure_add);
 // the nodal pressures are gathered next to the records (2 KB more shared
 // memory per CTA: 3 CTAs/SM instead of 4).
-template <int CFG, bool ORDERED, bool PEER = false, bool PR = false>
-__global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MINB * 3 + 3) / 4 : PrivCfg<CFG>::MINB)
+template <int CFG, bool ORDERED, bool PEER = false, bool PR = false, bool ST = false>
+__global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
+                                  (PR || ST) ? (PrivCfg<CFG>::MINB * 3 + 3) / 4 : PrivCfg<CFG>::MINB)
     k_assemble_private(PrivArgs pa, const double *__restrict__ nrec_g, RhsSoA rhs, ElemConsts kc,
                        PeerArgs peer)
 {
@@ -477,7 +478,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS, PR ? (PrivCfg<CFG>::MIN
                 cross3(e2, e3, c1);
                 cross3(e3, e1, c2);
                 const double det = fma(e1[0], c1[0], fma(e1[1], c1[1], e1[2] * c1[2]));
-                tet_tail<true, true, TAL_ORIENT != 0>(c1, c2, nc3, det, du1, du2, du3, Ua, Ub, S01, U2, U3, kc, R);
+                tet_tail<true, true, TAL_ORIENT != 0, ST>(c1, c2, nc3, det, du1, du2, du3, Ua, Ub, S01, U2, U3, kc, R);
                 if (PR) {
                     const double p3 = pres_s[ID(3 + nxt)];
                     const double c3[3] = {-nc3[0], -nc3[1], -nc3[2]};

@@ -439,7 +439,10 @@ void rcb_parts(const double *pts, int64_t n, int world, int32_t *part)
     };
     std::vector<int64_t> all((size_t)n);
     std::iota(all.begin(), all.end(), 0);
-    std::vector<Task> level{{std::move(all), 0, world}};
+    std::vector<Task> level(1);
+    level[0].idx.swap(all);
+    level[0].first = 0;
+    level[0].k = world;
     while (!level.empty()) {
         std::vector<Task> next_level((size_t)2 * level.size());
         std::vector<uint8_t> used(next_level.size(), 0);
