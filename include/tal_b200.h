@@ -236,6 +236,14 @@ int tal_graph_destroy(tal_handle *h);
  * scatter 'sequential', the B/RS shapes or the fused multi-GPU path
  * (TAL_EINVAL).  A captured graph (tal_graph_capture) is dropped. */
 int tal_set_stabilization(tal_handle *h, int enable, double c1, double c2);
+/* One assembly straight from and to the caller's device arrays d_u, d_rhs
+ * ((N,3) AoS doubles in the caller's node numbering), no internal layout
+ * conversion: the private kernel gathers u from d_u and writes the sums to
+ * d_rhs (scatter 'private' / 'private-atomic', symmetric rule, no pressure /
+ * SUPG / peers); otherwise the composition set_velocity_device -> run ->
+ * get_rhs_device.  Asynchronous on 'stream'. */
+int tal_run_caller(tal_handle *h, const tal_params *p, int scatter, const double *d_u, double *d_rhs,
+                   void *stream, int64_t *kernel_launches);
 /* tal_get_rhs_host blocks until rhs (caller order, (N,3) AoS) is complete. */
 int tal_get_rhs_host(tal_handle *h, double *rhs, void *stream);
 int tal_get_rhs_device(tal_handle *h, double *d_rhs, void *stream);

@@ -96,6 +96,7 @@ SIGNATURES = [
     ("tal_set_pressure_device", _I, [_P, _P, _P]),
     ("tal_set_velocity_device", _I, [_P, _P, _P]),
     ("tal_run", _I, [_P, ctypes.POINTER(TalParams), _I, _P, ctypes.POINTER(_I64)]),
+    ("tal_run_caller", _I, [_P, ctypes.POINTER(TalParams), _I, _P, _P, _P, ctypes.POINTER(_I64)]),
     ("tal_graph_capture", _I, [_P, ctypes.POINTER(TalParams), _I, _I]),
     ("tal_graph_launch", _I, [_P, _P, ctypes.POINTER(_I64)]),
     ("tal_graph_destroy", _I, [_P]),

@@ -451,6 +451,21 @@ class Assembler:
                                         _stream(stream), ctypes.byref(nl)))
         return int(nl.value)
 
+    def run_caller(self, params: PhysParams, d_u_ptr: int, d_rhs_ptr: int,
+                   scatter: Optional[str] = None, stream=None) -> int:
+        """One assembly from and to the caller's own device arrays ((N,3)
+        float64 in its node numbering; tal_run_caller): the private kernel
+        gathers u from d_u and writes d_rhs directly -- no pack/unpack
+        kernels.  Returns kernels launched (asynchronous on ``stream``)."""
+        scatter = scatter or self.cfg.scatter
+        if scatter not in N.SCATTER:
+            raise ValueError(f"unknown scatter mode {scatter!r}")
+        nl = ctypes.c_int64(0)
+        N.check(N.lib().tal_run_caller(self._h, ctypes.byref(_params(params)), N.SCATTER[scatter],
+                                       ctypes.c_void_p(d_u_ptr), ctypes.c_void_p(d_rhs_ptr),
+                                       _stream(stream), ctypes.byref(nl)))
+        return int(nl.value)
+
     def capture(self, params: PhysParams, scatter: Optional[str] = None, pmat=None,
                 variant: VariantId = VariantId.RSP) -> None:
         """Capture one assembly step (zeroing + kernels + merge) as a CUDA

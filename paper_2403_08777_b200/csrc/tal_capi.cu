@@ -110,6 +110,7 @@ struct tal_handle {
     uint8_t *d_blobs = nullptr;
     int32_t *d_blob_off = nullptr;
     int32_t *d_bnd_nodes = nullptr, *d_bnd_off = nullptr, *d_bnd_pos = nullptr;
+    int32_t *d_cg = nullptr, *d_cc = nullptr;  // caller ids of the chunk-node entries (tal_run_caller)
     double *d_partial = nullptr;  // 3 * n_chunk_nodes
     int priv_cfg = 1;
     int priv_grid_ext[4] = {0, 0, 0, 0};  // persistent grid per (pressure, SUPG) instance
@@ -177,7 +178,8 @@ struct tal_handle {
         free_graph();
         free_peers();
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
-                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press, d_seq_off, d_seq_ent, d_seq_dlt, d_seq_rows};
+                        d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press, d_seq_off, d_seq_ent, d_seq_dlt, d_seq_rows,
+                        d_cg, d_cc};
         for (void *p : ptrs)
             if (p)
                 cudaFree(p);
@@ -197,6 +199,7 @@ struct tal_handle {
         }
         async_next = 0;
         perm = iperm = d_blob_off = d_bnd_nodes = d_bnd_off = d_bnd_pos = nullptr;
+        d_cg = d_cc = nullptr;
         conn = conn_col = nullptr;
         d_blobs = nullptr;
         col_off.clear();
@@ -295,8 +298,10 @@ int check_params(const tal_params *p)
 }
 
 template <int CFG, bool ORDERED>
-const void *private_fn(bool peer, bool pr, bool st)
+const void *private_fn(bool peer, bool pr, bool st, bool cl = false)
 {
+    if (cl)  // caller layout: the plain step only (no peers, pressure, SUPG)
+        return (const void *)k_assemble_private<CFG, ORDERED, false, false, false, true>;
     if (peer)  // the fused multi-GPU path: no SUPG instance (host-checked)
         return pr ? (const void *)k_assemble_private<CFG, ORDERED, true, true>
                   : (const void *)k_assemble_private<CFG, ORDERED, true>;
@@ -311,12 +316,13 @@ cudaError_t launch_private_cfg(bool ordered, bool st, unsigned grid, cudaStream_
                                const double *nodes, RhsSoA rhs, ElemConsts kc, PeerArgs peer)
 {
     const bool pr = pa.press != nullptr;
+    const bool cl = pa.rhs_caller != nullptr;
     const size_t sm = pr ? PrivLayoutOf<CFG, true>::TOTAL : PrivLayoutOf<CFG>::TOTAL;
     constexpr int T = PrivCfg<CFG>::THREADS;
     void *args[] = {(void *)&pa, (void *)&nodes, (void *)&rhs, (void *)&kc, (void *)&peer};
     const bool peer_on = peer.pidx != nullptr && !ordered;
     const void *fn =
-        ordered ? private_fn<CFG, true>(false, pr, st) : private_fn<CFG, false>(peer_on, pr, st);
+        ordered ? private_fn<CFG, true>(false, pr, st, cl) : private_fn<CFG, false>(peer_on, pr, st, cl);
     // plain launch of a persistent grid (occupancy x SMs); no grid-wide barrier
     // is used, so CTAs that cannot be resident yet simply start later
     return cudaLaunchKernel(fn, dim3(grid), dim3(T), args, sm, s);
@@ -698,6 +704,90 @@ int launch_shape(tal_handle *h, const tal_params *p, int variant, int scatter, c
     return TAL_OK;
 }
 
+// caller ids of the chunk-node entries (gather order, rank order), built on
+// first use from the host chunk tables and the node permutation
+int build_caller_ids(tal_handle *h)
+{
+    if (h->d_cg || h->ch.gather_nodes.empty())
+        return TAL_OK;
+    const int64_t n = (int64_t)h->ch.gather_nodes.size();
+    std::vector<int32_t> perm;
+    if (!h->h_iperm.empty()) {
+        perm.resize((size_t)h->N);
+        for (int64_t c = 0; c < h->N; ++c)
+            perm[h->h_iperm[c]] = (int32_t)c;
+    }
+    std::vector<int32_t> cg((size_t)n), cc((size_t)n);
+    parallel_for(n, [&](int64_t i0, int64_t i1, int) {
+        for (int64_t i = i0; i < i1; ++i) {
+            const int32_t g = h->ch.gather_nodes[i], c = h->ch.cnodes[i] & 0x7fffffff;
+            cg[i] = perm.empty() ? g : perm[g];
+            cc[i] = perm.empty() ? c : perm[c];
+        }
+    });
+    if (int rc = dev_upload(&h->d_cg, cg.data(), cg.size()))
+        return rc;
+    return dev_upload(&h->d_cc, cc.data(), cc.size());
+}
+
+// One assembly from and to the caller's device arrays: the fused caller-layout
+// private kernel when it applies (symmetric rule, private / private-atomic,
+// no pressure / SUPG / peers), else the composition set_velocity_device ->
+// run -> get_rhs_device.
+int launch_caller(tal_handle *h, const tal_params *p, int scatter, const double *d_u, double *d_rhs,
+                  cudaStream_t s, int64_t *launches)
+{
+    ElemConsts kc;
+    bool sym;
+    if (!make_consts(p, kc, sym))
+        return fail(TAL_EINVAL, "non-finite physical parameters");
+    const bool fused = sym && !h->has_press && !h->has_st && !h->n_peers() && h->info.n_chunks > 0 &&
+                       (scatter == TAL_SCATTER_PRIVATE || scatter == TAL_SCATTER_PRIVATE_ATOMIC);
+    if (!fused) {
+        if (h->N) {
+            k_pack_velocity<<<grid_for(h->N, 256), 256, 0, s>>>(d_u, h->perm, h->N, h->REC());
+            TAL_CK_LAUNCH();
+        }
+        int64_t nl = 0;
+        if (int rc = launch_run(h, p, scatter, s, &nl))
+            return rc;
+        if (h->N) {
+            k_unpack_aos<<<grid_for(h->N, 256), 256, 0, s>>>(h->RX(), h->RY(), h->RZ(), h->iperm, h->N, d_rhs);
+            TAL_CK_LAUNCH();
+        }
+        if (launches)
+            *launches = nl + (h->N ? 2 : 0);
+        return TAL_OK;
+    }
+    if (int rc = build_caller_ids(h))
+        return rc;
+    const bool ordered = scatter == TAL_SCATTER_PRIVATE;
+    ProfMark pm{h, s};
+    int64_t nl = 0;
+    if (!ordered)  // shared nodes are REDed into it: zero the caller's rhs first
+        TAL_CK(cudaMemsetAsync(d_rhs, 0, sizeof(double) * 3 * h->N, s));
+    PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, ordered ? h->d_partial : nullptr, nullptr,
+                h->d_cg, h->d_cc, d_u, d_rhs};
+    RhsSoA rhs{h->RX(), h->RY(), h->RZ()};
+    const unsigned grid = (unsigned)std::min<int64_t>(h->priv_grid_ext[0], h->info.n_chunks);
+    pm.begin();
+    const cudaError_t le = launch_private(h->priv_cfg, ordered, false, grid, s, pa, h->REC(), rhs, kc, PeerArgs{});
+    pm.end();
+    if (le != cudaSuccess)
+        return fail(TAL_ECUDA, std::string("private kernel launch: ") + cudaGetErrorString(le));
+    ++nl;
+    const int64_t nb = (int64_t)h->ch.bnd_nodes.size();
+    if (ordered && nb) {
+        k_merge_partials<<<grid_for(nb, 256), 256, 0, s>>>(h->d_bnd_nodes, h->d_bnd_off, h->d_bnd_pos, nb,
+                                                          h->d_partial, rhs, d_rhs, h->perm);
+        TAL_CK_LAUNCH();
+        ++nl;
+    }
+    if (launches)
+        *launches = nl;
+    return TAL_OK;
+}
+
 int launch_any(tal_handle *h, const tal_params *p, int variant, int scatter, cudaStream_t s, int64_t *launches)
 {
     if (variant == TAL_VARIANT_RSP)
@@ -720,7 +810,8 @@ int set_attrs_cfg(int device, int grid_ext[4])
         const bool pr = ext & 1, st = ext & 2;
         const int bytes = pr ? sm_pr : sm;
         const void *fns[] = {private_fn<CFG, true>(false, pr, st), private_fn<CFG, false>(false, pr, st),
-                             private_fn<CFG, false>(true, pr, false)};
+                             private_fn<CFG, false>(true, pr, false), private_fn<CFG, true>(false, pr, st, true),
+                             private_fn<CFG, false>(false, pr, st, true)};
         for (const void *f : fns)
             TAL_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         int per_sm = 0;
@@ -1640,6 +1731,25 @@ int tal_graph_destroy(tal_handle *h)
     DeviceGuard g(h->device);
     h->free_graph();
     return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_run_caller(tal_handle *h, const tal_params *p, int scatter, const double *d_u, double *d_rhs, void *stream,
+                   int64_t *kernel_launches)
+{
+    TAL_GUARD_BEGIN
+    if (!h || ((!d_u || !d_rhs) && h->N))
+        return fail(TAL_EINVAL, "NULL argument");
+    if (!h->has_mesh)
+        return fail(TAL_ESTATE, "no mesh uploaded");
+    if (int rc = check_params(p))
+        return rc;
+    DeviceGuard g(h->device);
+    int64_t nl = 0;
+    const int rc = launch_caller(h, p, scatter, d_u, d_rhs, stream ? (cudaStream_t)stream : h->stream, &nl);
+    if (kernel_launches)
+        *kernel_launches = nl;
+    return rc;
     TAL_GUARD_END
 }
 

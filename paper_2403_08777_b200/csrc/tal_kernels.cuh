@@ -313,12 +313,22 @@ struct PrivArgs {
     int n_chunks;
     double *part;          // ordered-merge partials, AoS (x,y,z) per chunk-node entry node_begin + j
     const double *press;   // nodal pressures, internal order (PR instances)
+    // caller layout (CL instances): u and rhs are the caller's (N,3) AoS
+    // arrays in its own node numbering; caller ids of the chunk-node entries
+    // in gather order (cg) and in rank order (cc), indexed node_begin + j
+    const int32_t *__restrict__ cg;
+    const int32_t *__restrict__ cc;
+    const double *__restrict__ u_caller;
+    double *rhs_caller;
 };
 
 // PR: with the optional pressure-gradient term (tal_element.cuh pressure_add);
 // the nodal pressures are gathered next to the records (2 KB more shared
 // memory per CTA: 3 CTAs/SM instead of 4).
-template <int CFG, bool ORDERED, bool PEER = false, bool PR = false, bool ST = false>
+// CL: caller layout -- velocities gathered straight from the caller's (N,3)
+// array (coordinates still from the resident records) and sums written
+// straight to the caller's (N,3) rhs: no pack / unpack kernels per step.
+template <int CFG, bool ORDERED, bool PEER = false, bool PR = false, bool ST = false, bool CL = false>
 __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
                                   (PR || ST) ? (PrivCfg<CFG>::MINB * 3 + 3) / 4 : PrivCfg<CFG>::MINB)
     k_assemble_private(PrivArgs pa, const double *__restrict__ nrec_g, RhsSoA rhs, ElemConsts kc,
@@ -352,6 +362,25 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);
         const int32_t *gl = reinterpret_cast<const int32_t *>(bl + 16 + L::TABLES + 2 * BLOB_LEVELS);
         double *dst = nrec_s;
+        if constexpr (CL) {
+            // x,y (16 B) + z (8 B) of the resident record, then the caller's
+            // u as three 8-B copies (a (N,3) row is only 8-B aligned)
+            for (int q = tid; q < 2 * hdr.y; q += T) {
+                const int j = q >> 1;
+                const double *src = nrec_g + 6 * (int64_t)gl[j];
+                if (q & 1)
+                    cp_async8(dst + 6 * j + 2, src + 2);
+                else
+                    cp_async16(dst + 6 * j, src);
+            }
+            const int32_t *cg = pa.cg + hdr.z;
+            for (int q = tid; q < 3 * hdr.y; q += T) {
+                const int j = q / 3, c = q - 3 * j;
+                cp_async8(dst + 6 * j + 3 + c, pa.u_caller + 3 * (int64_t)__ldg(cg + j) + c);
+            }
+            cp_async_commit();
+            return;
+        }
 #if TAL_GATHER_COOP
         // 16-B segment per lane, lane-consecutive segments: a warp's copies
         // cover ~11 contiguous records (fewer L1 sectors / smem wavefronts
@@ -542,6 +571,24 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
             }
             const int raw = cn[q];
             const int v = raw & 0x7fffffff;
+            if constexpr (CL) {
+                double *r = pa.rhs_caller + 3 * (int64_t)__ldg(pa.cc + hdr.z + q);
+                if (raw < 0) {
+                    r[0] = ax;
+                    r[1] = ay;
+                    r[2] = az;
+                } else if (ORDERED) {
+                    double *d = pa.part + 3 * (int64_t)(hdr.z + q);
+                    d[0] = ax;
+                    d[1] = ay;
+                    d[2] = az;
+                } else {
+                    atomicAdd(r + 0, ax);
+                    atomicAdd(r + 1, ay);
+                    atomicAdd(r + 2, az);
+                }
+                continue;
+            }
             if (raw < 0) {  // interior: the complete sum
                 rhs.rx[v] = ax;
                 rhs.ry[v] = ay;
@@ -572,11 +619,13 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
 
 // ordered merge of chunk partials for nodes shared between chunks (and zero
 // for nodes without elements): rhs[v] = sum over its chunks in chunk order
+// (caller_out: write the caller's (N,3) rhs at perm[v] instead of the SoA)
 __global__ void __launch_bounds__(256) k_merge_partials(const int32_t *__restrict__ bnd_nodes,
                                                         const int32_t *__restrict__ bnd_off,
                                                         const int32_t *__restrict__ bnd_pos,
                                                         int64_t n_bnd, const double *__restrict__ part,
-                                                        RhsSoA rhs)
+                                                        RhsSoA rhs, double *caller_out = nullptr,
+                                                        const int32_t *__restrict__ perm = nullptr)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_bnd)
@@ -608,6 +657,13 @@ __global__ void __launch_bounds__(256) k_merge_partials(const int32_t *__restric
             }
     }
     const int v = bnd_nodes[i];
+    if (caller_out) {
+        double *r = caller_out + 3 * (int64_t)(perm ? perm[v] : v);
+        r[0] = ax;
+        r[1] = ay;
+        r[2] = az;
+        return;
+    }
     rhs.rx[v] = ax;
     rhs.ry[v] = ay;
     rhs.rz[v] = az;

@@ -585,3 +585,34 @@ def test_stateless_seam_entry_sees_changed_arrays(oracle):
     c = call()
     assert not np.allclose(a, c)
     del ctypes
+
+
+@pytest.mark.parametrize("renumber", ["rcm", "sfc", "none"])
+@pytest.mark.parametrize("permuted", [False, True])
+def test_run_caller_fused_layout(oracle, renumber, permuted):
+    """tal_run_caller: u read from / rhs written to the caller's own (N,3)
+    device arrays by the private kernel (no pack/unpack).  'private' is
+    bitwise the internal-layout result; every mode matches the oracle."""
+    import torch
+    g = tb.generate_box_mesh(10, 9, 8)
+    m = tb.permute_nodes(g, np.random.default_rng(5).permutation(g.n_nodes)) if permuted else g
+    u = tb.make_velocity(m, "random:9")
+    ref = oracle.assemble_rsp(m.coords, m.connectivity, u)
+    asm = tb.Assembler(m, tb.RunConfig(renumber=renumber), build_colors=True)
+    d_u = torch.as_tensor(u, device="cuda:0").contiguous()
+    for scatter in ("private", "private-atomic", "atomic", "colored"):
+        d_r = torch.full_like(d_u, float("nan"))
+        nl = asm.run_caller(P, d_u.data_ptr(), d_r.data_ptr(), scatter=scatter, stream=0)
+        torch.cuda.synchronize()
+        got = d_r.cpu().numpy()
+        assert_parity(oracle, got, ref, m, u)
+        if scatter == "private":
+            host, _ = asm.assemble(u, P, scatter="private")
+            np.testing.assert_array_equal(got, host)
+            assert nl <= 2  # kernel (+ ordered merge): no pack/unpack
+    asm.set_pressure(np.zeros(m.n_nodes))  # not fused: the composition path, same numbers
+    d_r = torch.empty_like(d_u)
+    asm.run_caller(P, d_u.data_ptr(), d_r.data_ptr(), scatter="private", stream=0)
+    torch.cuda.synchronize()
+    assert_parity(oracle, d_r.cpu().numpy(), ref, m, u)
+    asm.close()
