@@ -134,6 +134,10 @@ int tal_destroy(tal_handle *h);
 /* pinned host memory for copy-overlapped end-to-end use */
 int tal_host_alloc(int64_t bytes, void **out);
 int tal_host_free(void *p);
+/* page-lock / release an existing host buffer (cudaHostRegister): the seam
+ * and the host round trips then DMA it directly */
+int tal_host_register(void *p, int64_t bytes);
+int tal_host_unregister(void *p);
 
 /* ---- mesh ------------------------------------------------------------------ */
 /* Replaces the per-call coords/conn arguments of assemble_elements

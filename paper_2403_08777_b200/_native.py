@@ -70,6 +70,8 @@ SIGNATURES = [
     ("tal_destroy", _I, [_P]),
     ("tal_host_alloc", _I, [_I64, ctypes.POINTER(_P)]),
     ("tal_host_free", _I, [_P]),
+    ("tal_host_register", _I, [_P, _I64]),
+    ("tal_host_unregister", _I, [_P]),
     ("tal_upload_mesh", _I, [_P, _P, _P, _I64, _I64, _P, ctypes.POINTER(TalMeshOpts)]),
     ("tal_upload_mesh_ex", _I, [_P, _P, _P, _I64, _I64, _P, ctypes.POINTER(TalMeshOpts), _P, _I64]),
     ("tal_mesh_info_get", _I, [_P, ctypes.POINTER(TalMeshInfo)]),

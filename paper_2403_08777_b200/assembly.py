@@ -617,6 +617,9 @@ def clear_cache() -> None:
     while _SEAMS:
         _, (seam, *_) = _SEAMS.popitem()
         seam.close()
+    while _PINNED_U:
+        _, a = _PINNED_U.popitem()
+        N.lib().tal_host_unregister(N.ptr(a))
 
 
 def _stab_args(stabilization):
@@ -720,6 +723,30 @@ class _Seam:
 
 
 _SEAMS: "OrderedDict[tuple, tuple]" = OrderedDict()
+# velocity arrays page-locked for the seam (cudaHostRegister), held alive here
+# so the registration can never outlive the memory; the reference's drivers
+# pass the same u to every seam call of an assembly
+_PINNED_U: "OrderedDict[int, np.ndarray]" = OrderedDict()
+
+
+def _pin_velocity(u: np.ndarray) -> None:
+    if u.nbytes < (1 << 22) or not u.flags.c_contiguous:
+        return
+    key = u.ctypes.data
+    if key in _PINNED_U and _PINNED_U[key] is u:
+        _PINNED_U.move_to_end(key)
+        return
+    try:
+        N.check(N.lib().tal_host_register(N.ptr(u), u.nbytes))
+    except RuntimeError:  # e.g. overlapping an existing registration: keep the staged copy
+        return
+    old = _PINNED_U.pop(key, None)
+    if old is not None:
+        N.lib().tal_host_unregister(N.ptr(old))
+    _PINNED_U[key] = u
+    while len(_PINNED_U) > 2:
+        _, a = _PINNED_U.popitem(last=False)
+        N.lib().tal_host_unregister(N.ptr(a))
 
 
 def _seam_for(coords, conn, device) -> "_Seam":
@@ -768,6 +795,7 @@ def assemble_elements(coords, conn, u, rho, mu, cvre, pmat, ids, rhs, device: in
         if coords.shape[0] == 0 or ids.shape[0] == 0:
             return
         seam = _seam_for(coords, conn, device)
+        _pin_velocity(u)
         N.check(N.lib().tal_seam_assemble(seam.h, N.ptr(u), float(rho), float(mu), float(cvre),
                                           N.ptr(pm), N.ptr(ids), ids.shape[0], N.ptr(rhs)))
         return

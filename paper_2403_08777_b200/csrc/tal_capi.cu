@@ -1221,6 +1221,25 @@ int tal_host_alloc(int64_t bytes, void **out)
     TAL_GUARD_END
 }
 
+int tal_host_register(void *p, int64_t bytes)
+{
+    TAL_GUARD_BEGIN
+    if (!p || bytes <= 0)
+        return fail(TAL_EINVAL, "bad arguments");
+    TAL_CK(cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault));
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
+int tal_host_unregister(void *p)
+{
+    TAL_GUARD_BEGIN
+    if (p)
+        TAL_CK(cudaHostUnregister(p));
+    return TAL_OK;
+    TAL_GUARD_END
+}
+
 int tal_host_free(void *p)
 {
     TAL_GUARD_BEGIN
@@ -2181,10 +2200,15 @@ int seam_assemble_impl(tal_seam *c, const double *u, double rho, double mu, doub
     DeviceGuard g(h->device);
     cudaStream_t s = h->stream;
     const int64_t n3 = 3 * c->N;
+    constexpr int64_t PIECE = 1 << 19;  // doubles
+    cudaPointerAttributes pa_u{};
+    const bool u_locked = cudaPointerGetAttributes(&pa_u, u) == cudaSuccess && pa_u.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (u_locked)  // page-locked (cudaHostRegister / pinned): one DMA
+        TAL_CK(cudaMemcpyAsync(h->staging, u, sizeof(double) * n3, cudaMemcpyHostToDevice, s));
     // pageable u -> pinned -> device in 4 MB pieces: the host copy of piece
     // i+1 overlaps the DMA of piece i
-    constexpr int64_t PIECE = 1 << 19;  // doubles
-    for (int64_t i0 = 0; i0 < n3; i0 += PIECE) {
+    for (int64_t i0 = 0; i0 < n3 && !u_locked; i0 += PIECE) {
         const int64_t i1 = std::min(n3, i0 + PIECE);
         parallel_for(i1 - i0, [&](int64_t a, int64_t b, int) {
             std::memcpy(c->pin_u + i0 + a, u + i0 + a, sizeof(double) * (b - a));

@@ -27,6 +27,20 @@ if "big" not in sys.argv:  # the numba seam, fast and strict
     pm = interpolation_table()
     tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, rhs)
     tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids, rhs, strict=True)
+if "big" not in sys.argv:  # round 2 paths: SUPG, caller layout, seam subsets
+    for mode in ("private", "private-atomic", "atomic", "colored"):
+        tb.assemble_rsp(m, u, P, tb.RunConfig(scatter=mode), stabilization=True)
+    import torch
+    a2 = tb.Assembler(m, tb.RunConfig())
+    du = torch.as_tensor(u, device="cuda:0").contiguous()
+    dr = torch.empty_like(du)
+    for mode in ("private", "private-atomic"):
+        a2.run_caller(P, du.data_ptr(), dr.data_ptr(), scatter=mode, stream=0)
+    torch.cuda.synchronize()
+    a2.close()
+    ids2 = np.arange(5, m.n_elems // 2, dtype=np.int64)
+    tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids2, rhs)
+    tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids2[::3].copy(), rhs)
 for fn in () if "big" in sys.argv else (tb.assemble_baseline, tb.assemble_rs):
     fn(m, u, P, tb.RunConfig(scatter="atomic"))
 asm = tb.Assembler(m, tb.RunConfig(scatter="private-atomic", cta_patches=64, chunk_nodes=144))
