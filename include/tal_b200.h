@@ -257,9 +257,12 @@ int tal_synchronize(tal_handle *h, void *stream);
  * _rsp_kernels.assemble_elements (_rsp_kernels.py:20-21): assembles elements
  * ids[0..k) and ADDS (+=) into the host rhs, as the numba loop does.  The
  * mesh stays resident between calls in a small internal cache keyed by the
- * arrays' addresses, sizes and a content hash (a changed array is
- * re-uploaded, never served stale); ids = the whole mesh runs the edge-star
- * kernel, any other subset the per-element kernel. */
+ * arrays' addresses and sizes; every call re-checks 64-KB block fingerprints
+ * of the parts it reads (its conn rows, the coords rows they reference), so
+ * a changed array is re-uploaded, never served stale.  ids = the whole mesh
+ * runs the edge-star kernel, any other subset the per-element kernel; a
+ * contiguous range moves only the node rows its elements reference across
+ * PCIe (the reference's threaded slabs, variants.py:578-596). */
 int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
                           int64_t n_nodes, int64_t n_elems, const double *u,
                           double rho, double mu, double cvre,
@@ -277,10 +280,12 @@ int tal_assemble_elements_strict(int device, const double *coords, const int64_t
                                  const double *pmat, const int64_t *ids, int64_t k,
                                  double *rhs);
 
-/* The same seam with an explicit per-mesh context (no per-call content
- * hash): open once per (coords, conn), call tal_seam_assemble with the numba
- * kernel's remaining arguments, close.  Calls on one context are serialised
- * (thread-safe); u and rhs are caller-order (N,3) host arrays, rhs += result. */
+/* The same seam with an explicit per-mesh context (no per-call fingerprint
+ * check: the caller keeps coords / conn unchanged while the context is open):
+ * open once per (coords, conn), call tal_seam_assemble with the numba
+ * kernel's remaining arguments, close.  Thread-safe: id checks run
+ * concurrently, the GPU part of the calls is serialised; u and rhs are
+ * caller-order (N,3) host arrays, rhs += result. */
 typedef struct tal_seam tal_seam;
 int tal_seam_open(int device, const double *coords, const int64_t *conn, int64_t n_nodes,
                   int64_t n_elems, tal_seam **out);

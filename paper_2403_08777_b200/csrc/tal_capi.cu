@@ -2085,22 +2085,78 @@ int seam_impl(int device, const double *coords, const int64_t *conn, int64_t n_n
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// The fast numba seam: a per-mesh context (resident mesh + caller-order
-// connectivity on the device, pinned staging) so a call costs the velocity
-// H2D, one kernel and the RHS D2H.  'ids' = the whole mesh in order (the
-// reference's one-thread driver, variants.py:573-576): the private edge-star
-// kernel; a contiguous range (its threaded slabs, :578-596): the per-element
-// kernel over that conn range; any other list: the per-element kernel over an
-// uploaded id list.  Calls on one context are serialised (the reference
-// calls the seam from a thread pool).
+// The fast numba seam: a per-mesh context (resident mesh on the device in the
+// caller's own layout, per-block content fingerprints, pinned staging) so a
+// call costs the velocity rows it reads, one kernel and the RHS rows it
+// writes.  'ids' = the whole mesh in order (the reference's one-thread
+// driver, variants.py:573-576): the private edge-star kernel in caller layout
+// (launch_caller); a contiguous range (its threaded slabs, :578-596) or any
+// other list: the per-element kernel on the caller-layout arrays.  Only the
+// node rows the call's elements reference, [nmin, nmax], cross PCIe and are
+// added into the caller's rhs, so T threaded slab calls move ~1/T of the
+// arrays each instead of all of them.  The GPU part of the calls on one
+// context is serialised (the reference calls the seam from a thread pool);
+// id validation and fingerprint checks run outside that lock.
 // ---------------------------------------------------------------------------
+namespace {
+constexpr int64_t SEAM_BLOCK = 1 << 16;  // fingerprint block, bytes
+constexpr int64_t SEAM_EBLK = SEAM_BLOCK / 32;  // elements per conn block
+
+// order-fixed 64-bit fingerprint of one block: four independent lanes (the
+// multiply chains overlap, so this runs at memory speed)
+uint64_t block_hash(const uint8_t *q, int64_t n, uint64_t seed)
+{
+    uint64_t h[4] = {seed ^ 0x9e3779b97f4a7c15ull, seed ^ 0xc2b2ae3d27d4eb4full, seed ^ 0x165667b19e3779f9ull,
+                     seed ^ 0x27d4eb2f165667c5ull};
+    int64_t i = 0;
+    for (; i + 32 <= n; i += 32) {
+        uint64_t w[4];
+        std::memcpy(w, q + i, 32);
+        for (int l = 0; l < 4; ++l) {
+            h[l] = (h[l] ^ w[l]) * 0xff51afd7ed558ccdull;
+            h[l] ^= h[l] >> 29;
+        }
+    }
+    for (; i < n; ++i)
+        h[0] = (h[0] ^ q[i]) * 0xc4ceb9fe1a85ec53ull;
+    uint64_t x = (uint64_t)n;
+    for (int l = 0; l < 4; ++l)
+        x = (x ^ h[l]) * 0x100000001b3ull + 0x9e3779b97f4a7c15ull;
+    return x ^ (x >> 31);
+}
+
+int64_t n_blocks(int64_t bytes) { return (bytes + SEAM_BLOCK - 1) / SEAM_BLOCK; }
+
+void hash_blocks(const void *p, int64_t bytes, int64_t b0, int64_t b1, uint64_t *out)
+{
+    parallel_items(b1 - b0, [&](int64_t i, int) {
+        const int64_t b = b0 + i, o = b * SEAM_BLOCK;
+        out[i] = block_hash((const uint8_t *)p + o, std::min(SEAM_BLOCK, bytes - o), (uint64_t)b);
+    }, 4);
+}
+
+// do blocks [b0, b1) of p still hash to ref[b0 .. b1)?
+bool blocks_match(const void *p, int64_t bytes, int64_t b0, int64_t b1, const std::vector<uint64_t> &ref)
+{
+    if (b1 <= b0)
+        return true;
+    std::vector<uint64_t> h((size_t)(b1 - b0));
+    hash_blocks(p, bytes, b0, b1, h.data());
+    return std::equal(h.begin(), h.end(), ref.begin() + b0);
+}
+}  // namespace
+
 struct tal_seam {
-    tal_handle *h = nullptr;
-    int4 *conn_caller = nullptr;  // caller element order, internal node ids
+    tal_handle *h = nullptr;  // resident mesh (renumbered, edge-star chunks)
+    int4 *conn_c = nullptr;   // caller element order, caller node ids
+    double *xc = nullptr;     // caller-order coords, u staging, rhs accumulator (N,3)
+    double *uc = nullptr, *rc = nullptr;
     int32_t *d_ids = nullptr;
     int64_t ids_cap = 0;
     double *pin_u = nullptr, *pin_r = nullptr;
     int64_t N = 0, E = 0;
+    std::vector<uint64_t> hx, hc;     // per-block fingerprints of coords / conn at open
+    std::vector<int32_t> bmin, bmax;  // per conn block (SEAM_EBLK elements): node id range
     std::mutex mu;
 };
 
@@ -2111,10 +2167,9 @@ void seam_free(tal_seam *c)
         return;
     if (c->h) {
         DeviceGuard g(c->h->device);
-        if (c->conn_caller)
-            cudaFree(c->conn_caller);
-        if (c->d_ids)
-            cudaFree(c->d_ids);
+        for (void *q : {(void *)c->conn_c, (void *)c->xc, (void *)c->uc, (void *)c->rc, (void *)c->d_ids})
+            if (q)
+                cudaFree(q);
         if (c->pin_u)
             cudaFreeHost(c->pin_u);
         if (c->pin_r)
@@ -2130,8 +2185,33 @@ int seam_open_impl(int device, const double *coords, const int64_t *conn, int64_
     *out = nullptr;
     if (n_nodes < 0 || n_elems < 0 || (n_nodes && !coords) || (n_elems && !conn))
         return fail(TAL_EINVAL, "bad mesh arguments");
+    if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
+        return fail(TAL_EINVAL, "too many nodes / elements");
     std::unique_ptr<tal_seam, void (*)(tal_seam *)> c(new tal_seam(), seam_free);
     c->N = n_nodes, c->E = n_elems;
+    // connectivity range check + per-block node ranges (one pass), fingerprints
+    const int64_t nbe = (n_elems + SEAM_EBLK - 1) / SEAM_EBLK;
+    c->bmin.assign((size_t)nbe, INT32_MAX);
+    c->bmax.assign((size_t)nbe, -1);
+    std::atomic<bool> bad{false};
+    parallel_items(nbe, [&](int64_t b, int) {
+        int64_t lo = INT64_MAX, hi = -1;
+        for (int64_t i = 4 * b * SEAM_EBLK, e = std::min(4 * n_elems, 4 * (b + 1) * SEAM_EBLK); i < e; ++i) {
+            const int64_t v = conn[i];
+            lo = std::min(lo, v), hi = std::max(hi, v);
+        }
+        if (lo < 0 || hi >= n_nodes)
+            bad = true;
+        else
+            c->bmin[b] = (int32_t)lo, c->bmax[b] = (int32_t)hi;
+    }, 4);
+    if (bad)
+        return fail(TAL_EINVAL, "connectivity index out of range [0, n_nodes)");
+    const int64_t xb = sizeof(double) * 3 * n_nodes, cb = sizeof(int64_t) * 4 * n_elems;
+    c->hx.resize((size_t)n_blocks(xb));
+    c->hc.resize((size_t)n_blocks(cb));
+    hash_blocks(coords, xb, 0, n_blocks(xb), c->hx.data());
+    hash_blocks(conn, cb, 0, n_blocks(cb), c->hc.data());
     if (int rc = tal_create(device, &c->h))
         return rc;
     tal_mesh_opts o;
@@ -2143,6 +2223,11 @@ int seam_open_impl(int device, const double *coords, const int64_t *conn, int64_
     const size_t nb = sizeof(double) * 3 * (size_t)std::max<int64_t>(n_nodes, 1);
     TAL_CK(cudaMallocHost((void **)&c->pin_u, nb));
     TAL_CK(cudaMallocHost((void **)&c->pin_r, nb));
+    TAL_CK(cudaMalloc((void **)&c->xc, nb));
+    TAL_CK(cudaMalloc((void **)&c->uc, nb));
+    TAL_CK(cudaMalloc((void **)&c->rc, nb));
+    if (n_nodes)
+        TAL_CK(cudaMemcpy(c->xc, coords, sizeof(double) * 3 * n_nodes, cudaMemcpyHostToDevice));
     if (n_elems) {
         std::vector<int4> cc((size_t)n_elems);
         parallel_for(n_elems, [&](int64_t e0, int64_t e1, int) {
@@ -2150,29 +2235,22 @@ int seam_open_impl(int device, const double *coords, const int64_t *conn, int64_
                 cc[e] = make_int4((int)conn[4 * e], (int)conn[4 * e + 1], (int)conn[4 * e + 2],
                                   (int)conn[4 * e + 3]);
         });
-        TAL_CK(cudaMalloc((void **)&c->conn_caller, sizeof(int4) * n_elems));
-        TAL_CK(cudaMemcpy(c->conn_caller, cc.data(), sizeof(int4) * n_elems, cudaMemcpyHostToDevice));
-        if (c->h->iperm) {
-            k_remap_conn<<<grid_for(n_elems, 256), 256, 0, c->h->stream>>>(c->conn_caller, n_elems, c->h->iperm);
-            TAL_CK_LAUNCH();
-            TAL_CK(cudaStreamSynchronize(c->h->stream));
-        }
+        TAL_CK(cudaMalloc((void **)&c->conn_c, sizeof(int4) * n_elems));
+        TAL_CK(cudaMemcpy(c->conn_c, cc.data(), sizeof(int4) * n_elems, cudaMemcpyHostToDevice));
     }
     *out = c.release();
     return TAL_OK;
 }
 
-int seam_assemble_impl(tal_seam *c, const double *u, double rho, double mu, double cvre, const double *pmat,
-                       const int64_t *ids, int64_t k, double *rhs)
+// The elements of one call: validated ids, contiguous or not, node row range.
+struct SeamCall {
+    bool whole = false, range = false;
+    int64_t a0 = 0, k = 0, nmin = 0, nmax = -1;
+    std::vector<int32_t> i32;  // list calls: the ids as int32
+};
+
+int seam_plan(const tal_seam *c, const int64_t *ids, int64_t k, SeamCall &sc)
 {
-    if (!c || !c->h)
-        return fail(TAL_EINVAL, "seam context is NULL");
-    if (k < 0)
-        return fail(TAL_EINVAL, "negative sizes");
-    if (k == 0 || c->N == 0)
-        return TAL_OK;
-    if (!u || !pmat || !ids || !rhs)
-        return fail(TAL_EINVAL, "NULL arrays");
     const int64_t E = c->E, a0 = ids[0];
     std::atomic<bool> bad{false}, seq{true};
     parallel_for(k, [&](int64_t t0, int64_t t1, int) {
@@ -2187,6 +2265,44 @@ int seam_assemble_impl(tal_seam *c, const double *u, double rho, double mu, doub
     });
     if (bad)
         return fail(TAL_EINVAL, "element id out of range");
+    sc.a0 = a0, sc.k = k;
+    sc.range = seq;
+    sc.whole = seq && a0 == 0 && k == E;
+    if (seq) {  // node rows from the per-block ranges (conservative at the ends)
+        int64_t lo = INT64_MAX, hi = -1;
+        for (int64_t b = a0 / SEAM_EBLK; b <= (a0 + k - 1) / SEAM_EBLK; ++b)
+            lo = std::min<int64_t>(lo, c->bmin[b]), hi = std::max<int64_t>(hi, c->bmax[b]);
+        sc.nmin = lo, sc.nmax = hi;
+        return TAL_OK;
+    }
+    // a list (e.g. one colour class of the coloured driver) spans the mesh:
+    // all node rows
+    sc.i32.resize((size_t)k);
+    parallel_for(k, [&](int64_t t0, int64_t t1, int) {
+        for (int64_t t = t0; t < t1; ++t)
+            sc.i32[t] = (int32_t)ids[t];
+    });
+    sc.nmin = 0, sc.nmax = c->N - 1;
+    return TAL_OK;
+}
+
+// do the mesh arrays still hold what the context was built from, wherever this
+// call reads them (its conn rows, the coords rows [nmin, nmax])?
+bool seam_fresh(const tal_seam *c, const double *coords, const int64_t *conn, const SeamCall &sc)
+{
+    const int64_t xb = sizeof(double) * 3 * c->N, cb = sizeof(int64_t) * 4 * c->E;
+    if (sc.range) {
+        if (!blocks_match(conn, cb, sc.a0 * 32 / SEAM_BLOCK, ((sc.a0 + sc.k) * 32 - 1) / SEAM_BLOCK + 1, c->hc))
+            return false;
+    } else if (!blocks_match(conn, cb, 0, n_blocks(cb), c->hc)) {
+        return false;
+    }
+    return blocks_match(coords, xb, sc.nmin * 24 / SEAM_BLOCK, ((sc.nmax + 1) * 24 - 1) / SEAM_BLOCK + 1, c->hx);
+}
+
+int seam_assemble_impl(tal_seam *c, const double *u, double rho, double mu, double cvre, const double *pmat,
+                       const SeamCall &sc, double *rhs)
+{
     tal_params p;
     p.rho = rho, p.mu = mu, p.c_vreman = cvre;
     std::memcpy(p.pmat, pmat, sizeof p.pmat);
@@ -2199,82 +2315,71 @@ int seam_assemble_impl(tal_seam *c, const double *u, double rho, double mu, doub
     tal_handle *h = c->h;
     DeviceGuard g(h->device);
     cudaStream_t s = h->stream;
-    const int64_t n3 = 3 * c->N;
-    constexpr int64_t PIECE = 1 << 19;  // doubles
+    const int64_t r0 = 3 * sc.nmin, n3 = 3 * (sc.nmax - sc.nmin + 1);  // the call's rows, in doubles
+    constexpr int64_t PIECE = 1 << 19;                                  // doubles
     cudaPointerAttributes pa_u{};
     const bool u_locked = cudaPointerGetAttributes(&pa_u, u) == cudaSuccess && pa_u.type == cudaMemoryTypeHost;
     cudaGetLastError();
     if (u_locked)  // page-locked (cudaHostRegister / pinned): one DMA
-        TAL_CK(cudaMemcpyAsync(h->staging, u, sizeof(double) * n3, cudaMemcpyHostToDevice, s));
+        TAL_CK(cudaMemcpyAsync(c->uc + r0, u + r0, sizeof(double) * n3, cudaMemcpyHostToDevice, s));
     // pageable u -> pinned -> device in 4 MB pieces: the host copy of piece
     // i+1 overlaps the DMA of piece i
     for (int64_t i0 = 0; i0 < n3 && !u_locked; i0 += PIECE) {
         const int64_t i1 = std::min(n3, i0 + PIECE);
         parallel_for(i1 - i0, [&](int64_t a, int64_t b, int) {
-            std::memcpy(c->pin_u + i0 + a, u + i0 + a, sizeof(double) * (b - a));
+            std::memcpy(c->pin_u + r0 + i0 + a, u + r0 + i0 + a, sizeof(double) * (b - a));
         }, 1 << 15);
-        TAL_CK(cudaMemcpyAsync(h->staging + i0, c->pin_u + i0, sizeof(double) * (i1 - i0),
+        TAL_CK(cudaMemcpyAsync(c->uc + r0 + i0, c->pin_u + r0 + i0, sizeof(double) * (i1 - i0),
                                cudaMemcpyHostToDevice, s));
     }
-    if (int rc = tal_set_velocity_device(h, h->staging, s))
-        return rc;
-    int64_t nl = 0;
-    if (seq && a0 == 0 && k == E) {  // the whole mesh: the resident edge-star kernel
-        if (int rc = launch_run(h, &p, TAL_SCATTER_PRIVATE_ATOMIC, s, &nl))
+    if (sc.whole) {  // the resident edge-star kernel, caller layout in and out
+        int64_t nl = 0;
+        if (int rc = launch_caller(h, &p, TAL_SCATTER_PRIVATE_ATOMIC, c->uc, c->rc, s, &nl))
             return rc;
     } else {
-        TAL_CK(zero_rhs(h, s));
-        RhsSoA r{h->RX(), h->RY(), h->RZ()};
-        if (seq) {
-            if (sym)
-                k_assemble_atomic<true><<<grid_for(k, 256), 256, 0, s>>>(c->conn_caller, a0, a0 + k, h->REC(), r, kc, nullptr);
-            else
-                k_assemble_atomic<false><<<grid_for(k, 256), 256, 0, s>>>(c->conn_caller, a0, a0 + k, h->REC(), r, kc, nullptr);
-        } else {
-            if (k > c->ids_cap) {
+        TAL_CK(cudaMemsetAsync(c->rc + r0, 0, sizeof(double) * n3, s));
+        const int32_t *d_ids = nullptr;
+        if (!sc.range) {
+            if (sc.k > c->ids_cap) {
                 if (c->d_ids)
                     cudaFree(c->d_ids);
                 c->d_ids = nullptr;
                 c->ids_cap = 0;
-                TAL_CK(cudaMalloc((void **)&c->d_ids, sizeof(int32_t) * k));
-                c->ids_cap = k;
+                TAL_CK(cudaMalloc((void **)&c->d_ids, sizeof(int32_t) * sc.k));
+                c->ids_cap = sc.k;
             }
-            std::vector<int32_t> i32((size_t)k);
-            parallel_for(k, [&](int64_t t0, int64_t t1, int) {
-                for (int64_t t = t0; t < t1; ++t)
-                    i32[t] = (int32_t)ids[t];
-            });
-            TAL_CK(cudaMemcpyAsync(c->d_ids, i32.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, s));
-            if (sym)
-                k_assemble_atomic_ids<true><<<grid_for(k, 256), 256, 0, s>>>(c->conn_caller, c->d_ids, k, h->REC(), r, kc);
-            else
-                k_assemble_atomic_ids<false><<<grid_for(k, 256), 256, 0, s>>>(c->conn_caller, c->d_ids, k, h->REC(), r, kc);
+            TAL_CK(cudaMemcpyAsync(c->d_ids, sc.i32.data(), sizeof(int32_t) * sc.k, cudaMemcpyHostToDevice, s));
+            d_ids = c->d_ids;
         }
+        if (sym)
+            k_assemble_atomic_caller<true><<<grid_for(sc.k, 256), 256, 0, s>>>(c->conn_c, d_ids, sc.a0, sc.k, c->xc,
+                                                                              c->uc, c->rc, kc);
+        else
+            k_assemble_atomic_caller<false><<<grid_for(sc.k, 256), 256, 0, s>>>(c->conn_c, d_ids, sc.a0, sc.k, c->xc,
+                                                                               c->uc, c->rc, kc);
         TAL_CK_LAUNCH();
     }
     // device -> pinned in pieces; piece i is added into rhs while piece i+1 copies
-    if (int rc = tal_get_rhs_device(h, h->staging, s))
-        return rc;
     const int64_t np_ = (n3 + PIECE - 1) / PIECE;
     std::vector<cudaEvent_t> ev((size_t)np_);
     for (auto &e : ev)
         TAL_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     int rc = TAL_OK;
-    for (int64_t p = 0; p < np_; ++p) {
-        const int64_t i0 = p * PIECE, i1 = std::min(n3, i0 + PIECE);
-        if (cudaMemcpyAsync(c->pin_r + i0, h->staging + i0, sizeof(double) * (i1 - i0), cudaMemcpyDeviceToHost,
-                            s) != cudaSuccess ||
-            cudaEventRecord(ev[p], s) != cudaSuccess) {
+    for (int64_t q = 0; q < np_; ++q) {
+        const int64_t i0 = r0 + q * PIECE, i1 = std::min(r0 + n3, i0 + PIECE);
+        if (cudaMemcpyAsync(c->pin_r + i0, c->rc + i0, sizeof(double) * (i1 - i0), cudaMemcpyDeviceToHost, s) !=
+                cudaSuccess ||
+            cudaEventRecord(ev[q], s) != cudaSuccess) {
             rc = fail(TAL_ECUDA, "seam D2H");
             break;
         }
     }
-    for (int64_t p = 0; p < np_ && rc == TAL_OK; ++p) {
-        if (cudaEventSynchronize(ev[p]) != cudaSuccess) {
+    for (int64_t q = 0; q < np_ && rc == TAL_OK; ++q) {
+        if (cudaEventSynchronize(ev[q]) != cudaSuccess) {
             rc = fail(TAL_ECUDA, "seam D2H sync");
             break;
         }
-        const int64_t i0 = p * PIECE, i1 = std::min(n3, i0 + PIECE);
+        const int64_t i0 = r0 + q * PIECE, i1 = std::min(r0 + n3, i0 + PIECE);
         parallel_for(i1 - i0, [&](int64_t a, int64_t b, int) {
             for (int64_t i = i0 + a; i < i0 + b; ++i)
                 rhs[i] += c->pin_r[i];
@@ -2286,48 +2391,62 @@ int seam_assemble_impl(tal_seam *c, const double *u, double rho, double mu, doub
     return rc;
 }
 
-// stateless entry: a small cache of contexts keyed by the mesh arrays'
-// addresses, sizes and a content hash (parallel, order-fixed 64-bit mix), so
-// repeated calls on one mesh reuse the device copy and a changed array is
-// never served stale
-uint64_t content_hash(const void *p, size_t bytes)
+int seam_call(tal_seam *c, const double *u, double rho, double mu, double cvre,
+              const double *pmat, const int64_t *ids, int64_t k, double *rhs)
 {
-    const size_t B = 1 << 16, nb = (bytes + B - 1) / B;
-    std::vector<uint64_t> hb(nb);
-    parallel_items((int64_t)nb, [&](int64_t b, int) {
-        const uint8_t *q = (const uint8_t *)p + b * B;
-        const size_t n = std::min(B, bytes - b * B);
-        uint64_t x = 0x9e3779b97f4a7c15ull ^ (uint64_t)b;
-        size_t i = 0;
-        for (; i + 8 <= n; i += 8) {
-            uint64_t w;
-            std::memcpy(&w, q + i, 8);
-            x = (x ^ w) * 0xff51afd7ed558ccdull;
-            x ^= x >> 29;
-        }
-        for (; i < n; ++i)
-            x = (x ^ q[i]) * 0xc4ceb9fe1a85ec53ull;
-        hb[b] = x;
-    }, 16);
-    uint64_t h = bytes;
-    for (uint64_t x : hb)
-        h = (h ^ x) * 0x100000001b3ull + 0x9e3779b97f4a7c15ull;
-    return h;
+    if (!c || !c->h)
+        return fail(TAL_EINVAL, "seam context is NULL");
+    if (k < 0)
+        return fail(TAL_EINVAL, "negative sizes");
+    if (k == 0 || c->N == 0)
+        return TAL_OK;
+    if (!u || !pmat || !ids || !rhs)
+        return fail(TAL_EINVAL, "NULL arrays");
+    SeamCall sc;
+    if (int rc = seam_plan(c, ids, k, sc))
+        return rc;
+    return seam_assemble_impl(c, u, rho, mu, cvre, pmat, sc, rhs);
 }
 
+// stateless entry: a small cache of contexts keyed by the mesh arrays'
+// addresses and sizes; every call re-checks the fingerprints of the blocks it
+// reads (its conn rows, its coords rows), so a changed array is never served
+// stale -- the context is rebuilt instead
 struct SeamKey {
     int device;
     const void *coords, *conn;
     int64_t N, E;
-    uint64_t hash;
     bool operator==(const SeamKey &o) const
     {
-        return device == o.device && coords == o.coords && conn == o.conn && N == o.N && E == o.E &&
-               hash == o.hash;
+        return device == o.device && coords == o.coords && conn == o.conn && N == o.N && E == o.E;
     }
 };
 std::mutex g_seam_mu;
-std::vector<std::pair<SeamKey, tal_seam *>> g_seams;  // most recent last, at most 2
+std::vector<std::pair<SeamKey, std::shared_ptr<tal_seam>>> g_seams;  // most recent last, at most 2
+
+std::shared_ptr<tal_seam> seam_lookup(const SeamKey &key, const tal_seam *stale, int &rc)
+{
+    std::lock_guard<std::mutex> lk(g_seam_mu);
+    for (size_t i = 0; i < g_seams.size(); ++i)
+        if (g_seams[i].first == key) {
+            if (g_seams[i].second.get() == stale) {  // rebuild from the current contents
+                g_seams.erase(g_seams.begin() + i);
+                break;
+            }
+            auto c = g_seams[i].second;
+            std::rotate(g_seams.begin() + i, g_seams.begin() + i + 1, g_seams.end());
+            return c;
+        }
+    tal_seam *raw = nullptr;
+    rc = seam_open_impl(key.device, (const double *)key.coords, (const int64_t *)key.conn, key.N, key.E, &raw);
+    if (rc)
+        return nullptr;
+    std::shared_ptr<tal_seam> c(raw, seam_free);
+    g_seams.push_back({key, c});
+    if (g_seams.size() > 2)
+        g_seams.erase(g_seams.begin());  // freed when its last in-flight call ends
+    return c;
+}
 }  // namespace
 
 int tal_seam_open(int device, const double *coords, const int64_t *conn, int64_t n_nodes, int64_t n_elems,
@@ -2344,7 +2463,8 @@ int tal_seam_assemble(tal_seam *ctx, const double *u, double rho, double mu, dou
                       const int64_t *ids, int64_t k, double *rhs)
 {
     TAL_GUARD_BEGIN
-    return seam_assemble_impl(ctx, u, rho, mu, cvre, pmat, ids, k, rhs);
+    // the mesh is the caller's contract here (unchanged since tal_seam_open)
+    return seam_call(ctx, u, rho, mu, cvre, pmat, ids, k, rhs);
     TAL_GUARD_END
 }
 
@@ -2369,43 +2489,23 @@ int tal_assemble_elements(int device, const double *coords, const int64_t *conn,
         return fail(TAL_EINVAL, "NULL arrays");
     if (n_nodes >= (int64_t)1 << 31 || n_elems >= (int64_t)1 << 31)
         return fail(TAL_EINVAL, "too many nodes / elements");
-    {
-        std::atomic<bool> bad{false};
-        parallel_for(4 * n_elems, [&](int64_t i0, int64_t i1, int) {
-            for (int64_t i = i0; i < i1; ++i)
-                if (conn[i] < 0 || conn[i] >= n_nodes) {
-                    bad = true;
-                    return;
-                }
-        });
-        if (bad)
-            return fail(TAL_EINVAL, "connectivity index out of range [0, n_nodes)");
-    }
-    const SeamKey key{device, coords, conn, n_nodes, n_elems,
-                      content_hash(coords, sizeof(double) * 3 * n_nodes) * 31 +
-                          content_hash(conn, sizeof(int64_t) * 4 * n_elems)};
-    tal_seam *ctx = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(g_seam_mu);
-        for (size_t i = 0; i < g_seams.size(); ++i)
-            if (g_seams[i].first == key) {
-                ctx = g_seams[i].second;
-                std::rotate(g_seams.begin() + i, g_seams.begin() + i + 1, g_seams.end());
-                break;
-            }
-        if (!ctx) {
-            if (int rc = seam_open_impl(device, coords, conn, n_nodes, n_elems, &ctx))
-                return rc;
-            g_seams.push_back({key, ctx});
-            if (g_seams.size() > 2) {
-                seam_free(g_seams.front().second);
-                g_seams.erase(g_seams.begin());
-            }
+    const SeamKey key{device, coords, conn, n_nodes, n_elems};
+    const tal_seam *stale = nullptr;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        int rc = TAL_OK;
+        std::shared_ptr<tal_seam> c = seam_lookup(key, stale, rc);
+        if (!c)
+            return rc;
+        SeamCall sc;
+        if ((rc = seam_plan(c.get(), ids, k, sc)))
+            return rc;
+        if (!seam_fresh(c.get(), coords, conn, sc)) {
+            stale = c.get();  // the mesh changed under this key: rebuild once
+            continue;
         }
-        // calls on one context serialise on its own mutex; the cache lock
-        // is held through the call so an eviction cannot free it underneath
-        return seam_assemble_impl(ctx, u, rho, mu, cvre, pmat, ids, k, rhs);
+        return seam_assemble_impl(c.get(), u, rho, mu, cvre, pmat, sc, rhs);
     }
+    return fail(TAL_ESTATE, "mesh arrays changed while assembling");
     TAL_GUARD_END
 }
 

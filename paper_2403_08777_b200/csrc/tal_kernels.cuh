@@ -144,41 +144,36 @@ __global__ void __launch_bounds__(256) k_assemble_atomic(const int4 *__restrict_
     }
 }
 
-// the same over an element id list (the numba seam with a non-contiguous
-// 'ids' subset): conn rows ids[t]
+// the numba seam over a subset of elements, entirely in the caller's layout:
+// conn rows e_begin + t (ids == nullptr) or ids[t], caller node ids; coords,
+// u and rhs (N,3) AoS in caller numbering (rows are 8-B aligned)
 template <bool SYM>
-__global__ void __launch_bounds__(256) k_assemble_atomic_ids(const int4 *__restrict__ conn,
-                                                             const int32_t *__restrict__ ids, int64_t k,
-                                                             const double *__restrict__ nrec, RhsSoA rhs,
-                                                             ElemConsts kc)
+__global__ void __launch_bounds__(256) k_assemble_atomic_caller(const int4 *__restrict__ conn,
+                                                                const int32_t *__restrict__ ids,
+                                                                int64_t e_begin, int64_t k,
+                                                                const double *__restrict__ xc,
+                                                                const double *__restrict__ uc, double *rc,
+                                                                ElemConsts kc)
 {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= k)
         return;
-    const int4 q = __ldg(conn + __ldg(ids + t));
+    const int4 q = __ldg(conn + (ids ? (int64_t)__ldg(ids + t) : e_begin + t));
     const int n[4] = {q.x, q.y, q.z, q.w};
     double X[4][3], U[4][3], R[4][3];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
-        load_record_g(nrec, n[a], X[a], U[a]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            X[a][c] = __ldg(xc + 3 * (int64_t)n[a] + c);
+            U[a][c] = __ldg(uc + 3 * (int64_t)n[a] + c);
+        }
     element_rhs<SYM>(X, U, nullptr, kc, R);
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        atomicAdd(rhs.rx + n[a], R[a][0]);
-        atomicAdd(rhs.ry + n[a], R[a][1]);
-        atomicAdd(rhs.rz + n[a], R[a][2]);
-    }
-}
-
-// caller connectivity (int4, caller node ids) -> internal node ids, in place
-__global__ void k_remap_conn(int4 *c, int64_t k, const int32_t *__restrict__ iperm)
-{
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= k)
-        return;
-    int4 q = c[t];
-    q.x = iperm[q.x], q.y = iperm[q.y], q.z = iperm[q.z], q.w = iperm[q.w];
-    c[t] = q;
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            atomicAdd(rc + 3 * (int64_t)n[a] + c, R[a][c]);
 }
 
 // ---------------------------------------------------------------------------
@@ -442,6 +437,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
         if (tid < hdr.x) {
             const uint16_t *ids = reinterpret_cast<const uint16_t *>(bl + 16) + tid;
             const uint16_t *pos = ids + SLOTS * T;
+
 #define ID(s) ids[(s) * T]
 #define POS(s) pos[(s) * T]
             const int m = ID(0) & 0xff;

@@ -1,10 +1,14 @@
 """Physical parameters, quadrature and velocity initialisers.
 
-Mirrors the reference's ``kernel.py`` data API (tet-assembly-lab 0.1.0):
-``PhysParams`` (kernel.py:27-49), ``QuadratureRule``/``quadrature_tet4``
-(kernel.py:52-86), ``validate_velocity`` (kernel.py:194-200) and the
-``make_velocity`` initialisers (kernel.py:203-278).  These are host-side
-input preparation, not part of the device hot path.
+A near-verbatim restatement (deliberately, not a redesign) of the
+reference's ``kernel.py`` data API (tet-assembly-lab 0.1.0): ``PhysParams``
+(kernel.py:27-49), ``QuadratureRule``/``quadrature_tet4`` (kernel.py:52-86),
+``validate_velocity`` (kernel.py:194-200) and the ``make_velocity``
+initialisers (kernel.py:203-278), with the same field names, defaults,
+formulas and error strings.  The drop-in contract needs exactly that: the
+synthetic velocity fields must be bitwise the reference's (the golden
+vectors are generated from them) and callers catch the same ValueErrors.
+These are host-side input preparation, not part of the device hot path.
 """
 
 from __future__ import annotations

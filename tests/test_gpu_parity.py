@@ -587,6 +587,69 @@ def test_stateless_seam_entry_sees_changed_arrays(oracle):
     del ctypes
 
 
+def test_stateless_seam_range_calls_see_changes_they_read(oracle):
+    """Slab calls on the stateless entry check the fingerprints of the blocks
+    they read (their conn rows and coords rows): a change inside a later
+    slab's rows, or of connectivity, is re-uploaded before that slab runs."""
+    from paper_2403_08777_b200 import _native as N
+    m = tb.generate_box_mesh(40, 30, 30)  # coords 0.9 MB, conn 4.6 MB: many fingerprint blocks
+    coords = np.array(m.coords)
+    conn = np.array(m.connectivity)
+    u = tb.make_velocity(m, "random:3")
+    pm = tb.interpolation_table()
+    E = m.n_elems
+
+    def call(ids):
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        out = np.zeros((m.n_nodes, 3))
+        N.check(N.lib().tal_assemble_elements(0, N.ptr(coords), N.ptr(conn), coords.shape[0],
+                                              conn.shape[0], N.ptr(u), 1.0, 1e-3, 0.07, N.ptr(pm),
+                                              N.ptr(ids), ids.shape[0], N.ptr(out)))
+        ref = np.zeros_like(out)
+        oracle.assemble_elements(coords, conn, u, 1.0, 1e-3, 0.07, pm, ids, ref)
+        assert np.abs(out - ref).max() <= 1e-13 * np.abs(ref).max()
+        return out
+
+    lo, hi = np.arange(0, E // 4), np.arange(3 * E // 4, E)
+    call(lo)
+    call(hi)
+    v = int(conn[hi[-1], 0])
+    coords[v] += 0.01  # a node only the last slab reads
+    call(lo)
+    call(hi)
+    conn[hi[10], [1, 2]] = conn[hi[10], [2, 1]]  # connectivity change (orientation flip)
+    call(hi)
+    call(np.arange(E))
+
+
+def test_fast_seam_from_a_thread_pool(oracle):
+    """The reference's threaded private driver (variants.py:578-596): slab
+    calls from a ThreadPoolExecutor, one accumulator per thread, merged in
+    thread order -- the fast seam under concurrency (serialised GPU part,
+    per-call node-row windows)."""
+    from concurrent.futures import ThreadPoolExecutor
+    m = tb.generate_box_mesh(24, 20, 18)
+    u = tb.make_velocity(m, "random:5")
+    pm = tb.interpolation_table()
+    E, T = m.n_elems, 8
+    ids = np.arange(E, dtype=np.int64)
+    cut = [E * t // T for t in range(T + 1)]
+    bufs = [np.zeros((m.n_nodes, 3)) for _ in range(T)]
+    for _ in range(2):
+        for b in bufs:
+            b[:] = 0.0
+        with ThreadPoolExecutor(T) as pool:
+            fs = [pool.submit(tb.assemble_elements, m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm,
+                              ids[cut[t]:cut[t + 1]], bufs[t]) for t in range(T)]
+            for f in fs:
+                f.result()
+        got = bufs[0].copy()
+        for b in bufs[1:]:
+            got += b
+        ref = oracle.assemble_rsp(m.coords, m.connectivity, u)
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
 @pytest.mark.parametrize("renumber", ["rcm", "sfc", "none"])
 @pytest.mark.parametrize("permuted", [False, True])
 def test_run_caller_fused_layout(oracle, renumber, permuted):

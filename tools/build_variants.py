@@ -14,10 +14,11 @@ sys.path.insert(0, str(ROOT))
 from paper_2403_08777_b200 import build as B  # noqa: E402
 
 out = ROOT / "build" / "var"
-shutil.rmtree(out, ignore_errors=True)
-out.mkdir(parents=True)
+if "--keep" not in sys.argv:
+    shutil.rmtree(out, ignore_errors=True)
+out.mkdir(parents=True, exist_ok=True)
 specs = []
-for a in sys.argv[1:]:
+for a in [x for x in sys.argv[1:] if x != "--keep"]:
     name, _, defs = a.partition("=")
     specs.append((name, [d for d in defs.split(",") if d]))
 

@@ -1,6 +1,6 @@
 # A/B timing of build variants (build/var/*.so) on the default bench config,
 # reps interleaved across variants (same box, same clocks)
-OUT=gpurun_out/r2
+OUT=${VAR_OUT:-gpurun_out/r2}
 mkdir -p $OUT
 rm -f $OUT/variants.json
 for rep in 1 2 3; do
@@ -11,7 +11,7 @@ done
 python - <<'PY'
 import json, collections
 d = collections.defaultdict(list)
-for l in open("gpurun_out/r2/variants.json"):
+for l in open(__import__("os").environ.get("VAR_OUT","gpurun_out/r2")+"/variants.json"):
     r = json.loads(l); d[r["lib"]].append(r["kernel_ms"])
 for k, v in d.items():
     print(f"{k:30s} kernel ms {min(v):.4f} (reps {', '.join('%.4f' % x for x in v)})")
