@@ -287,7 +287,9 @@ def run_reference(a) -> None:
     elif a.scaling == "weak":
         workload = f"{c}x{c}x{gz} Kuhn box, a {c}^3 slab per rank ({ws} ranks), {a.init}"
     else:
-        workload = f"{c}^3 Kuhn box cut into {ws} z-slabs, {a.init}"
+        cut = "z-slabs" if a.partition == "slab" else "RCB parts"
+        workload = f"{c}^3 Kuhn box cut into {ws} {cut}" + (" (random node numbering)" if a.permute else "") + \
+            f", {a.init}"
     line = {
         "impl": "reference", "metric": "assembled elements/s", "value": cb["value"],
         "unit": "elem/s", "n_gpus": ws, "steps": cb["steps"], "warmup": a.warmup,
@@ -425,6 +427,9 @@ def run_ours(a) -> None:
     torch.cuda.synchronize()
     asm.profile_read()
     fp64_tf, fp64_mhz = N.fp64_peak(dev, 5.0)  # >= 5 ms DFMA launches, best of 20
+    gpus_shared = torch.cuda.device_count() < ws
+    if gpus_shared:  # ranks time-sharing one GPU probe concurrently: each sees a fraction
+        fp64_tf = NOMINAL_FP64_TFLOPS
 
     sampler = ClockSampler(dev)
     sampler.start()
@@ -698,7 +703,9 @@ def run_ours(a) -> None:
     elif a.scaling == "weak":
         workload = f"{c}x{c}x{gz} Kuhn box, a {c}^3 slab per rank ({ws} ranks), {a.init}"
     else:
-        workload = f"{c}^3 Kuhn box cut into {ws} z-slabs, {a.init}"
+        cut = "z-slabs" if a.partition == "slab" else "RCB parts"
+        workload = f"{c}^3 Kuhn box cut into {ws} {cut}" + (" (random node numbering)" if a.permute else "") + \
+            f", {a.init}"
     tf = FLOP_PER_ELEM * rate / 1e12  # per GPU (the slowest rank at N>1)
     alg_bytes = 16 * E + 72 * Nn  # int32 conn + coords/u read + rhs write
     hbm_gbs = bytes_per_elem * rate / 1e9
@@ -728,7 +735,7 @@ def run_ours(a) -> None:
                    "cuda_graph": bool(use_graph),
                    "l2": "flushed (256 MiB write) before every step, outside the timed events"
                          if flush_buf is not None else "not flushed",
-                   "gpus_shared": torch.cuda.device_count() < ws,
+                   "gpus_shared": gpus_shared,
                    "traffic_key": traffic_key(a, workload),
                    "parallelism": (f"dp{ws} z-slabs" if a.partition == "slab" else f"dp{ws} RCB parts")
                    if ws > 1 else "single GPU",
@@ -738,12 +745,15 @@ def run_ours(a) -> None:
                        + (f" (fused unavailable: {dom.fused_error})" if dom.fused_error else ""))},
         "roofline": {"bound": "fp64", "kernel": kname, "achieved": tf, "peak": fp64_tf,
                      "unit": "TFLOP/s", "frac": tf / fp64_tf,
-                     "peak_source": "live DFMA probe in this run (tal_fp64_peak: >= 5 ms "
+                     "peak_source": ("nominal 148 SM x 64 DFMA/clk x 2 x 1965 MHz: the ranks share one "
+                                     "GPU, so a live probe would see a fraction of the pipe (validation "
+                                     "line, not a performance claim)") if gpus_shared else (
+                                    "live DFMA probe in this run (tal_fp64_peak: >= 5 ms "
                                     "launches of 8 independent DFMA chains per thread, best of 20, at "
                                     f"{fp64_mhz:.0f} MHz measured in-kernel); DFMA issues at ~58.3 of "
                                     "the nominal 64 lanes/clk/SM while DMUL/DADD reach 63.8 "
                                     "(tools/probe_fp64.cu, profiles/round2/probe_fp64.txt); nominal "
-                                    f"{NOMINAL_FP64_TFLOPS} at 1965 MHz",
+                                    f"{NOMINAL_FP64_TFLOPS} at 1965 MHz"),
                      "frac_of_nominal": tf / NOMINAL_FP64_TFLOPS,
                      "probe_sm_mhz": fp64_mhz,
                      "flop_per_elem": FLOP_PER_ELEM, "kernel_ms": kmean,
