@@ -109,7 +109,6 @@ struct tal_handle {
     Chunking ch;
     uint8_t *d_blobs = nullptr;
     int32_t *d_blob_off = nullptr;
-    int *d_sched = nullptr;  // dynamic chunk scheduling counters (2 ints, zero between launches)
     int32_t *d_bnd_nodes = nullptr, *d_bnd_off = nullptr, *d_bnd_pos = nullptr;
     int32_t *d_cg = nullptr, *d_cc = nullptr;  // caller ids of the chunk-node entries (tal_run_caller)
     double *d_partial = nullptr;  // 3 * n_chunk_nodes
@@ -178,7 +177,7 @@ struct tal_handle {
     {
         free_graph();
         free_peers();
-        void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off, d_sched,
+        void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
                         d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press, d_seq_off, d_seq_ent, d_seq_dlt, d_seq_rows,
                         d_cg, d_cc};
         for (void *p : ptrs)
@@ -203,7 +202,6 @@ struct tal_handle {
         d_cg = d_cc = nullptr;
         conn = conn_col = nullptr;
         d_blobs = nullptr;
-        d_sched = nullptr;
         col_off.clear();
         h_iperm.clear();
         ch = Chunking();
@@ -532,7 +530,6 @@ int launch_run(tal_handle *h, const tal_params *p, int scatter, cudaStream_t s, 
         const bool ordered = scatter == TAL_SCATTER_PRIVATE;
         PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, nullptr,
                     h->has_press ? h->d_press : nullptr};
-        pa.sched = h->d_sched;
         PeerArgs peer{};
         const int np = h->n_peers();
         if (np && ordered)
@@ -771,7 +768,6 @@ int launch_caller(tal_handle *h, const tal_params *p, int scatter, const double 
         TAL_CK(cudaMemsetAsync(d_rhs, 0, sizeof(double) * 3 * h->N, s));
     PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, ordered ? h->d_partial : nullptr, nullptr,
                 h->d_cg, h->d_cc, d_u, d_rhs};
-    pa.sched = h->d_sched;
     RhsSoA rhs{h->RX(), h->RY(), h->RZ()};
     const unsigned grid = (unsigned)std::min<int64_t>(h->priv_grid_ext[0], h->info.n_chunks);
     pm.begin();
@@ -1424,8 +1420,6 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
         return rc;
     if ((rc = dev_upload(&h->d_blob_off, blob_off.data(), blob_off.size())))
         return rc;
-    TAL_CK(cudaMalloc((void **)&h->d_sched, 2 * sizeof(int)));
-    TAL_CK(cudaMemset(h->d_sched, 0, 2 * sizeof(int)));
     if ((rc = dev_upload(&h->d_bnd_nodes, C.bnd_nodes.data(), C.bnd_nodes.size())))
         return rc;
     if ((rc = dev_upload(&h->d_bnd_off, C.bnd_off.data(), C.bnd_off.size())))

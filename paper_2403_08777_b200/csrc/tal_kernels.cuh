@@ -263,9 +263,6 @@ constexpr int kRingUnroll = TAL_RING_UNROLL;
 #ifndef TAL_RELOAD_AB
 #define TAL_RELOAD_AB 0
 #endif
-#ifndef TAL_DYN
-#define TAL_DYN 0  // chunks handed out by a global counter instead of dealt round-robin
-#endif
 #ifndef TAL_ORIENT
 #define TAL_ORIENT 0  // experiment: host-oriented patches (every ring tet det > 0)
 #endif
@@ -318,9 +315,6 @@ struct PrivArgs {
     const int32_t *__restrict__ cc;
     const double *__restrict__ u_caller;
     double *rhs_caller;
-    // dynamic chunk scheduling: [0] next chunk, [1] CTAs done (both zero
-    // between launches: the last CTA to finish resets them)
-    int *sched;
 };
 
 // PR: with the optional pressure-gradient term (tal_element.cuh pressure_add);
@@ -344,29 +338,15 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
     double *resy = resx + NC, *resz = resy + NC;
     const int tid = threadIdx.x;
     const int first = blockIdx.x, stride = gridDim.x;
-#if TAL_DYN
-    // chunk ids of the two blob buffers (smem bytes 16..23, between the
-    // mbarriers and the blobs); a chunk id >= n_chunks ends the walk
-    volatile int *cid = reinterpret_cast<volatile int *>(sm + 16);
-    const int n_my = 1 << 30;
-#else
     const int n_my = pa.n_chunks > first ? (pa.n_chunks - first + stride - 1) / stride : 0;
     if (n_my == 0)
         return;
-#endif
     auto blob = [&](int b) { return sm + L::BLOBS + b * L::BLOB_AL; };
     double *const nrec_s = reinterpret_cast<double *>(sm + L::NREC);
     double *const pres_s = reinterpret_cast<double *>(sm + L::PRS);
 
     auto issue = [&](int i, int b) {  // one thread: bulk-copy chunk i's blob into buffer b
-#if TAL_DYN
-        const int c = atomicAdd(pa.sched, 1);
-        cid[b] = c;
-        if (c >= pa.n_chunks)
-            return;
-#else
         const int c = first + i * stride;
-#endif
         const int o0 = __ldg(pa.blob_off + c), o1 = __ldg(pa.blob_off + c + 1);
         const uint32_t bytes = (uint32_t)(o1 - o0) * 16u;
         mbar_expect_tx(&bar[b], bytes);
@@ -431,37 +411,20 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
         if (n_my > 1)
             issue(1, 1);
     }
-#if TAL_DYN
-    __syncthreads();
-    const bool any = cid[0] < pa.n_chunks;
-    if (any) {
-        mbar_wait(&bar[0], 0);
-        gather(0);
-    }
-    for (int i = 0; any; ++i) {
-#else
     mbar_wait(&bar[0], 0);
     gather(0);
 
     for (int i = 0; i < n_my; ++i) {
-#endif
         const int b = i & 1;
         cp_async_wait_all();
         __syncthreads();  // node records of chunk i visible to all; phase C(i-1) done
         // blob i+1 into the buffer chunk i-1 used: every thread has finished
         // reading it (phase C(i-1)) before the barrier above, so no third
         // barrier per chunk is needed; it lands during phase B(i)
-#if TAL_DYN
-        if (tid == 0 && i >= 1 && cid[b ^ 1] < pa.n_chunks) {  // ids[b^1] = chunk i-1 was real
-            fence_proxy_async();
-            issue(i + 1, b ^ 1);
-        }
-#else
         if (tid == 0 && i >= 1 && i + 1 < n_my) {
             fence_proxy_async();
             issue(i + 1, b ^ 1);
         }
-#endif
         const uint8_t *bl = blob(b);
         const int4 hdr = *reinterpret_cast<const int4 *>(bl);  // n_patch, n_node, node_begin, n_contrib
         const uint16_t *lev = reinterpret_cast<const uint16_t *>(bl + 16 + L::TABLES);
@@ -585,12 +548,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
         __syncthreads();
         // records of chunk i+1 into the (single) record buffer, free now that
         // phase B(i) is done; its blob has had all of phase B(i) to land
-#if TAL_DYN
-        const bool more = cid[b ^ 1] < pa.n_chunks;  // written before the phase-B barrier
-        if (more) {
-#else
         if (i + 1 < n_my) {
-#endif
             mbar_wait(&bar[b ^ 1], ((i + 1) >> 1) & 1);
             gather(b ^ 1);
         }
@@ -652,22 +610,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
                 }
             }
         }
-#if TAL_DYN
-        if (!more)
-            break;
-#endif
     }
-#if TAL_DYN
-    // the last CTA out resets the counters for the next launch (every CTA's
-    // failing fetch happened before its 'done' increment)
-    if (tid == 0) {
-        __threadfence();
-        if (atomicAdd(pa.sched + 1, 1) == (int)gridDim.x - 1) {
-            atomicExch(pa.sched, 0);
-            atomicExch(pa.sched + 1, 0);
-        }
-    }
-#endif
 }
 
 // ordered merge of chunk partials for nodes shared between chunks (and zero
