@@ -110,7 +110,10 @@ struct tal_handle {
     uint8_t *d_blobs = nullptr;
     int32_t *d_blob_off = nullptr;
     int32_t *d_bnd_nodes = nullptr, *d_bnd_off = nullptr, *d_bnd_pos = nullptr;
-    int32_t *d_cg = nullptr, *d_cc = nullptr;  // caller ids of the chunk-node entries (tal_run_caller)
+    // tal_run_caller: chunk blobs with caller node ids, caller-order coordinates
+    uint8_t *d_blobs_cl = nullptr;
+    double *d_xc = nullptr;
+    int64_t blob_bytes = 0;
     double *d_partial = nullptr;  // 3 * n_chunk_nodes
     int priv_cfg = 1;
     int priv_grid_ext[4] = {0, 0, 0, 0};  // persistent grid per (pressure, SUPG) instance
@@ -179,7 +182,7 @@ struct tal_handle {
         free_peers();
         void *ptrs[] = {nodebuf, staging, perm, iperm, conn, conn_col, d_blobs, d_blob_off,
                         d_bnd_nodes, d_bnd_off, d_bnd_pos, d_partial, d_press, d_seq_off, d_seq_ent, d_seq_dlt, d_seq_rows,
-                        d_cg, d_cc};
+                        d_blobs_cl, d_xc};
         for (void *p : ptrs)
             if (p)
                 cudaFree(p);
@@ -199,7 +202,9 @@ struct tal_handle {
         }
         async_next = 0;
         perm = iperm = d_blob_off = d_bnd_nodes = d_bnd_off = d_bnd_pos = nullptr;
-        d_cg = d_cc = nullptr;
+        d_blobs_cl = nullptr;
+        d_xc = nullptr;
+        blob_bytes = 0;
         conn = conn_col = nullptr;
         d_blobs = nullptr;
         col_off.clear();
@@ -708,7 +713,7 @@ int launch_shape(tal_handle *h, const tal_params *p, int variant, int scatter, c
 // first use from the host chunk tables and the node permutation
 int build_caller_ids(tal_handle *h)
 {
-    if (h->d_cg || h->ch.gather_nodes.empty())
+    if (h->d_blobs_cl || h->ch.gather_nodes.empty())
         return TAL_OK;
     const int64_t n = (int64_t)h->ch.gather_nodes.size();
     std::vector<int32_t> perm;
@@ -725,9 +730,33 @@ int build_caller_ids(tal_handle *h)
             cc[i] = perm.empty() ? c : perm[c];
         }
     });
-    if (int rc = dev_upload(&h->d_cg, cg.data(), cg.size()))
-        return rc;
-    return dev_upload(&h->d_cc, cc.data(), cc.size());
+    int32_t *d_cg = nullptr, *d_cc = nullptr;
+    int rc = dev_upload(&d_cg, cg.data(), cg.size());
+    if (!rc)
+        rc = dev_upload(&d_cc, cc.data(), cc.size());
+    cudaError_t e = cudaSuccess;
+    if (!rc && ((e = cudaMalloc((void **)&h->d_blobs_cl, (size_t)h->blob_bytes)) != cudaSuccess ||
+                (e = cudaMalloc((void **)&h->d_xc, sizeof(double) * 3 * h->N)) != cudaSuccess ||
+                (e = cudaMemcpyAsync(h->d_blobs_cl, h->d_blobs, (size_t)h->blob_bytes, cudaMemcpyDeviceToDevice,
+                                     h->stream)) != cudaSuccess))
+        rc = fail(TAL_ECUDA, std::string("caller-layout tables: ") + cudaGetErrorString(e));
+    if (!rc) {
+        const unsigned nc = (unsigned)h->info.n_chunks;
+        if (h->priv_cfg == 0)
+            k_cl_blobs<0><<<nc, PrivCfg<0>::THREADS, 0, h->stream>>>(h->d_blobs_cl, h->d_blob_off, d_cg, d_cc);
+        else if (h->priv_cfg == 1)
+            k_cl_blobs<1><<<nc, PrivCfg<1>::THREADS, 0, h->stream>>>(h->d_blobs_cl, h->d_blob_off, d_cg, d_cc);
+        else
+            k_cl_blobs<2><<<nc, PrivCfg<2>::THREADS, 0, h->stream>>>(h->d_blobs_cl, h->d_blob_off, d_cg, d_cc);
+        k_caller_coords<<<grid_for(h->N, 256), 256, 0, h->stream>>>(h->REC(), h->perm, h->N, h->d_xc);
+        if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(h->stream)) != cudaSuccess)
+            rc = fail(TAL_ECUDA, std::string("caller-layout tables: ") + cudaGetErrorString(e));
+    }
+    if (d_cg)
+        cudaFree(d_cg);
+    if (d_cc)
+        cudaFree(d_cc);
+    return rc;
 }
 
 // One assembly from and to the caller's device arrays: the fused caller-layout
@@ -766,8 +795,8 @@ int launch_caller(tal_handle *h, const tal_params *p, int scatter, const double 
     int64_t nl = 0;
     if (!ordered)  // shared nodes are REDed into it: zero the caller's rhs first
         TAL_CK(cudaMemsetAsync(d_rhs, 0, sizeof(double) * 3 * h->N, s));
-    PrivArgs pa{h->d_blobs, h->d_blob_off, (int)h->info.n_chunks, ordered ? h->d_partial : nullptr, nullptr,
-                h->d_cg, h->d_cc, d_u, d_rhs};
+    PrivArgs pa{h->d_blobs_cl, h->d_blob_off, (int)h->info.n_chunks, ordered ? h->d_partial : nullptr, nullptr,
+                h->d_xc, d_u, d_rhs};
     RhsSoA rhs{h->RX(), h->RY(), h->RZ()};
     const unsigned grid = (unsigned)std::min<int64_t>(h->priv_grid_ext[0], h->info.n_chunks);
     pm.begin();
@@ -1418,6 +1447,7 @@ int tal_upload_mesh_ex(tal_handle *h, const double *coords, const int64_t *conn,
     const Chunking &C = h->ch;
     if ((rc = dev_upload(&h->d_blobs, blobs.data(), blobs.size())))
         return rc;
+    h->blob_bytes = (int64_t)blobs.size();
     if ((rc = dev_upload(&h->d_blob_off, blob_off.data(), blob_off.size())))
         return rc;
     if ((rc = dev_upload(&h->d_bnd_nodes, C.bnd_nodes.data(), C.bnd_nodes.size())))

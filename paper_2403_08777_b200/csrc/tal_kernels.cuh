@@ -309,10 +309,10 @@ struct PrivArgs {
     double *part;          // ordered-merge partials, AoS (x,y,z) per chunk-node entry node_begin + j
     const double *press;   // nodal pressures, internal order (PR instances)
     // caller layout (CL instances): u and rhs are the caller's (N,3) AoS
-    // arrays in its own node numbering; caller ids of the chunk-node entries
-    // in gather order (cg) and in rank order (cc), indexed node_begin + j
-    const int32_t *__restrict__ cg;
-    const int32_t *__restrict__ cc;
+    // arrays in its own node numbering; the CL blobs hold caller node ids in
+    // their gather and rank lists (k_cl_blobs), coordinates come from the
+    // caller-order copy xc -- no global index loads inside the kernel
+    const double *__restrict__ xc;
     const double *__restrict__ u_caller;
     double *rhs_caller;
 };
@@ -358,20 +358,29 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
         const int32_t *gl = reinterpret_cast<const int32_t *>(bl + 16 + L::TABLES + 2 * BLOB_LEVELS);
         double *dst = nrec_s;
         if constexpr (CL) {
-            // x,y (16 B) + z (8 B) of the resident record, then the caller's
-            // u as three 8-B copies (a (N,3) row is only 8-B aligned)
+            // two segments per node (lane-consecutive): the coordinates from
+            // the caller-order copy (16 + 8 B when the 24-B row is 16-B aligned,
+            // else 3 x 8 B) and the caller's u (3 x 8 B: its record slot at
+            // +24 B is only 8-B aligned)
             for (int q = tid; q < 2 * hdr.y; q += T) {
                 const int j = q >> 1;
-                const double *src = nrec_g + 6 * (int64_t)gl[j];
-                if (q & 1)
-                    cp_async8(dst + 6 * j + 2, src + 2);
-                else
-                    cp_async16(dst + 6 * j, src);
-            }
-            const int32_t *cg = pa.cg + hdr.z;
-            for (int q = tid; q < 3 * hdr.y; q += T) {
-                const int j = q / 3, c = q - 3 * j;
-                cp_async8(dst + 6 * j + 3 + c, pa.u_caller + 3 * (int64_t)__ldg(cg + j) + c);
+                const int64_t g = gl[j];
+                double *d = dst + 6 * j;
+                if (q & 1) {
+                    const double *us = pa.u_caller + 3 * g;
+                    cp_async8(d + 3, us);
+                    cp_async8(d + 4, us + 1);
+                    cp_async8(d + 5, us + 2);
+                } else {
+                    const double *xs = pa.xc + 3 * g;
+                    if (g & 1) {
+                        cp_async8(d, xs);
+                        cp_async8(d + 1, xs + 1);
+                    } else {
+                        cp_async16(d, xs);
+                    }
+                    cp_async8(d + 2, xs + 2);
+                }
             }
             cp_async_commit();
             return;
@@ -568,7 +577,7 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
             const int raw = cn[q];
             const int v = raw & 0x7fffffff;
             if constexpr (CL) {
-                double *r = pa.rhs_caller + 3 * (int64_t)__ldg(pa.cc + hdr.z + q);
+                double *r = pa.rhs_caller + 3 * (int64_t)v;  // CL blobs: caller id
                 if (raw < 0) {
                     r[0] = ax;
                     r[1] = ay;
@@ -611,6 +620,39 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
             }
         }
     }
+}
+
+// caller-layout blobs (tal_run_caller): a copy of the chunk blobs whose
+// gather list and rank-ordered node list hold caller node ids (cg / cc,
+// indexed node_begin + j) instead of internal ones, interior bit kept
+template <int CFG>
+__global__ void __launch_bounds__(PrivCfg<CFG>::THREADS) k_cl_blobs(uint8_t *__restrict__ blobs,
+                                                                    const int32_t *__restrict__ blob_off,
+                                                                    const int32_t *__restrict__ cg,
+                                                                    const int32_t *__restrict__ cc)
+{
+    using L = PrivLayoutOf<CFG>;
+    uint8_t *bl = blobs + (size_t)blob_off[blockIdx.x] * 16;
+    const int4 hdr = *reinterpret_cast<const int4 *>(bl);
+    int32_t *gl = reinterpret_cast<int32_t *>(bl + 16 + L::TABLES + 2 * BLOB_LEVELS);
+    int32_t *cn = reinterpret_cast<int32_t *>(bl + 16 + L::TABLES + 2 * BLOB_LEVELS + pad16(4 * hdr.y));
+    for (int j = threadIdx.x; j < hdr.y; j += blockDim.x) {
+        gl[j] = cg[hdr.z + j];
+        cn[j] = (int32_t)((uint32_t)cc[hdr.z + j] | ((uint32_t)cn[j] & 0x80000000u));
+    }
+}
+
+// caller-order coordinate copy for the caller-layout gather: xc[perm[i]] = rec[i]
+__global__ void __launch_bounds__(256) k_caller_coords(const double *__restrict__ rec,
+                                                       const int32_t *__restrict__ perm, int64_t n, double *xc)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    const int64_t c = perm ? (int64_t)perm[i] : i;
+    xc[3 * c + 0] = rec[6 * i + 0];
+    xc[3 * c + 1] = rec[6 * i + 1];
+    xc[3 * c + 2] = rec[6 * i + 2];
 }
 
 // ordered merge of chunk partials for nodes shared between chunks (and zero
