@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--permute", action="store_true", help="config 3: random node permutation")
+    ap.add_argument("--mesh", default="box",
+                    help="box (Kuhn box of --cells) | delaunay:NPOINTS (unstructured: the Delaunay "
+                         "tetrahedralisation of NPOINTS seeded random points; N=1 only)")
     ap.add_argument("--pressure", action="store_true",
                     help="add the P1 pressure-gradient term (extension; uniform [-1,1) nodal p, seed 2)")
     ap.add_argument("--supg", action="store_true",
@@ -361,6 +364,8 @@ def run_ours(a) -> None:
     gz = c * ws if a.scaling == "weak" else c  # global box: (c, c, gz)
     if gz < ws:
         raise SystemExit(f"bench.py: {gz} cell layers cannot be split over {ws} ranks")
+    if a.mesh != "box" and ws > 1:
+        raise SystemExit("bench.py: --mesh delaunay runs on one GPU (N=1)")
     t0 = time.perf_counter()
     gperm = None
     if ws > 1 and a.partition == "rcb":
@@ -378,6 +383,11 @@ def run_ours(a) -> None:
         dom = SlabDomain((c, c, gz), rank, ws, cfg)
         mesh, u = dom.mesh, dom.velocity(a.init)
         asm = dom.assembler
+    elif a.mesh.startswith("delaunay"):
+        dom = None
+        mesh = tb.generate_delaunay_mesh(int(a.mesh.partition(":")[2] or 2_000_000), seed=0)
+        u = tb.make_velocity(mesh, a.init)
+        asm = tb.Assembler(mesh, cfg, build_colors=(a.scatter == "colored"))
     else:
         dom = None
         mesh = tb.generate_box_mesh(c, c, c)
@@ -667,7 +677,7 @@ def run_ours(a) -> None:
         rhs_gpu, _ = asm.assemble(u, P, variant=a.variant)
         # bounded sample of the same workload on all host cores (the reference's
         # own numba path when importable); the oracle's vector is the checker
-        cpu_baseline = reference_cpu((c, c, c), a.init, 3, 0, budget_s=30.0)
+        cpu_baseline = None if a.mesh != "box" else reference_cpu((c, c, c), a.init, 3, 0, budget_s=30.0)
         ref = O.assemble_rsp(mesh.coords, mesh.connectivity, u, n_threads=O.default_threads())
         if press is not None:
             ref = ref + O.pressure_gradient(mesh.coords, mesh.connectivity, press)
@@ -698,7 +708,10 @@ def run_ours(a) -> None:
                       "gathered": f"owned rows of {ws} ranks vs single-domain oracle"}
     asm.profile(False)
 
-    if ws == 1:
+    if a.mesh.startswith("delaunay"):
+        workload = (f"unstructured: Delaunay of {mesh.n_nodes} random points in the unit cube "
+                    f"({mesh.n_elems} tets), {a.init}")
+    elif ws == 1:
         workload = f"{c}^3 Kuhn box, {a.init}"
     elif a.scaling == "weak":
         workload = f"{c}x{c}x{gz} Kuhn box, a {c}^3 slab per rank ({ws} ranks), {a.init}"
@@ -727,7 +740,8 @@ def run_ours(a) -> None:
         "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated Kuhn box mesh, seeded velocity)",
         "config": {"workload": workload, "n_elems": E_all, "n_elems_rank0": E, "n_nodes_rank0": Nn,
-                   "box_cells": [c, c, gz], "scatter": a.scatter,
+                   "box_cells": [c, c, gz] if a.mesh == "box" else None, "mesh": a.mesh,
+                   "scatter": a.scatter,
                    "renumber": a.renumber, "element_order": a.element_order,
                    "patches": a.patches, "cta_patches": a.cta_patches, "chunk_nodes": a.chunk_nodes,
                    "permuted": bool(a.permute), "variant": a.variant,

@@ -46,6 +46,7 @@ from .mesh import (
     Mesh,
     color_elements,
     generate_box_mesh,
+    generate_delaunay_mesh,
     permute_nodes,
     renumber_nodes,
     signed_volumes,

@@ -113,6 +113,27 @@ def generate_box_mesh(nx: int, ny: int, nz: int, extents=(1.0, 1.0, 1.0)) -> Mes
     return Mesh(coords=coords, connectivity=conn)
 
 
+def generate_delaunay_mesh(n_points: int, seed: int = 0) -> Mesh:
+    """Unstructured tetrahedral mesh of the unit cube: the Delaunay
+    tetrahedralisation (scipy.spatial) of ``n_points`` uniform random points
+    (``default_rng(seed)``), every element oriented positively (last two nodes
+    swapped where the volume is negative), zero-volume slivers dropped.  A
+    synthetic stand-in for the general meshes the reference's Mesh accepts:
+    irregular valences, open and closed edge rings of every size, ~6.7 tets
+    per node.  Host-side input preparation (scipy needed)."""
+    from scipy.spatial import Delaunay
+    if n_points < 4:
+        raise ValueError(f"n_points must be >= 4, got {n_points}")
+    pts = np.random.default_rng(seed).random((int(n_points), 3))
+    conn = np.ascontiguousarray(Delaunay(pts).simplices, dtype=np.int64)
+    x = pts[conn]
+    det = np.einsum("ij,ij->i", x[:, 1] - x[:, 0], np.cross(x[:, 2] - x[:, 0], x[:, 3] - x[:, 0]))
+    neg = det < 0.0
+    conn[neg, 2], conn[neg, 3] = conn[neg, 3].copy(), conn[neg, 2].copy()
+    conn = np.ascontiguousarray(conn[det != 0.0])
+    return Mesh(coords=pts, connectivity=conn)
+
+
 def color_elements(mesh) -> Mesh:
     """Greedy lowest-free colouring in element order (mesh.py:235-257)."""
     conn = np.ascontiguousarray(mesh.connectivity, dtype=np.int64)

@@ -273,3 +273,16 @@ def test_bank_aware_record_placement_reduces_conflicts():
     assert after / groups < 1.6 < before / groups
     # contribution stores (half-warp STS.64 groups): levels / equal-count ranks
     assert sgroups <= safter < sbefore
+
+
+def test_delaunay_mesh_generator():
+    """The unstructured synthetic mesh: deterministic per seed, every element
+    positively oriented, irregular edge rings (open and closed) for the
+    patch builder."""
+    a = tb.generate_delaunay_mesh(3000, seed=1)
+    b = tb.generate_delaunay_mesh(3000, seed=1)
+    assert np.array_equal(a.connectivity, b.connectivity)
+    assert (tb.signed_volumes(a.coords, a.connectivity) > 0).all()
+    assert 5.0 < a.n_elems / a.n_nodes < 7.5
+    rings = {len(r) for _, _, r, _ in tb.mesh.edge_star_patches(a)}
+    assert len(rings) >= 4
