@@ -1113,19 +1113,33 @@ void pos_stats(int64_t *groups, int64_t *before, int64_t *after)
     *groups = g_pos.groups, *before = g_pos.wave_before, *after = g_pos.wave_after;
 }
 
-bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_nodes, int max_contrib,
+namespace {
+// patches of a chunk ordered by ring length (TAL_RING_SORT=0: as built)
+int ring_sort_mode()
+{
+    static int mode = [] {
+        const char *e = std::getenv("TAL_RING_SORT");
+        return e ? std::atoi(e) : 1;
+    }();
+    return mode;
+}
+}  // namespace
+
+bool build_chunks(const Patches &P_in, int64_t n_nodes, int max_patches, int max_nodes, int max_contrib,
                   const uint8_t *external, Chunking &out, std::string &err)
 {
+    const Patches *pp = &P_in;
     if (max_patches < 1 || max_nodes < PATCH_MAX_RING + 2 || max_contrib < PATCH_MAX_RING + 2 ||
         max_contrib > 65535 || max_nodes > 65535) {
         err = "invalid chunk limits";
         return false;
     }
+    const Patches &P0 = P_in;
     out = Chunking();
     out.max_patches = max_patches;
     out.max_nodes = max_nodes;
     out.max_contrib = max_contrib;
-    const int64_t np = P.n_patches();
+    const int64_t np = P0.n_patches();
     out.pids.assign((size_t)np * PATCH_SLOTS, 0);
     out.ppos.assign((size_t)np * PATCH_SLOTS, 0);
 
@@ -1150,15 +1164,15 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
             contrib = 0;
         };
         for (int64_t g = 0; g < np; ++g) {
-            const int32_t n = P.off[g + 1] - P.off[g];
+            const int32_t n = P0.off[g + 1] - P0.off[g];
             if (n - 2 > PATCH_MAX_RING || n < 4) {
                 err = "patch ring size out of range";
                 return false;
             }
             int fresh = 0;
             bool full_level = false;
-            for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
-                const int32_t v = P.nodes[k];
+            for (int32_t k = P0.off[g]; k < P0.off[g + 1]; ++k) {
+                const int32_t v = P0.nodes[k];
                 if (stamp[v] != chunk)
                     ++fresh;
                 else if (cnt[v] + 1 > CHUNK_LEVELS)
@@ -1167,8 +1181,8 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
             if (g > p_begin && ((g - p_begin) + 1 > max_patches || (int64_t)nodes.size() + fresh > max_nodes ||
                                 contrib + n > max_contrib || full_level))
                 close(g);
-            for (int32_t k = P.off[g]; k < P.off[g + 1]; ++k) {
-                const int32_t v = P.nodes[k];
+            for (int32_t k = P0.off[g]; k < P0.off[g + 1]; ++k) {
+                const int32_t v = P0.nodes[k];
                 if (stamp[v] != chunk) {
                     stamp[v] = chunk;
                     nodes.push_back(v);
@@ -1182,6 +1196,39 @@ bool build_chunks(const Patches &P, int64_t n_nodes, int max_patches, int max_no
     }
     lap("pass1");
     const int64_t n_chunks = (int64_t)spans.size();
+    // Within every chunk, patches by tet count, descending (stable): thread
+    // = patch, so a warp's lanes then walk rings of equal length.  On a Kuhn
+    // box every interior ring has 6 tets and this changes little; on an
+    // unstructured mesh (rings of 1-8 tets) it keeps the ring loop's SIMT
+    // lanes busy instead of idling behind the longest ring of the warp.
+    Patches sorted_p;
+    if (ring_sort_mode()) {
+        std::vector<int32_t> ord((size_t)np);
+        for (int64_t g = 0; g < np; ++g)
+            ord[g] = (int32_t)g;
+        auto tets = [&](int32_t g) {
+            const int32_t m = P0.off[g + 1] - P0.off[g] - 2;
+            return P0.closed[g] ? m : m - 1;
+        };
+        parallel_items(n_chunks, [&](int64_t c, int) {
+            std::stable_sort(ord.begin() + spans[c].p0, ord.begin() + spans[c].p1,
+                             [&](int32_t x, int32_t y) { return tets(x) > tets(y); });
+        }, 64);
+        sorted_p.off.assign((size_t)np + 1, 0);
+        sorted_p.closed.resize((size_t)np);
+        for (int64_t g = 0; g < np; ++g) {
+            sorted_p.off[g + 1] = sorted_p.off[g] + (P0.off[ord[g] + 1] - P0.off[ord[g]]);
+            sorted_p.closed[g] = P0.closed[ord[g]];
+        }
+        sorted_p.nodes.resize(P0.nodes.size());
+        parallel_for(np, [&](int64_t g0, int64_t g1, int) {
+            for (int64_t g = g0; g < g1; ++g)
+                std::copy(P0.nodes.begin() + P0.off[ord[g]], P0.nodes.begin() + P0.off[ord[g] + 1],
+                          sorted_p.nodes.begin() + sorted_p.off[g]);
+        });
+        pp = &sorted_p;
+    }
+    const Patches &P = *pp;
     std::vector<int64_t> nbeg((size_t)n_chunks + 1, 0);
     for (int64_t c = 0; c < n_chunks; ++c)
         nbeg[c + 1] = nbeg[c] + spans[c].nn;

@@ -167,19 +167,19 @@ def test_parallel_prep_reproduces_serial_layouts():
     greedy with serial fix-up, per-chunk parallel placement) yields the
     serial code's layouts bit for bit: SHA-256 of blobs / offsets / node
     permutation over 29 (mesh x option) cases, recorded by the serial
-    round-1 code (tools/layout_digest.py)."""
-    import json
+    round-1 code (tools/layout_digest.py), reproduced with the round-2
+    within-chunk ring-length sort switched off (TAL_RING_SORT=0) at the
+    default and at 3 threads; with the sort on (the default) the layouts
+    match their own record at both thread counts."""
     import subprocess
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parent.parent
-    sys.path.insert(0, str(root / "tools"))
-    import layout_digest as LD
-    want = json.loads((root / "tests" / "golden" / "layout_digests.json").read_text())
-    got = LD.compute()
-    assert got == want
-    # and independent of the thread count
-    env = {**__import__("os").environ, "TAL_PREP_THREADS": "3"}
-    r = subprocess.run([sys.executable, str(root / "tools" / "layout_digest.py")], env=env,
-                       capture_output=True, text=True, check=True)
-    assert "mismatch: none" in r.stdout
+    for ring_sort in ("0", "1"):
+        for threads in (None, "3"):
+            env = {**__import__("os").environ, "TAL_RING_SORT": ring_sort}
+            if threads:
+                env["TAL_PREP_THREADS"] = threads
+            r = subprocess.run([sys.executable, str(root / "tools" / "layout_digest.py")], env=env,
+                               capture_output=True, text=True, check=True)
+            assert "mismatch: none" in r.stdout, (ring_sort, threads, r.stdout)

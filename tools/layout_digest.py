@@ -18,7 +18,13 @@ sys.path.insert(0, str(ROOT))
 import paper_2403_08777_b200 as tb  # noqa: E402
 from paper_2403_08777_b200.mesh import plan_blobs  # noqa: E402
 
-OUT = ROOT / "tests" / "golden" / "layout_digests.json"
+import os  # noqa: E402
+
+# TAL_RING_SORT=0 (patches in build order inside each chunk) is the layout the
+# round-1 serial code wrote; the default sorts each chunk's patches by ring
+# length and has its own record
+OUT = ROOT / "tests" / "golden" / ("layout_digests.json" if os.environ.get("TAL_RING_SORT") == "0"
+                                   else "layout_digests_ringsort.json")
 
 
 def cases():
