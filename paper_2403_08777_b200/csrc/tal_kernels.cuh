@@ -764,15 +764,26 @@ __global__ void k_peer_signal(unsigned long long *f0, unsigned long long *f1, in
         atomicAdd_system(f1 + which, 1ull);
 }
 
+// A neighbour that never signals (its process died, a mismatched step count)
+// must not hang the GPU: after TAL_PEER_WAIT_NS of waiting the kernel traps,
+// so the step fails with a launch error instead of spinning forever.
+#ifndef TAL_PEER_WAIT_NS
+#define TAL_PEER_WAIT_NS 30000000000ull  // 30 s
+#endif
 __global__ void k_peer_wait(const unsigned long long *flags, int which, int n_peers)
 {
     const unsigned long long target = flags[2] * (unsigned long long)n_peers;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
-        unsigned long long v;
+        unsigned long long v, t;
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + which) : "memory");
         if (v >= target)
             break;
         __nanosleep(256);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > TAL_PEER_WAIT_NS)
+            __trap();
     }
     __threadfence_system();
 }
