@@ -446,7 +446,6 @@ __global__ void __launch_bounds__(PrivCfg<CFG>::THREADS,
         if (tid < hdr.x) {
             const uint16_t *ids = reinterpret_cast<const uint16_t *>(bl + 16) + tid;
             const uint16_t *pos = ids + SLOTS * T;
-
 #define ID(s) ids[(s) * T]
 #define POS(s) pos[(s) * T]
             const int m = ID(0) & 0xff;
