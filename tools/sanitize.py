@@ -41,6 +41,11 @@ if "big" not in sys.argv:  # round 2 paths: SUPG, caller layout, seam subsets
     ids2 = np.arange(5, m.n_elems // 2, dtype=np.int64)
     tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids2, rhs)
     tb.assemble_elements(m.coords, m.connectivity, u, 1.0, 1e-3, 0.07, pm, ids2[::3].copy(), rhs)
+if "big" not in sys.argv:  # an unstructured mesh: open arcs, 1..8-tet rings, ring-sorted chunks
+    md = tb.generate_delaunay_mesh(3000, seed=2)
+    ud = tb.make_velocity(md, "random:4")
+    for mode in ("private", "private-atomic", "atomic"):
+        tb.assemble_rsp(md, ud, P, tb.RunConfig(scatter=mode))
 for fn in () if "big" in sys.argv else (tb.assemble_baseline, tb.assemble_rs):
     fn(m, u, P, tb.RunConfig(scatter="atomic"))
 asm = tb.Assembler(m, tb.RunConfig(scatter="private-atomic", cta_patches=64, chunk_nodes=144))
