@@ -136,3 +136,17 @@ def test_supg_with_pressure_and_graph_replay(oracle):
     got = asm.get_rhs_host()
     _check(oracle, got, _ref(oracle, m, u), m, u)
     asm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scatter", ["private", "private-atomic", "atomic"])
+def test_supg_and_pressure_on_an_unstructured_mesh(oracle, scatter):
+    """Both f4 extensions on a Delaunay mesh (irregular rings, open arcs,
+    ring-sorted chunks): SUPG and the pressure term together against the
+    sum of their oracles."""
+    m = tb.generate_delaunay_mesh(6000, seed=8)
+    u = tb.make_velocity(m, "random:3")
+    p = np.random.default_rng(6).uniform(-1.0, 1.0, m.n_nodes)
+    res = tb.assemble_rsp(m, u, P, tb.RunConfig(scatter=scatter), pressure=p, stabilization=True)
+    ref = _ref(oracle, m, u) + oracle.pressure_gradient(m.coords, m.connectivity, p)
+    _check(oracle, res.rhs, ref, m, u)
